@@ -1,0 +1,391 @@
+/*
+ * ljmd_oracle.c -- CPU ORACLE for the Lennard-Jones PairLoop hot path of
+ * arXiv 1704.03329 (PPMD).  TEST INFRASTRUCTURE ONLY: only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load this library.  It shares no code, header, table or constant
+ * generator with the CUDA path in paper_1704_03329_b200/csrc/.
+ *
+ * Plain, slow, obviously-correct fp64 C.  Compiled with -O2 -ffp-contract=off
+ * so that every a*b+c below is two roundings, exactly as written.
+ *
+ * Citations: P:n = PAPER.md line n.  Readings R1..R17 are listed in DESIGN.md.
+ *
+ *   O1 wrap              : periodic box [0,L) (reading R10)
+ *   O2 pair displacement : minimum image, canonical r^2 (reading R9)
+ *   O3 brute neighbours  : Def. 3 Local Particle Pair Loop at rbar_c
+ *   O4 cell neighbours   : cell method of Sec. 3.4, independent
+ *   O5 forces / energies : Eq. eqn:LJpotential, Eq. eqn:LJforce
+ *                          (P:969-978), Listing lst:LJ-kernel
+ *                          with the Eq. sign (reading R1) and PE = 1/2 sum
+ *                          over ordered pairs (reading R2)
+ *   O6 velocity Verlet   : Algorithm alg:VelocityVerlet, Listings
+ *                          lst:position_update / lst:velocity_update
+ *                          (P:659-675), Tab. access_descriptors
+ *   O7 rebuild schedule  : IntegratorRange, every Ns = 20 steps
+ *                          (P:728); optional displacement check (R7)
+ *
+ * Every function is pinned by a -m "not gpu" test (tests/test_oracle_*.py)
+ * against closed forms, golden fixtures or brute force; see DESIGN.md §Oracle.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ O1 -- */
+/* Wrap one coordinate into the half-open interval [0, L) (reading R10).
+ * Arbitrary input: x - L*floor(x/L), then fold the +-1 ulp artefacts. */
+static double wrap1(double x, double L)
+{
+    double k = floor(x / L);
+    double t = x - L * k;
+    if (t < 0.0) t = t + L;
+    if (t >= L) t = t - L;
+    return t;
+}
+
+/* Returns -1 on success, else the index of the first particle with a
+ * non-finite coordinate (nothing is modified in that case). */
+int64_t orc_wrap(int64_t n, double *pos, const double box[3])
+{
+    for (int64_t i = 0; i < n; ++i)
+        for (int d = 0; d < 3; ++d)
+            if (!isfinite(pos[3 * i + d])) return i;
+    for (int64_t i = 0; i < n; ++i)
+        for (int d = 0; d < 3; ++d)
+            pos[3 * i + d] = wrap1(pos[3 * i + d], box[d]);
+    return -1;
+}
+
+/* ------------------------------------------------------------------ O2 -- */
+/* Minimum-image displacement r_i - r_j (reading R9):
+ *   d0 = xi - xj;  s = +1 if d0 > L/2, -1 if d0 < -L/2, else 0;
+ *   dx = xi - (xj + s*L)          (one rounding for the image position) */
+void orc_displacement(const double *xi, const double *xj, const double box[3], double d[3])
+{
+    for (int k = 0; k < 3; ++k) {
+        double d0 = xi[k] - xj[k];
+        double half = 0.5 * box[k];
+        double s = 0.0;
+        if (d0 > half) s = 1.0;
+        else if (d0 < -half) s = -1.0;
+        double img = xj[k] + s * box[k];
+        d[k] = xi[k] - img;
+    }
+}
+
+/* r^2 = (dx*dx + dy*dy) + dz*dz, left to right, no contraction (R9). */
+double orc_r2(const double d[3])
+{
+    double a = d[0] * d[0];
+    double b = d[1] * d[1];
+    double c = d[2] * d[2];
+    return (a + b) + c;
+}
+
+/* ------------------------------------------------------------------ O3 -- */
+/* Brute-force neighbour sets NB(i) = { j != i : r^2(i,j) < rn^2 } (strict,
+ * reading R4), O(N^2), each NB(i) in ascending j.  Two-pass use: call with
+ * nbr == NULL to get offsets (size n+1) and the total; then with nbr. */
+int64_t orc_neigh_brute(int64_t n, const double *pos, const double box[3], double rn,
+                        int64_t *offsets, int64_t *nbr)
+{
+    double rn2 = rn * rn;
+    int64_t tot = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        offsets[i] = tot;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double d[3];
+            orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
+            if (orc_r2(d) < rn2) {
+                if (nbr) nbr[tot] = j;
+                ++tot;
+            }
+        }
+    }
+    offsets[n] = tot;
+    return tot;
+}
+
+/* ------------------------------------------------------------------ O4 -- */
+/* Cell-list neighbour sets, Sec. 3.4: cells of side
+ * Lambda >= rbar_c; n_c = floor(L / (rn*(1+1e-12))) >= 3, w = L/n_c,
+ * cell = min(floor(x/w), n_c-1); scan the 27 periodic neighbour cells.
+ * Input positions must already be wrapped into [0,L).  Returns the total
+ * number of (i,j) entries, or -1 if a dimension has fewer than 3 cells.
+ * Each NB(i) is returned in ascending j (reading R15). */
+static int cmp_i64(const void *a, const void *b)
+{
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return (x > y) - (x < y);
+}
+
+int orc_cell_dims(const double box[3], double rn, int64_t nc[3])
+{
+    for (int d = 0; d < 3; ++d) {
+        nc[d] = (int64_t)floor(box[d] / (rn * (1.0 + 1e-12)));
+        if (nc[d] < 3) return -1;
+    }
+    return 0;
+}
+
+int64_t orc_neigh_cells(int64_t n, const double *pos, const double box[3], double rn,
+                        int64_t *offsets, int64_t *nbr)
+{
+    int64_t nc[3];
+    if (orc_cell_dims(box, rn, nc) != 0) return -1;
+    double w[3] = {box[0] / (double)nc[0], box[1] / (double)nc[1], box[2] / (double)nc[2]};
+    int64_t ncell = nc[0] * nc[1] * nc[2];
+    /* linked-list cells (Rapaport), head[c] -> next[i] */
+    int64_t *head = (int64_t *)malloc(sizeof(int64_t) * ncell);
+    int64_t *next = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    int64_t *cid = (int64_t *)malloc(sizeof(int64_t) * 3 * (n > 0 ? n : 1));
+    for (int64_t c = 0; c < ncell; ++c) head[c] = -1;
+    for (int64_t i = n - 1; i >= 0; --i) {
+        int64_t c3[3];
+        for (int d = 0; d < 3; ++d) {
+            int64_t c = (int64_t)floor(pos[3 * i + d] / w[d]);
+            if (c < 0) c = 0;
+            if (c > nc[d] - 1) c = nc[d] - 1;
+            c3[d] = c;
+            cid[3 * i + d] = c;
+        }
+        int64_t c = (c3[2] * nc[1] + c3[1]) * nc[0] + c3[0];
+        next[i] = head[c];
+        head[c] = i;
+    }
+    double rn2 = rn * rn;
+    int64_t tot = 0;
+    int64_t *scratch = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        offsets[i] = tot;
+        int64_t cnt = 0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int64_t cx = (cid[3 * i + 0] + dx + nc[0]) % nc[0];
+                    int64_t cy = (cid[3 * i + 1] + dy + nc[1]) % nc[1];
+                    int64_t cz = (cid[3 * i + 2] + dz + nc[2]) % nc[2];
+                    int64_t c = (cz * nc[1] + cy) * nc[0] + cx;
+                    for (int64_t j = head[c]; j >= 0; j = next[j]) {
+                        if (j == i) continue;
+                        double d[3];
+                        orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
+                        if (orc_r2(d) < rn2) scratch[cnt++] = j;
+                    }
+                }
+        qsort(scratch, (size_t)cnt, sizeof(int64_t), cmp_i64);
+        if (nbr)
+            for (int64_t k = 0; k < cnt; ++k) nbr[tot + k] = scratch[k];
+        tot += cnt;
+    }
+    offsets[n] = tot;
+    free(scratch);
+    free(cid);
+    free(next);
+    free(head);
+    return tot;
+}
+
+/* ------------------------------------------------------------------ O5 -- */
+typedef struct {
+    double rc;      /* force cutoff r_c (Tab. 7.2T1: 2.5)                      */
+    double eps;     /* epsilon                                                 */
+    double sigma;   /* sigma                                                   */
+    double shift;   /* s in 4 eps [(sigma/r)^12 - (sigma/r)^6 + s]; 1/4 in the
+                       paper's Eq. eqn:LJpotential, reading R3          */
+} orc_lj;
+
+/* One ordered pair, Listing lst:LJ-kernel with
+ * C_F = +48 eps / sigma^2 (Eq. eqn:LJforce, reading R1), C_V = 4 eps.
+ * Contributions are added only if r^2 < r_c^2 (strict, reading R4). */
+static void pair_accumulate(const double d[3], const orc_lj *lj, double *Fi, double *Ui,
+                            double *Si, double *Ai)
+{
+    double rc_sq = lj->rc * lj->rc;
+    double sigma2 = lj->sigma * lj->sigma;
+    double CV = 4.0 * lj->eps;
+    double CF = 48.0 * lj->eps / sigma2;
+    double dr_sq = orc_r2(d);
+    if (!(dr_sq < rc_sq)) return;
+    double r_m2 = sigma2 / dr_sq;
+    double r_m4 = r_m2 * r_m2;
+    double r_m6 = r_m4 * r_m2;
+    double r_m8 = r_m4 * r_m4;
+    double u = CV * ((r_m6 - 1.0) * r_m6 + lj->shift);
+    double f_tmp = CF * (r_m6 - 0.5) * r_m8;
+    Fi[0] += f_tmp * d[0];
+    Fi[1] += f_tmp * d[1];
+    Fi[2] += f_tmp * d[2];
+    *Ui += u;
+    *Si += fabs(f_tmp) * sqrt(dr_sq);
+    *Ai += fabs(u);
+}
+
+/* Neumaier-compensated sum (used for global PE and KE). */
+double orc_sum(const double *x, int64_t n)
+{
+    double s = 0.0, c = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double t = s + x[i];
+        if (fabs(s) >= fabs(x[i])) c += (s - t) + x[i];
+        else c += (x[i] - t) + s;
+        s = t;
+    }
+    return s + c;
+}
+
+/* F[n][3] (INC_ZERO: zeroed first, reading R5), e[n] = 1/2 sum_j V (R2),
+ * S[n] = sum_j |f_ij| (tolerance scale, reading R16), A[n] = sum_j |V_ij|.
+ * Any of e/S/A may be NULL.  If offsets == NULL: brute force over all j in
+ * ascending order; else over NB(i) = nbr[offsets[i]..offsets[i+1]).
+ * Returns PE = sum_i e_i (Neumaier). */
+double orc_forces(int64_t n, const double *pos, const double box[3], const orc_lj *lj,
+                  const int64_t *offsets, const int64_t *nbr,
+                  double *F, double *e, double *S, double *A)
+{
+    double *etmp = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        double Fi[3] = {0.0, 0.0, 0.0}, Ui = 0.0, Si = 0.0, Ai = 0.0;
+        if (offsets == NULL) {
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i) continue;
+                double d[3];
+                orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
+                pair_accumulate(d, lj, Fi, &Ui, &Si, &Ai);
+            }
+        } else {
+            for (int64_t k = offsets[i]; k < offsets[i + 1]; ++k) {
+                double d[3];
+                orc_displacement(pos + 3 * i, pos + 3 * nbr[k], box, d);
+                pair_accumulate(d, lj, Fi, &Ui, &Si, &Ai);
+            }
+        }
+        F[3 * i + 0] = Fi[0];
+        F[3 * i + 1] = Fi[1];
+        F[3 * i + 2] = Fi[2];
+        etmp[i] = 0.5 * Ui;
+        if (e) e[i] = etmp[i];
+        if (S) S[i] = Si;
+        if (A) A[i] = Ai;
+    }
+    double pe = orc_sum(etmp, n);
+    free(etmp);
+    return pe;
+}
+
+/* KE = 1/2 m sum_i |v_i|^2 (Example 1), Neumaier over particles. */
+double orc_kinetic(int64_t n, const double *vel, double mass)
+{
+    double *k = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        const double *v = vel + 3 * i;
+        k[i] = 0.5 * mass * ((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+    }
+    double ke = orc_sum(k, n);
+    free(k);
+    return ke;
+}
+
+/* ------------------------------------------------------------- O6 / O7 -- */
+typedef struct {
+    orc_lj lj;
+    double dt;            /* delta t                                           */
+    double mass;          /* scalar m (reading R11)                            */
+    double delta;         /* shell thickness delta = rbar_c - r_c  */
+    int64_t ns;           /* reuse count Ns (20)                        */
+    int64_t check;        /* 1: also rebuild when 2 max|x - x_build| > delta   */
+    int64_t mode;         /* 0: brute-force forces, 1: cell + neighbour list   */
+    int64_t energy_every; /* sample PE/KE every k steps (10)            */
+} orc_params;
+
+typedef struct {
+    int64_t *off, *nbr;
+} orc_list;
+
+static int build_list(int64_t n, const double *pos, const double box[3], double rn, orc_list *L)
+{
+    free(L->off);
+    free(L->nbr);
+    L->off = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
+    int64_t tot = orc_neigh_cells(n, pos, box, rn, L->off, NULL);
+    if (tot < 0) return -1;
+    L->nbr = (int64_t *)malloc(sizeof(int64_t) * (tot > 0 ? tot : 1));
+    orc_neigh_cells(n, pos, box, rn, L->off, L->nbr);
+    return 0;
+}
+
+/* Velocity Verlet, Algorithm alg:VelocityVerlet:
+ *   init : wrap (O1), build list, F <- F(r0) (reading R6), sample 0
+ *   step : v += (dt/2m) F ; r += dt v          (line 6, Listing P:659-666)
+ *          rebuild if due: wrap + list (O7, after the drift, reading R8)
+ *          F <- INC_ZERO pair loop              (line 7)
+ *          v += (dt/2m) F                       (line 8, Listing P:671-675)
+ *          sample PE, KE every energy_every steps
+ * Positions are wrapped only when the cell/neighbour structure is rebuilt
+ * (Listing lst:position_update has no wrap; migration happens every n steps,
+ * P:436-438; reading R10).  In brute-force mode the same schedule decides
+ * when to wrap, so brute and list trajectories are bitwise identical while
+ * no pair enters r_c from beyond rbar_c between rebuilds.
+ *
+ * pe_hist/ke_hist: nsteps/energy_every + 1 entries.  rebuild_steps: the MD
+ * step index of each rebuild after init (cap entries).  Returns the number
+ * of rebuilds, or -1 on error (box too small for cells). */
+int64_t orc_run(int64_t n, double *pos, double *vel, const double box[3], const orc_params *p,
+                int64_t nsteps, double *F, double *pe_hist, double *ke_hist,
+                int64_t *rebuild_steps, int64_t rebuild_cap)
+{
+    double h = 0.5 * p->dt / p->mass;       /* dht_iMASS = dt/(2m) */
+    double rn = p->lj.rc + p->delta;
+    orc_list L = {NULL, NULL};
+    double *xb = (double *)malloc(sizeof(double) * 3 * (n > 0 ? n : 1));
+    int64_t nreb = 0;
+
+    orc_wrap(n, pos, box);
+    if (p->mode == 1 && build_list(n, pos, box, rn, &L) != 0) { free(xb); return -1; }
+    memcpy(xb, pos, sizeof(double) * 3 * n);
+    double pe = orc_forces(n, pos, box, &p->lj, p->mode == 1 ? L.off : NULL, L.nbr, F, NULL, NULL, NULL);
+    int64_t ks = 0;
+    if (pe_hist) pe_hist[ks] = pe;
+    if (ke_hist) ke_hist[ks] = orc_kinetic(n, vel, p->mass);
+    ++ks;
+    int64_t since = 0;
+    for (int64_t step = 1; step <= nsteps; ++step) {
+        for (int64_t i = 0; i < 3 * n; ++i) {
+            vel[i] = vel[i] + h * F[i];
+            pos[i] = pos[i] + p->dt * vel[i];
+        }
+        ++since;
+        int due = (since >= p->ns);
+        if (!due && p->check) {
+            double m = 0.0;
+            for (int64_t i = 0; i < n; ++i) {
+                double d[3] = {pos[3 * i] - xb[3 * i], pos[3 * i + 1] - xb[3 * i + 1],
+                               pos[3 * i + 2] - xb[3 * i + 2]};
+                double r2 = orc_r2(d);
+                if (r2 > m) m = r2;
+            }
+            due = (4.0 * m > p->delta * p->delta);
+        }
+        if (due) {
+            orc_wrap(n, pos, box);
+            if (p->mode == 1 && build_list(n, pos, box, rn, &L) != 0) { free(xb); return -1; }
+            memcpy(xb, pos, sizeof(double) * 3 * n);
+            if (rebuild_steps && nreb < rebuild_cap) rebuild_steps[nreb] = step;
+            ++nreb;
+            since = 0;
+        }
+        pe = orc_forces(n, pos, box, &p->lj, p->mode == 1 ? L.off : NULL, L.nbr, F, NULL, NULL, NULL);
+        for (int64_t i = 0; i < 3 * n; ++i) vel[i] = vel[i] + h * F[i];
+        if (p->energy_every > 0 && step % p->energy_every == 0) {
+            if (pe_hist) pe_hist[ks] = pe;
+            if (ke_hist) ke_hist[ks] = orc_kinetic(n, vel, p->mass);
+            ++ks;
+        }
+    }
+    free(L.off);
+    free(L.nbr);
+    free(xb);
+    return nreb;
+}
