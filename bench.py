@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""bench.py -- LJ particle-timesteps/s of the B200-native PairLoop engine (arXiv 1704.03329).
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on
+rank 0.  One bench "step" = one rebuild cycle of the paper's benchmark: Ns = 20 MD steps of
+velocity Verlet, i.e. one cell binning + neighbour-list build, 20 force
+evaluations (2 of them with PE, energy_every = 10) and the Verlet updates --
+every row of SURVEY.md §8(a).
+
+N = 1 workload: BASELINE.json configs[1] (C2: FCC 64^3 cells, N = 1,048,576, rho = 0.8442,
+rc = 2.5, rbar_c = 2.75, dt = 0.005, T0 = 1.44).  N > 1: weak scaling at 1,048,576 particles
+per GPU (64 x 64 x 64N cells, z-slabs).
+
+--impl reference: the CPU oracle (oracle/, the only other place this script executes it)
+timed on the box's host cores on the same config; each of its steps is one MD step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ljinputs as li  # noqa: E402
+
+MD_PER_STEP = li.NS           # one rebuild cycle
+METRIC = "LJ particle-timesteps/s"
+UNIT = "particle-timesteps/s"
+FLOPS_PER_CAND = 21.0         # Listing lst:LJ-kernel, force only
+FLOPS_PER_CAND_E = 26.0       # + potential energy
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def workload(n_gpus: int, name: str | None):
+    if name:
+        cfg = li.CONFIGS[name]
+    elif n_gpus == 1:
+        cfg = li.CONFIGS["C2"]
+    else:
+        cfg = li.weak_config(n_gpus)
+    return cfg
+
+
+def clocks_start(path):
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        f = open(path, "w")
+        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                             stdout=f, stderr=subprocess.DEVNULL)
+        return p, f
+    except Exception:
+        return None, None
+
+
+def clocks_stop(h, path, gpu_index):
+    p, f = h
+    if p is None:
+        return None
+    p.terminate()
+    try:
+        p.wait(timeout=5)
+    except Exception:
+        p.kill()
+    f.close()
+    sm, smax, reasons = [], 0.0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(path):
+        parts = [x.strip() for x in line.split(",")]
+        if len(parts) < 9:
+            continue
+        try:
+            if int(parts[0]) != gpu_index:
+                continue
+            sm.append(float(parts[1]))
+            smax = max(smax, float(parts[2]))
+        except ValueError:
+            continue
+        for k, v in zip(names, parts[5:9]):
+            if v.lower() == "active":
+                reasons.add(k)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+# ---------------------------------------------------------------------------------- oracle legs
+
+def oracle_cycle_rate(pos, vel, box, n_steps=2):
+    """Bounded oracle sample: init (wrap + cell/neighbour list + F) and n_steps list-mode VV
+    steps on one host core; extrapolated to one rebuild cycle (1 build + 20 steps)."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.run(pos, vel, box, 0, mode="list", energy_every=0)
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.run(pos, vel, box, n_steps, mode="list", energy_every=10)
+    t_run = time.perf_counter() - t0
+    t_step = max(t_run - t_init, 1e-9) / n_steps
+    cycle = t_init + MD_PER_STEP * t_step
+    return len(pos) * MD_PER_STEP / cycle, t_init, t_step
+
+
+def run_reference(args, cfg):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    pos, vel, box = cfg.build()
+    n = len(pos)
+    cores, model = cpu_info()
+    # warm-up: W MD steps (includes one init build)
+    oracle.run(pos, vel, box, max(args.warmup, 0), mode="list", energy_every=10)
+    t0 = time.perf_counter()
+    r = oracle.run(pos, vel, box, args.steps, mode="list", energy_every=10)
+    t = time.perf_counter() - t0
+    value = n * args.steps / t
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "md_steps_per_step": 1, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic FCC (ljinputs, seeded)",
+        "config": {"workload": cfg.name, "n_particles": n, "rho": li.RHO, "rc": li.RC,
+                   "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "dt": li.DT, "t0": cfg.t0},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{cfg.name}: oracle list-mode VV, {args.steps} MD steps in one call "
+                                   f"(init build + rebuilds every {li.NS}), 1 thread, {model}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "rebuilds": int(len(r.rebuild_steps)),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------- our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, help="C1..C5 (default: C2 at N=1, weak C2 per GPU at N>1)")
+    ap.add_argument("--check", type=int, default=0, help="1: displacement-checked rebuild (safe policy)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    cfg = workload(args.gpus, args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        raise SystemExit("multi-GPU slab decomposition not built in this revision")
+    torch.cuda.set_device(local)
+    from paper_1704_03329_b200 import LJMD, ljmd
+
+    pos, vel, box = cfg.build()
+    n = len(pos)
+    stream = torch.cuda.current_stream()
+    opts = ljmd.default_options(device=local, stream=stream.cuda_stream, profile=1,
+                                rebuild_check=args.check)
+    ctx = LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=opts)
+    for _ in range(args.warmup):
+        ctx.step(MD_PER_STEP)
+    torch.cuda.synchronize()
+    st0 = ctx.stats()
+    clk_path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv") if os.path.isdir(
+        os.path.join(ROOT, "gpurun_out")) else f"/tmp/ljmd_clocks_{os.getpid()}.csv"
+    clk = (None, None) if args.no_clocks else clocks_start(clk_path)
+    time.sleep(0.3 if clk[0] is not None else 0.0)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ctx.step(MD_PER_STEP)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clocks = clocks_stop(clk, clk_path, local) if clk[0] is not None else None
+    st1 = ctx.stats()
+    md_steps = args.steps * MD_PER_STEP
+    value = n * md_steps / (ms * 1e-3)
+
+    # dominant kernel: the force kernel (CUDA events around each launch on the same stream)
+    launches = st1["force_launches"] - st0["force_launches"]
+    f_ms = (st1["force_ms"] - st0["force_ms"]) / max(launches, 1)
+    cand = st1["total_neighbours"]
+    e_frac = 1.0 / 10.0
+    flops = cand * (FLOPS_PER_CAND * (1 - e_frac) + FLOPS_PER_CAND_E * e_frac)
+    achieved = flops / (f_ms * 1e-3) / 1e12
+    try:
+        peak = ljmd.measure_fp64_peak(local)
+        peak_src = "measured (DFMA-chain probe, ljmd_measure_fp64_peak)"
+    except Exception:
+        peak = 148 * 64 * 2 * 1.965e9 / 1e12
+        peak_src = "derived 148 SM x 64 FP64 lanes x 2 x 1.965 GHz"
+
+    # end to end through the public API with host buffers (pinned), per bench step:
+    # set_state (H2D pos+vel) + step(20) + positions readback (D2H) + energy readback
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(pos.copy()).pin_memory()
+        hv = torch.from_numpy(vel.copy()).pin_memory()
+        ho = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        k_e2e = max(2, min(args.steps, 10))
+        ctx.set_state_ptr(hp.data_ptr(), hv.data_ptr())
+        ctx.step(MD_PER_STEP)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k_e2e):
+            ctx.set_state_ptr(hp.data_ptr(), hv.data_ptr())
+            ctx.step(MD_PER_STEP)
+            ctx.positions_into_ptr(ho.data_ptr())
+            ctx.energy()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ms_e2e = max(e0.elapsed_time(e1), wall * 1e3)
+        e2e = {"value": n * MD_PER_STEP * k_e2e / (ms_e2e * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(2 * 24 * n), "d2h_bytes_per_step": int(24 * n + 16),
+               "steps": k_e2e}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        cores, model = cpu_info()
+        c2pos, c2vel, c2box = pos, vel, box
+        rate, t_init, t_step = oracle_cycle_rate(c2pos, c2vel, c2box, n_steps=2)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{cfg.name} (N={n}): oracle init build ({t_init:.1f} s) + 2 list-mode VV steps "
+                         f"({t_step:.2f} s/step) on 1 thread of {cores} ({model}); rate = N*20/(build+20*step)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "md_steps_per_step": MD_PER_STEP,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic FCC crystal (ljinputs: rho 0.8442, PCG64 seeds 87287/1704)",
+        "config": {"workload": cfg.name, "n_particles": n, "rho": li.RHO, "rc": li.RC,
+                   "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "energy_every": 10, "dt": li.DT,
+                   "t0": cfg.t0, "rebuild_policy": "safe" if args.check else "paper-fixed-20",
+                   "parallelism": f"z-slab x{world}",
+                   "l2": "working set > L2 (list %.0f MB + positions %.0f MB)" % (
+                       4 * cand / 1e6, 32 * (n + st1["n_ghost"]) / 1e6)},
+        "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
+        "roofline": {"bound": "alu", "kernel": "k_force (fp64 LJ pair loop)", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "flops_per_launch": flops, "avg_launch_ms": f_ms, "peak_source": peak_src,
+                     "flop_count": "Listing 9: 21 flops per list candidate (+5 with PE every 10th step)"},
+        "force_share": (st1["force_ms"] - st0["force_ms"]) / ms,
+        "neighbours_per_particle": cand / n,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

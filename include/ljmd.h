@@ -1,0 +1,168 @@
+/*
+ * ljmd.h -- C ABI of the B200-native Lennard-Jones PairLoop engine
+ * (hot path of arXiv 1704.03329, PPMD: cell binning, Verlet neighbour list
+ * within rbar_c = rc + delta, fp64 LJ force/energy, velocity-Verlet updates).
+ *
+ * The calls follow the paper's statement of the problem:
+ *   - State / Domain / PositionDat / ParticleDat (Sec. 3.1, PAPER.md:234-299,
+ *     Listing lst:state-example PAPER.md:385-402)      -> ljmd_init
+ *   - IntegratorRange(Ni, dt, v, Ns, delta) driving Algorithm
+ *     alg:VelocityVerlet   -> ljmd_step
+ *   - PairLoop of Listing lst:LJ-loop returning F and u
+ *                                                    -> ljmd_get_forces/energy
+ *
+ * Conventions (all calls):
+ *   - Return ljmd_status; LJMD_OK == 0.  The first error puts the context in
+ *     the error state: every later call except ljmd_last_error/ljmd_destroy
+ *     returns LJMD_E_STATE.  ljmd_last_error names the particle (global index,
+ *     "gid" = row in the caller's arrays) where one applies.
+ *   - Host arrays are owned by the caller, row-major [n][3] float64 in the
+ *     caller's particle order (gid = row).  They are copied in by ljmd_init /
+ *     ljmd_set_state and written by the getters; the library never keeps a
+ *     pointer to them.  The library owns all device memory, the CUDA stream it
+ *     creates (unless one is passed in ljmd_options.stream) and the NCCL
+ *     communicator, and releases them in ljmd_destroy.
+ *   - Periodic orthorhombic box [0,Lx) x [0,Ly) x [0,Lz) only (reading R10).
+ *   - Not thread-safe per context; one context per rank/GPU.
+ *   - No CPU fallback: every computation runs in the sm_100a kernels of
+ *     libljmd.so; a missing GPU returns LJMD_E_CUDA.
+ */
+#ifndef LJMD_H
+#define LJMD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ljmd_ctx ljmd_ctx;
+
+typedef enum {
+    LJMD_OK = 0,
+    LJMD_E_ARG = -1,       /* bad argument (NULL pointer, n <= 0, rc <= 0, ...)            */
+    LJMD_E_BOX = -2,       /* fewer than 3 cells of width >= rbar_c in some dimension       */
+    LJMD_E_NONFINITE = -3, /* non-finite position/velocity; message names the gid           */
+    LJMD_E_OVERLAP = -4,   /* two particles at r^2 == 0; message names both gids            */
+    LJMD_E_CAPACITY = -5,  /* device allocation for a regrown buffer failed                 */
+    LJMD_E_CUDA = -6,      /* CUDA runtime error / no device                                 */
+    LJMD_E_NCCL = -7,      /* NCCL error (nranks > 1)                                        */
+    LJMD_E_STATE = -8      /* context poisoned by an earlier error                           */
+} ljmd_status;
+
+/* Every field is 8 bytes wide so the struct has no padding (ctypes-friendly). */
+typedef struct {
+    double  delta;          /* shell thickness delta = rbar_c - rc; default 0.25 = 0.1 rc
+                               (Tab. 7.2T1)                      */
+    int64_t rebuild_every;  /* list reuse count Ns; default 20               */
+    int64_t rebuild_check;  /* 0: fixed Ns only (paper); 1: also rebuild when
+                               2 max_i |x_i - x_i(build)| > delta (reading R7)              */
+    double  mass;           /* scalar particle mass m; default 1 (reading R11)              */
+    double  energy_shift;   /* s in V = 4 eps[(sigma/r)^12 - (sigma/r)^6 + s]; default 0.25
+                               = the paper's Eq. eqn:LJpotential (R3)         */
+    int64_t energy_every;   /* sample PE/KE every k steps inside ljmd_step; default 10
+                               (PAPER.md:866); 0 disables in-loop sampling                  */
+    int64_t device;         /* CUDA device ordinal; -1 = current device (default)           */
+    int64_t nbr_capacity;   /* initial neighbour-list width K; 0 = automatic. Grown
+                               transparently (and the list rebuilt) on overflow             */
+    int64_t rank;           /* this rank in [0, nranks); default 0                          */
+    int64_t nranks;         /* number of z-slab ranks; 1 = single GPU (no NCCL)             */
+    const void* nccl_id;    /* nranks > 1: pointer to a 128-byte ncclUniqueId, identical on
+                               every rank (broadcast by the caller, e.g. torch.distributed) */
+    void*   stream;         /* cudaStream_t to launch on; NULL = library-created stream    */
+    int64_t profile;        /* 1: time every force launch with CUDA events (ljmd_get_stats) */
+} ljmd_options;
+
+typedef struct {
+    int64_t steps_done;        /* MD steps since init / set_state                           */
+    int64_t n_rebuilds;        /* cell + neighbour rebuilds after init                      */
+    int64_t n_owned;           /* particles owned by this rank                              */
+    int64_t n_ghost;           /* ghost (periodic image / halo) particles                   */
+    int64_t nbr_capacity;      /* current list width K                                      */
+    int64_t max_neighbours;    /* longest list at the last build                            */
+    int64_t total_neighbours;  /* sum of list lengths at the last build (this rank)         */
+    int64_t n_cells[3];        /* global cell grid                                          */
+    int64_t regrows;           /* capacity regrowths so far                                 */
+    int64_t force_launches;    /* force launches timed (profile = 1)                        */
+    double  force_ms;          /* summed CUDA-event time of those launches (profile = 1)    */
+    int64_t energy_samples;    /* samples available from ljmd_get_energy_history            */
+    int64_t kernel_launches;   /* kernels of this library launched since init               */
+} ljmd_stats;
+
+/* Fill *o with the defaults listed above. */
+ljmd_status ljmd_default_options(ljmd_options* o);
+
+/* Create a context: copies pos/vel ([n][3] fp64, host) to the device, wraps
+ * positions into the box (half-open, reading R10), bins them into cells of
+ * width >= rbar_c (Sec. 3.4), builds the neighbour list at
+ * rbar_c = rc + delta (Eq. eqn:extended_cutoff PAPER.md:406-408)
+ * and computes F(r0) (reading R6) plus PE/KE at step 0.
+ *   box     : [3] box lengths (Lx, Ly, Lz) > 0
+ *   rc      : force cutoff (> 0); epsilon, sigma > 0; dt > 0
+ *   opt     : NULL -> ljmd_default_options
+ * With nranks > 1 every rank passes the same global arrays and keeps the
+ * particles of its z-slab.  On failure *out is NULL and the message is
+ * available from ljmd_last_error(NULL). */
+ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double* vel,
+                      const double box[3], double rc, double epsilon, double sigma, double dt,
+                      const ljmd_options* opt);
+
+/* Replace positions and velocities (same n, box and parameters as init) and
+ * redo the init sequence (wrap, bin, list, F(r0), step-0 energies). */
+ljmd_status ljmd_set_state(ljmd_ctx* c, const double* pos, const double* vel);
+
+/* Advance nsteps velocity-Verlet steps (Alg. alg:VelocityVerlet lines 5-9):
+ * v += dt/(2m) F; r += dt v; [rebuild every Ns steps, after the drift, R8];
+ * F <- sum over the list of Eq. eqn:LJforce (INC_ZERO, R5); v += dt/(2m) F.
+ * PE and KE are sampled every energy_every steps.  On return x, v and F are
+ * synchronised at the final step (velocities at full step). */
+ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps);
+
+/* Readback in the caller's order ([n][3] / [n]; with nranks > 1 only rows of
+ * particles owned by this rank are written).  Positions are the raw device
+ * positions (wrapped at the last rebuild, R10) unless wrapped != 0. */
+ljmd_status ljmd_get_forces(ljmd_ctx* c, double* out);
+ljmd_status ljmd_get_positions(ljmd_ctx* c, double* out, int64_t wrapped);
+ljmd_status ljmd_get_velocities(ljmd_ctx* c, double* out);
+/* e_i = 1/2 sum_j V(r_ij) over the list, r_ij < rc (reading R2). */
+ljmd_status ljmd_get_particle_energy(ljmd_ctx* c, double* out);
+/* Global PE = sum_i e_i and KE = 1/2 m sum_i |v_i|^2 (Example 1)
+ * at the current state (deterministic fixed-order sums; summed over ranks). */
+ljmd_status ljmd_get_energy(ljmd_ctx* c, double* pe, double* ke);
+/* In-loop samples recorded by ljmd_step since init/set_state (index 0 = step 0).
+ * Writes min(cap, available) entries of pe/ke and *count = available. */
+ljmd_status ljmd_get_energy_history(ljmd_ctx* c, double* pe, double* ke, int64_t cap,
+                                    int64_t* count);
+/* The current Verlet list as gid pairs: offsets[n+1] (CSR over the caller's
+ * order; empty rows for particles not owned) and, if gids != NULL and
+ * cap >= offsets[n], the neighbour gids of each row in list order. */
+ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, int64_t cap);
+/* MD step index of each rebuild after init (min(cap, n_rebuilds) entries). */
+ljmd_status ljmd_get_rebuild_steps(ljmd_ctx* c, int64_t* out, int64_t cap, int64_t* count);
+ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s);
+
+/* Message of the last error of c (or of the last failed ljmd_init if c == NULL). */
+const char* ljmd_last_error(const ljmd_ctx* c);
+void ljmd_destroy(ljmd_ctx* c);
+
+/* Library version string, e.g. "ljmd 0.1 sm_100a". */
+const char* ljmd_version(void);
+
+/* Measurement utility (bench.py roofline denominator): FP64 FMA throughput of the
+ * device, from a DFMA-chain probe kernel timed with CUDA events (best of 5), in
+ * TFLOP/s (2 flops per FMA).  device = -1: current device. */
+ljmd_status ljmd_measure_fp64_peak(int64_t device, double* tflops);
+
+/* ---- host-side decomposition planning (pure host code, no GPU needed) ----
+ * Cell grid of Sec. 3.4: n_d = floor(L_d / (rbar_c (1 + 1e-12))) (>= 3 required)
+ * and the z-slab split used for nranks > 1 (slab boundaries on global cell
+ * planes; the first (ncz mod nranks) ranks get one extra plane).
+ * Returns LJMD_E_BOX if a dimension has fewer than 3 cells or a slab has
+ * fewer than 1 plane.... */
+ljmd_status ljmd_plan_cells(const double box[3], double rbar_c, int64_t nc[3]);
+ljmd_status ljmd_plan_slab(int64_t ncz, int64_t nranks, int64_t rank, int64_t* z0, int64_t* z1);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LJMD_H */

@@ -68,6 +68,11 @@ def _load():
         lib.orc_sum.argtypes = [_D, ctypes.c_int64]
         lib.orc_kinetic.restype = ctypes.c_double
         lib.orc_kinetic.argtypes = [ctypes.c_int64, _D, ctypes.c_double]
+        lib.orc_neigh_rows.restype = ctypes.c_int64
+        lib.orc_neigh_rows.argtypes = [ctypes.c_int64, _D, _D, ctypes.c_double, _I, ctypes.c_int64, _I, _I]
+        lib.orc_forces_rows.restype = None
+        lib.orc_forces_rows.argtypes = [ctypes.c_int64, _D, _D, ctypes.POINTER(_LJ), _I, ctypes.c_int64,
+                                        _D, _D, _D, _D]
         lib.orc_run.restype = ctypes.c_int64
         lib.orc_run.argtypes = [ctypes.c_int64, _D, _D, _D, ctypes.POINTER(_Params), ctypes.c_int64,
                                 _D, _D, _D, _I, ctypes.c_int64]
@@ -167,6 +172,32 @@ def forces(pos, box, lj: LJ = LJ(), nlist=None):
     pe = _load().orc_forces(n, _dp(p), _dp(b), ctypes.byref(c), _ip(off), _ip(nbr),
                             _dp(F), _dp(e), _dp(S), _dp(A))
     return Forces(F, e, S, A, pe)
+
+
+def neighbours_rows(pos, box, rn, rows):
+    """O3 restricted to rows (sampled checks at full size): CSR over the given rows."""
+    p = _f64(pos, (-1, 3))
+    b = _f64(box)
+    idx = np.ascontiguousarray(rows, dtype=np.int64)
+    off = np.zeros(idx.shape[0] + 1, dtype=np.int64)
+    lib = _load()
+    tot = lib.orc_neigh_rows(p.shape[0], _dp(p), _dp(b), float(rn), _ip(idx), idx.shape[0], _ip(off), None)
+    nbr = np.zeros(max(tot, 1), dtype=np.int64)
+    lib.orc_neigh_rows(p.shape[0], _dp(p), _dp(b), float(rn), _ip(idx), idx.shape[0], _ip(off), _ip(nbr))
+    return off, nbr[:tot]
+
+
+def forces_rows(pos, box, rows, lj: LJ = LJ()):
+    """O5 brute force restricted to rows: Forces over the given rows (pe = sum of their e_i)."""
+    p = _f64(pos, (-1, 3))
+    b = _f64(box)
+    idx = np.ascontiguousarray(rows, dtype=np.int64)
+    m = idx.shape[0]
+    F, e, S, A = np.zeros((m, 3)), np.zeros(m), np.zeros(m), np.zeros(m)
+    c = lj.c()
+    _load().orc_forces_rows(p.shape[0], _dp(p), _dp(b), ctypes.byref(c), _ip(idx), m,
+                            _dp(F), _dp(e), _dp(S), _dp(A))
+    return Forces(F, e, S, A, float(e.sum()))
 
 
 def neumaier_sum(x):

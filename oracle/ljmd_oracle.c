@@ -288,6 +288,53 @@ double orc_kinetic(int64_t n, const double *vel, double mass)
     return ke;
 }
 
+/* ------------------------------------------------------- row-sampled O3/O5 -- */
+/* Brute force restricted to the rows i in idx[0..m): used to check full-size runs
+ * on sampled particles (same arithmetic as orc_neigh_brute / orc_forces, all j
+ * ascending).  nbr rows are returned CSR in offsets[m+1]. */
+int64_t orc_neigh_rows(int64_t n, const double *pos, const double box[3], double rn,
+                       const int64_t *idx, int64_t m, int64_t *offsets, int64_t *nbr)
+{
+    double rn2 = rn * rn;
+    int64_t tot = 0;
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t i = idx[r];
+        offsets[r] = tot;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double d[3];
+            orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
+            if (orc_r2(d) < rn2) {
+                if (nbr) nbr[tot] = j;
+                ++tot;
+            }
+        }
+    }
+    offsets[m] = tot;
+    return tot;
+}
+
+void orc_forces_rows(int64_t n, const double *pos, const double box[3], const orc_lj *lj,
+                     const int64_t *idx, int64_t m, double *F, double *e, double *S, double *A)
+{
+    for (int64_t r = 0; r < m; ++r) {
+        int64_t i = idx[r];
+        double Fi[3] = {0.0, 0.0, 0.0}, Ui = 0.0, Si = 0.0, Ai = 0.0;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double d[3];
+            orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
+            pair_accumulate(d, lj, Fi, &Ui, &Si, &Ai);
+        }
+        F[3 * r + 0] = Fi[0];
+        F[3 * r + 1] = Fi[1];
+        F[3 * r + 2] = Fi[2];
+        e[r] = 0.5 * Ui;
+        S[r] = Si;
+        A[r] = Ai;
+    }
+}
+
 /* ------------------------------------------------------------- O6 / O7 -- */
 typedef struct {
     orc_lj lj;

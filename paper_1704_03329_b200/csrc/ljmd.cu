@@ -1,0 +1,961 @@
+// ljmd.cu -- host side of libljmd.so: the C ABI declared in include/ljmd.h.
+// Owns device memory, the stream, the rebuild policy (IntegratorRange)
+// and the velocity-Verlet step loop (Alg. alg:VelocityVerlet).
+#include "../../include/ljmd.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace ljmd;
+
+namespace {
+
+thread_local std::string g_init_error;
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+};
+
+}  // namespace
+
+struct ljmd_ctx {
+    // ---- parameters
+    int64_t n_global = 0;
+    int n_own = 0;
+    double rc = 0, eps = 0, sigma = 0, dt = 0, rn = 0;
+    ljmd_options opt{};
+    Geo geo{};
+    int n_ocell = 0, n_ecell = 0, n_gcell = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // ---- status
+    ljmd_status err = LJMD_OK;
+    std::string msg;
+    // ---- capacities
+    int own_cap = 0, slot_cap = 0, K = 0, n_pad = 0;
+    int n_slots = 0;
+    // ---- slot space
+    double4* x[2] = {nullptr, nullptr};
+    int xc = 0;                       // current position buffer
+    float4* xf = nullptr;
+    int* slot_gid = nullptr;
+    // ---- owned space (double-buffered across rebuilds)
+    double* v[2] = {nullptr, nullptr};  // [3][own_cap]
+    int* gid[2] = {nullptr, nullptr};
+    int oc_cur = 0;
+    int* own_slot = nullptr;
+    int* ocell_of = nullptr;
+    double* F = nullptr;                // [3][own_cap]
+    double* e = nullptr;
+    double4* xbuild = nullptr;
+    double4* xw = nullptr;
+    int* cell_of = nullptr;
+    int* rank_in = nullptr;
+    int* perm = nullptr;
+    // ---- cells
+    int* ocount = nullptr;
+    int* obegin = nullptr;   // n_ocell + 1
+    int* ecount = nullptr;
+    int* ebegin = nullptr;   // n_ecell + 1
+    int* ecell_src = nullptr;
+    int* gc_dst = nullptr;
+    int* gc_src = nullptr;
+    int* gc_shift = nullptr;
+    int* scan_tmp = nullptr;
+    int scan_tmp_n = 0;
+    // ---- list
+    int* nbr = nullptr;
+    int* ncount = nullptr;
+    // ---- energies
+    double* pe_part = nullptr;
+    double* ke_part = nullptr;
+    int n_fblocks = 0;
+    double* hist = nullptr;   // [hist_cap][2]
+    int64_t hist_cap = 0, hist_count = 0;
+    std::vector<double> h_hist;
+    // ---- flags / staging
+    DevFlags* d_fl = nullptr;
+    DevFlags* h_fl = nullptr;      // pinned
+    int* h_slots = nullptr;        // pinned
+    double* d_stage = nullptr;     // [3][own_cap] readback staging
+    // ---- policy / stats
+    int64_t since = 0, steps_done = 0, n_rebuilds = 0, regrows = 0;
+    std::vector<int64_t> rebuild_steps;
+    int max_nbr = 0;
+    unsigned long long total_nbr = 0;
+    // ---- profiling
+    std::vector<cudaEvent_t> ev;
+    int64_t force_launches = 0;
+    double force_ms = 0.0;
+    int64_t kernel_launches = 0;   // launches of this library's kernels (CKL after each)
+};
+
+namespace {
+
+ljmd_status set_err(ljmd_ctx* c, ljmd_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        if (c->err == LJMD_OK) {
+            c->err = s;
+            c->msg = buf;
+        }
+    } else {
+        g_init_error = buf;
+    }
+    return s;
+}
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return set_err(c, LJMD_E_CUDA, "%s failed: %s (%s:%d)", #call,                 \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+    } while (0)
+
+#define CKL()                                                                               \
+    do {                                                                                    \
+        ++c->kernel_launches;                                                               \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess)                                                              \
+            return set_err(c, LJMD_E_CUDA, "kernel launch failed: %s (%s:%d)",             \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+    } while (0)
+
+#define TRY(expr)                       \
+    do {                                \
+        ljmd_status s_ = (expr);        \
+        if (s_ != LJMD_OK) return s_;   \
+    } while (0)
+
+template <class T>
+ljmd_status dalloc(ljmd_ctx* c, T** p, size_t n) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return set_err(c, LJMD_E_CAPACITY, "cudaMalloc of %zu bytes failed: %s", n * sizeof(T),
+                       cudaGetErrorString(e));
+    }
+    return LJMD_OK;
+}
+
+inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+// exclusive scan of n ints: out[0..n) prefixes, out[n] = total
+ljmd_status scan(ljmd_ctx* c, const int* in, int n, int* out) {
+    int nb = std::max(1, nblk(n, kScanTile));
+    if (nb > c->scan_tmp_n) {
+        TRY(dalloc(c, &c->scan_tmp, nb));
+        c->scan_tmp_n = nb;
+    }
+    k_scan_reduce<<<nb, kScanThreads, 0, c->stream>>>(in, n, c->scan_tmp);
+    k_scan_top<<<1, 1024, 0, c->stream>>>(c->scan_tmp, nb, out + n);
+    k_scan_down<<<nb, kScanThreads, 0, c->stream>>>(in, n, c->scan_tmp, out, 0);
+    c->kernel_launches += 2;
+    CKL();
+    return LJMD_OK;
+}
+
+ljmd_status sync_flags(ljmd_ctx* c) {
+    CK(cudaMemcpyAsync(c->h_fl, c->d_fl, sizeof(DevFlags), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return LJMD_OK;
+}
+
+ljmd_status reset_flags(ljmd_ctx* c) {
+    DevFlags f{};
+    f.max_nbr = 0;
+    f.nonfinite_gid = INT_MAX;
+    f.overlap_gid = INT_MAX;
+    f.overlap_gid_j = -1;
+    f.maxdisp2 = 0ull;
+    f.total_nbr = 0ull;
+    *c->h_fl = f;
+    CK(cudaMemcpyAsync(c->d_fl, c->h_fl, sizeof(DevFlags), cudaMemcpyHostToDevice, c->stream));
+    return LJMD_OK;
+}
+
+// ------------------------------------------------------------------ geometry / tables
+ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
+    int64_t nc[3];
+    if (ljmd_plan_cells(box, c->rn, nc) != LJMD_OK)
+        return set_err(c, LJMD_E_BOX,
+                       "box (%g, %g, %g) too small: need >= 3 cells of width >= rbar_c = %g per dimension",
+                       box[0], box[1], box[2], c->rn);
+    int64_t z0 = 0, z1 = nc[2];
+    if (ljmd_plan_slab(nc[2], c->opt.nranks, c->opt.rank, &z0, &z1) != LJMD_OK)
+        return set_err(c, LJMD_E_BOX, "cannot split %lld z-planes over %lld ranks", (long long)nc[2],
+                       (long long)c->opt.nranks);
+    Geo& g = c->geo;
+    for (int d = 0; d < 3; ++d) {
+        g.L[d] = box[d];
+        g.nc[d] = (int)nc[d];
+        g.w[d] = box[d] / (double)nc[d];
+        g.inv_w[d] = 1.0 / g.w[d];
+    }
+    g.z0 = (int)z0;
+    g.nzl = (int)(z1 - z0);
+    g.ex = g.nc[0] + 2;
+    g.ey = g.nc[1] + 2;
+    g.ez = g.nzl + 2;
+    c->n_ocell = g.nc[0] * g.nc[1] * g.nzl;
+    c->n_ecell = g.ex * g.ey * g.ez;
+    c->n_gcell = c->n_ecell - c->n_ocell;
+    if ((int64_t)c->n_ecell > (int64_t)INT_MAX / 2)
+        return set_err(c, LJMD_E_ARG, "cell grid too large");
+
+    // ghost-cell table (single rank: every ghost cell is a periodic image of an owned cell)
+    std::vector<int> src(c->n_ecell), gd, gs, gsh;
+    gd.reserve(c->n_gcell);
+    for (int iz = 0; iz < g.ez; ++iz)
+        for (int iy = 0; iy < g.ey; ++iy)
+            for (int ix = 0; ix < g.ex; ++ix) {
+                int ec = (iz * g.ey + iy) * g.ex + ix;
+                int cx = ix - 1, cy = iy - 1, cz = iz - 1;
+                int sx = cx < 0 ? -1 : (cx >= g.nc[0] ? 1 : 0);
+                int sy = cy < 0 ? -1 : (cy >= g.nc[1] ? 1 : 0);
+                int sz = cz < 0 ? -1 : (cz >= g.nzl ? 1 : 0);
+                int ox = cx - sx * g.nc[0], oy = cy - sy * g.nc[1], oz = cz - sz * g.nzl;
+                int oc = (oz * g.nc[1] + oy) * g.nc[0] + ox;
+                src[ec] = oc;
+                if (sx || sy || sz) {
+                    gd.push_back(ec);
+                    gs.push_back(((oz + 1) * g.ey + (oy + 1)) * g.ex + (ox + 1));
+                    gsh.push_back((sx + 1) | ((sy + 1) << 2) | ((sz + 1) << 4));
+                }
+            }
+    TRY(dalloc(c, &c->ecell_src, c->n_ecell));
+    TRY(dalloc(c, &c->gc_dst, c->n_gcell));
+    TRY(dalloc(c, &c->gc_src, c->n_gcell));
+    TRY(dalloc(c, &c->gc_shift, c->n_gcell));
+    CK(cudaMemcpy(c->ecell_src, src.data(), sizeof(int) * src.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->gc_dst, gd.data(), sizeof(int) * gd.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->gc_src, gs.data(), sizeof(int) * gs.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->gc_shift, gsh.data(), sizeof(int) * gsh.size(), cudaMemcpyHostToDevice));
+    TRY(dalloc(c, &c->ocount, c->n_ocell));
+    TRY(dalloc(c, &c->obegin, c->n_ocell + 1));
+    TRY(dalloc(c, &c->ecount, c->n_ecell));
+    TRY(dalloc(c, &c->ebegin, c->n_ecell + 1));
+    return LJMD_OK;
+}
+
+ljmd_status alloc_owned(ljmd_ctx* c, int cap) {
+    c->own_cap = cap;
+    c->n_pad = (cap + 31) / 32 * 32;
+    for (int b = 0; b < 2; ++b) {
+        TRY(dalloc(c, &c->v[b], (size_t)3 * cap));
+        TRY(dalloc(c, &c->gid[b], cap));
+    }
+    TRY(dalloc(c, &c->own_slot, cap));
+    TRY(dalloc(c, &c->ocell_of, cap));
+    TRY(dalloc(c, &c->F, (size_t)3 * cap));
+    TRY(dalloc(c, &c->e, cap));
+    TRY(dalloc(c, &c->xw, cap));
+    TRY(dalloc(c, &c->cell_of, cap));
+    TRY(dalloc(c, &c->rank_in, cap));
+    TRY(dalloc(c, &c->perm, cap));
+    TRY(dalloc(c, &c->ncount, cap));
+    TRY(dalloc(c, &c->d_stage, (size_t)3 * cap));
+    if (c->opt.rebuild_check) TRY(dalloc(c, &c->xbuild, cap));
+    c->n_fblocks = nblk(cap, kForceThreads);
+    TRY(dalloc(c, &c->pe_part, c->n_fblocks));
+    TRY(dalloc(c, &c->ke_part, c->n_fblocks));
+    return LJMD_OK;
+}
+
+ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
+    double4* nx[2] = {nullptr, nullptr};
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t e = cudaMalloc(&nx[b], sizeof(double4) * (size_t)cap);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            if (nx[0]) cudaFree(nx[0]);
+            return set_err(c, LJMD_E_CAPACITY, "cudaMalloc of %zu position slots failed", (size_t)cap);
+        }
+    }
+    if (keep_current && c->x[c->xc])
+        CK(cudaMemcpyAsync(nx[c->xc], c->x[c->xc], sizeof(double4) * (size_t)c->slot_cap,
+                           cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int b = 0; b < 2; ++b) {
+        if (c->x[b]) cudaFree(c->x[b]);
+        c->x[b] = nx[b];
+    }
+    TRY(dalloc(c, &c->xf, cap));
+    TRY(dalloc(c, &c->slot_gid, cap));
+    c->slot_cap = cap;
+    return LJMD_OK;
+}
+
+ljmd_status alloc_list(ljmd_ctx* c, int K) {
+    c->K = K;
+    TRY(dalloc(c, &c->nbr, (size_t)K * c->n_pad));
+    return LJMD_OK;
+}
+
+// ------------------------------------------------------------------ kernels launchers
+ljmd_status launch_nlist(ljmd_ctx* c) {
+    NlistArgs a;
+    a.g = c->geo;
+    a.x = c->x[c->xc];
+    a.xf = c->xf;
+    a.own_slot = c->own_slot;
+    a.ocell_of = c->ocell_of;
+    a.ebegin = c->ebegin;
+    a.ecount = c->ecount;
+    a.nbr = c->nbr;
+    a.ncount = c->ncount;
+    a.n_own = c->n_own;
+    a.n_pad = c->n_pad;
+    a.K = c->K;
+    a.rn2 = c->rn * c->rn;
+    // fp32 prefilter: |x_f - x| <= 2^-24 |x| per coordinate (|x| <= L + w) and the fp32
+    // difference/product roundings; a margin of 4x that bound keeps the filter conservative.
+    double xmax = 0.0;
+    for (int d = 0; d < 3; ++d) xmax = std::max(xmax, c->geo.L[d] + 2.0 * c->geo.w[d]);
+    double m = 4.0 * (std::ldexp(xmax, -23) + std::ldexp(c->rn, -21)) + 1e-7;
+    a.thr_f = (float)((c->rn + m) * (c->rn + m) * (1.0 + std::ldexp(1.0, -18)));
+    double slop = 1e-9 * (1.0 + xmax);
+    a.prune2 = (c->rn + slop) * (c->rn + slop);
+    a.fl = c->d_fl;
+    a.slot_gid = c->slot_gid;
+    k_build_nlist<<<nblk(c->n_own, 128), 128, 0, c->stream>>>(a);
+    CKL();
+    return LJMD_OK;
+}
+
+ForceArgs force_args(ljmd_ctx* c) {
+    ForceArgs a;
+    const double s2 = c->sigma * c->sigma, s6 = s2 * s2 * s2, s12 = s6 * s6;
+    a.x = c->x[c->xc];
+    a.x_next = c->x[c->xc ^ 1];
+    a.own_slot = c->own_slot;
+    a.nbr = c->nbr;
+    a.ncount = c->ncount;
+    a.fx = c->F;
+    a.fy = c->F + c->own_cap;
+    a.fz = c->F + 2 * (size_t)c->own_cap;
+    double* v = c->v[c->oc_cur];
+    a.vx = v;
+    a.vy = v + c->own_cap;
+    a.vz = v + 2 * (size_t)c->own_cap;
+    a.e = c->e;
+    a.pe_part = c->pe_part;
+    a.ke_part = c->ke_part;
+    a.xbuild = c->xbuild;
+    a.fl = c->d_fl;
+    a.n_own = c->n_own;
+    a.n_pad = c->n_pad;
+    a.rc2 = c->rc * c->rc;
+    a.c12 = 48.0 * c->eps * s12;
+    a.c6 = 24.0 * c->eps * s6;
+    a.a12 = 4.0 * c->eps * s12;
+    a.a6 = 4.0 * c->eps * s6;
+    a.a0 = 4.0 * c->eps * c->opt.energy_shift;
+    a.h = 0.5 * c->dt / c->opt.mass;
+    a.dt = c->dt;
+    a.half_m = 0.5 * c->opt.mass;
+    return a;
+}
+
+template <bool E, int M, bool C>
+void force_launch(ljmd_ctx* c, const ForceArgs& a) {
+    k_force<E, M, C><<<nblk(c->n_own, kForceThreads), kForceThreads, 0, c->stream>>>(a);
+}
+
+ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check) {
+    ForceArgs a = force_args(c);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->opt.profile) {
+        size_t k = (size_t)c->force_launches * 2;
+        while (c->ev.size() < k + 2) {
+            cudaEvent_t ev;
+            CK(cudaEventCreate(&ev));
+            c->ev.push_back(ev);
+        }
+        e0 = c->ev[k];
+        e1 = c->ev[k + 1];
+        CK(cudaEventRecord(e0, c->stream));
+    }
+    if (energy) {
+        if (mode == kStore) force_launch<true, kStore, false>(c, a);
+        else if (mode == kKick) force_launch<true, kKick, false>(c, a);
+        else if (check) force_launch<true, kKKD, true>(c, a);
+        else force_launch<true, kKKD, false>(c, a);
+    } else {
+        if (mode == kStore) force_launch<false, kStore, false>(c, a);
+        else if (mode == kKick) force_launch<false, kKick, false>(c, a);
+        else if (check) force_launch<false, kKKD, true>(c, a);
+        else force_launch<false, kKKD, false>(c, a);
+    }
+    CKL();
+    if (c->opt.profile) {
+        CK(cudaEventRecord(e1, c->stream));
+        ++c->force_launches;
+    }
+    return LJMD_OK;
+}
+
+ljmd_status collect_profile(ljmd_ctx* c, int64_t first_launch) {
+    if (!c->opt.profile) return LJMD_OK;
+    for (int64_t k = first_launch; k < c->force_launches; ++k) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev[2 * k], c->ev[2 * k + 1]));
+        c->force_ms += ms;
+    }
+    return LJMD_OK;
+}
+
+ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
+    GhostCells gc{c->gc_dst, c->gc_src, c->gc_shift, c->n_gcell};
+    int blocks = nblk((int64_t)c->n_gcell * 32, 256);
+    if (c->n_gcell == 0) return LJMD_OK;
+    if (at_build)
+        k_ghost_refresh<true><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo, c->x[c->xc],
+                                                             c->xf, c->slot_gid);
+    else
+        k_ghost_refresh<false><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo,
+                                                              c->x[c->xc], c->xf, c->slot_gid);
+    CKL();
+    return LJMD_OK;
+}
+
+// Cell binning (counting sort + gid order), ghost images and the Verlet list
+// (Sec. 3.4; IntegratorRange rebuild).
+ljmd_status rebuild(ljmd_ctx* c) {
+    TRY(reset_flags(c));
+    CK(cudaMemsetAsync(c->ocount, 0, sizeof(int) * c->n_ocell, c->stream));
+    const int n = c->n_own;
+    const int* gid_old = c->gid[c->oc_cur];
+    k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, c->geo, c->xw, c->ocount,
+                                                    c->cell_of, c->rank_in, gid_old, c->d_fl);
+    CKL();
+    TRY(scan(c, c->ocount, c->n_ocell, c->obegin));
+    k_ext_counts<<<nblk(c->n_ecell, 256), 256, 0, c->stream>>>(c->n_ecell, c->ocount, c->geo, c->ecell_src,
+                                                              c->ecount);
+    CKL();
+    TRY(scan(c, c->ecount, c->n_ecell, c->ebegin));
+    CK(cudaMemcpyAsync(c->h_slots, c->ebegin + c->n_ecell, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TRY(sync_flags(c));
+    if (c->h_fl->nonfinite_gid != INT_MAX)
+        return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
+                       c->h_fl->nonfinite_gid);
+    const int need = *c->h_slots;
+    if (need > c->slot_cap) {
+        TRY(alloc_slots(c, (int)std::min<int64_t>((int64_t)need * 5 / 4 + 1024, INT_MAX), true));
+        ++c->regrows;
+    }
+    c->n_slots = need;
+    k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm);
+    CKL();
+    const int on = c->oc_cur ^ 1;
+    const double* vo = c->v[c->oc_cur];
+    double* vn = c->v[on];
+    const size_t oc = c->own_cap;
+    double4* xn = c->x[c->xc ^ 1];
+    k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
+        c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, gid_old, c->xw, vo, vo + oc, vo + 2 * oc,
+        xn, c->xf, vn, vn + oc, vn + 2 * oc, c->gid[on], c->own_slot, c->ocell_of, c->slot_gid,
+        c->opt.rebuild_check ? c->xbuild : nullptr);
+    CKL();
+    c->oc_cur = on;
+    c->xc ^= 1;
+    TRY(refresh_ghosts(c, true));
+    TRY(launch_nlist(c));
+    TRY(sync_flags(c));
+    if (c->h_fl->overlap_gid != INT_MAX)
+        return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)", c->h_fl->overlap_gid,
+                       c->h_fl->overlap_gid_j);
+    if (c->h_fl->max_nbr > c->K) {
+        int K = (c->h_fl->max_nbr * 5 / 4 + 8) / 8 * 8;
+        TRY(alloc_list(c, K));
+        ++c->regrows;
+        TRY(reset_flags(c));
+        TRY(launch_nlist(c));
+        TRY(sync_flags(c));
+    }
+    c->max_nbr = c->h_fl->max_nbr;
+    c->total_nbr = c->h_fl->total_nbr;
+    return LJMD_OK;
+}
+
+ljmd_status ensure_hist(ljmd_ctx* c, int64_t need) {
+    if (need <= c->hist_cap) return LJMD_OK;
+    int64_t cap = std::max<int64_t>(need, 64);
+    TRY(dalloc(c, &c->hist, (size_t)2 * cap));
+    c->hist_cap = cap;
+    return LJMD_OK;
+}
+
+ljmd_status finalize_energy(ljmd_ctx* c, double* dst) {
+    k_finalize_energy<<<1, 1024, 0, c->stream>>>(c->pe_part, c->ke_part, nblk(c->n_own, kForceThreads), dst);
+    CKL();
+    return LJMD_OK;
+}
+
+ljmd_status pull_hist(ljmd_ctx* c, int64_t count) {
+    if (count <= 0) return LJMD_OK;
+    std::vector<double> tmp((size_t)2 * count);
+    CK(cudaMemcpyAsync(tmp.data(), c->hist, sizeof(double) * 2 * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->h_hist.insert(c->h_hist.end(), tmp.begin(), tmp.end());
+    return LJMD_OK;
+}
+
+// init sequence shared by ljmd_init and ljmd_set_state
+ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
+    const int64_t n = c->n_global;
+    double* dpos = nullptr;
+    double* dvel = nullptr;
+    TRY(dalloc(c, &dpos, (size_t)3 * n));
+    TRY(dalloc(c, &dvel, (size_t)3 * n));
+    CK(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dvel, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    TRY(reset_flags(c));
+    c->oc_cur = 0;
+    c->xc = 0;
+    double* v = c->v[0];
+    const size_t oc = c->own_cap;
+    k_load_rows<<<nblk(n, 256), 256, 0, c->stream>>>((int)n, dpos, dvel, c->x[0], v, v + oc, v + 2 * oc,
+                                                    c->gid[0], c->own_slot, c->d_fl);
+    CKL();
+    TRY(sync_flags(c));
+    cudaFree(dpos);
+    cudaFree(dvel);
+    if (c->h_fl->nonfinite_gid != INT_MAX)
+        return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
+                       c->h_fl->nonfinite_gid);
+    c->n_own = (int)n;
+    c->since = 0;
+    c->steps_done = 0;
+    c->n_rebuilds = 0;
+    c->rebuild_steps.clear();
+    c->h_hist.clear();
+    TRY(rebuild(c));
+    TRY(ensure_hist(c, 1));
+    TRY(launch_force(c, true, kStore, false));
+    TRY(finalize_energy(c, c->hist));
+    TRY(pull_hist(c, 1));
+    return LJMD_OK;
+}
+
+ljmd_status check_ctx(ljmd_ctx* c) {
+    if (!c) return LJMD_E_ARG;
+    if (c->err != LJMD_OK) return LJMD_E_STATE;
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return set_err(c, LJMD_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    return LJMD_OK;
+}
+
+// host scatter of a compact owned-space [n_own][3] (or [n_own]) array into caller rows
+ljmd_status readback(ljmd_ctx* c, const double* dsrc, int width, double* out) {
+    std::vector<double> tmp((size_t)width * c->n_own);
+    std::vector<int> g(c->n_own);
+    CK(cudaMemcpyAsync(tmp.data(), dsrc, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g.data(), c->gid[c->oc_cur], sizeof(int) * g.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int t = 0; t < c->n_own; ++t)
+        for (int k = 0; k < width; ++k) out[(size_t)g[t] * width + k] = tmp[(size_t)t * width + k];
+    return LJMD_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* ljmd_version(void) { return "ljmd 0.1 sm_100a"; }
+
+ljmd_status ljmd_default_options(ljmd_options* o) {
+    if (!o) return LJMD_E_ARG;
+    std::memset(o, 0, sizeof *o);
+    o->delta = 0.25;
+    o->rebuild_every = 20;
+    o->rebuild_check = 0;
+    o->mass = 1.0;
+    o->energy_shift = 0.25;
+    o->energy_every = 10;
+    o->device = -1;
+    o->nbr_capacity = 0;
+    o->rank = 0;
+    o->nranks = 1;
+    o->nccl_id = nullptr;
+    o->stream = nullptr;
+    o->profile = 0;
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_plan_cells(const double box[3], double rbar_c, int64_t nc[3]) {
+    if (!box || !nc || !(rbar_c > 0.0)) return LJMD_E_ARG;
+    for (int d = 0; d < 3; ++d) {
+        if (!(box[d] > 0.0) || !std::isfinite(box[d])) return LJMD_E_ARG;
+        double q = std::floor(box[d] / (rbar_c * (1.0 + 1e-12)));
+        if (q < 3.0) return LJMD_E_BOX;
+        if (q > 1e6) return LJMD_E_ARG;
+        nc[d] = (int64_t)q;
+    }
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_plan_slab(int64_t ncz, int64_t nranks, int64_t rank, int64_t* z0, int64_t* z1) {
+    if (!z0 || !z1 || nranks < 1 || rank < 0 || rank >= nranks) return LJMD_E_ARG;
+    if (ncz < 3 || ncz < nranks) return LJMD_E_BOX;
+    int64_t base = ncz / nranks, extra = ncz % nranks;
+    *z0 = rank * base + std::min(rank, extra);
+    *z1 = *z0 + base + (rank < extra ? 1 : 0);
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double* vel, const double box[3],
+                      double rc, double epsilon, double sigma, double dt, const ljmd_options* opt) {
+    if (out) *out = nullptr;
+    if (!out || !pos || !vel || !box || n <= 0 || n > INT_MAX / 2)
+        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: bad pointer or n = %lld", (long long)n);
+    if (!(rc > 0.0) || !(epsilon > 0.0) || !(sigma > 0.0) || !(dt > 0.0) || !std::isfinite(rc) ||
+        !std::isfinite(dt))
+        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: rc, epsilon, sigma and dt must be positive and finite");
+    ljmd_options o;
+    ljmd_default_options(&o);
+    if (opt) o = *opt;
+    if (!(o.delta >= 0.0) || o.rebuild_every < 1 || !(o.mass > 0.0) || o.energy_every < 0)
+        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: bad options (delta >= 0, rebuild_every >= 1, mass > 0)");
+    if (o.nranks != 1)
+        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: nranks > 1 requires the NCCL build (not in this library)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(nullptr, LJMD_E_CUDA, "ljmd_init: no CUDA device");
+    }
+    ljmd_ctx* c = new ljmd_ctx();
+    c->opt = o;
+    c->n_global = n;
+    c->rc = rc;
+    c->eps = epsilon;
+    c->sigma = sigma;
+    c->dt = dt;
+    c->rn = rc + o.delta;
+    auto fail = [&](ljmd_status s) {
+        g_init_error = c->msg.empty() ? std::string("ljmd_init failed") : c->msg;
+        ljmd_destroy(c);
+        return s;
+    };
+    if (o.device >= 0) {
+        if (cudaSetDevice((int)o.device) != cudaSuccess) {
+            set_err(c, LJMD_E_CUDA, "cudaSetDevice(%lld) failed", (long long)o.device);
+            return fail(LJMD_E_CUDA);
+        }
+    }
+    cudaGetDevice(&c->device);
+    if (o.stream) {
+        c->stream = (cudaStream_t)o.stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            set_err(c, LJMD_E_CUDA, "cudaStreamCreate failed");
+            return fail(LJMD_E_CUDA);
+        }
+        c->own_stream = true;
+    }
+    ljmd_status s;
+    if ((s = plan_geometry(c, box)) != LJMD_OK) return fail(s);
+    if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
+        cudaMallocHost(&c->h_fl, sizeof(DevFlags)) != cudaSuccess ||
+        cudaMallocHost(&c->h_slots, sizeof(int)) != cudaSuccess) {
+        set_err(c, LJMD_E_CUDA, "flag allocation failed");
+        return fail(LJMD_E_CUDA);
+    }
+    const int cap = (int)n;
+    if ((s = alloc_owned(c, cap)) != LJMD_OK) return fail(s);
+    const double ghost_ratio = (double)c->n_ecell / (double)c->n_ocell;
+    int64_t scap = (int64_t)std::ceil(n * ghost_ratio * 1.15) + 4096;
+    if ((s = alloc_slots(c, (int)std::min<int64_t>(scap, INT_MAX / 2), false)) != LJMD_OK) return fail(s);
+    // list width K: expected 4/3 pi rbar_c^3 rho neighbours with headroom
+    double vol = box[0] * box[1] * box[2];
+    double expect = 4.0 / 3.0 * M_PI * c->rn * c->rn * c->rn * (double)n / vol;
+    int K = o.nbr_capacity > 0 ? (int)o.nbr_capacity : ((int)std::ceil(expect * 1.4) + 16 + 7) / 8 * 8;
+    if ((s = alloc_list(c, K)) != LJMD_OK) return fail(s);
+    if ((s = load_state(c, pos, vel)) != LJMD_OK) return fail(s);
+    *out = c;
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_set_state(ljmd_ctx* c, const double* pos, const double* vel) {
+    TRY(check_ctx(c));
+    if (!pos || !vel) return LJMD_E_ARG;
+    return load_state(c, pos, vel);
+}
+
+ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
+    TRY(check_ctx(c));
+    if (nsteps < 0) return set_err(c, LJMD_E_ARG, "ljmd_step: nsteps < 0");
+    if (nsteps == 0) return LJMD_OK;
+    const bool check = c->opt.rebuild_check != 0;
+    const int64_t ee = c->opt.energy_every;
+    TRY(ensure_hist(c, nsteps / std::max<int64_t>(ee, 1) + 2));
+    int64_t nsamp = 0;
+    const int64_t first_launch = c->force_launches;
+    const double delta2 = c->opt.delta * c->opt.delta;
+    // Alg. alg:VelocityVerlet line 6 of the first step (uses the stored F)
+    if (check) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
+    {
+        double* v = c->v[c->oc_cur];
+        const size_t oc = c->own_cap;
+        double h = 0.5 * c->dt / c->opt.mass;
+        if (check)
+            k_kick_drift<true><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
+                c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
+                c->dt, c->xbuild, c->d_fl);
+        else
+            k_kick_drift<false><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
+                c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
+                c->dt, c->xbuild, c->d_fl);
+        CKL();
+    }
+    for (int64_t s = 1; s <= nsteps; ++s) {
+        ++c->since;
+        ++c->steps_done;
+        bool due = c->since >= c->opt.rebuild_every;
+        if (!due && check) {
+            TRY(sync_flags(c));
+            double m2;
+            std::memcpy(&m2, &c->h_fl->maxdisp2, sizeof m2);
+            due = 4.0 * m2 > delta2;
+        }
+        if (due) {
+            TRY(rebuild(c));
+            c->since = 0;
+            ++c->n_rebuilds;
+            c->rebuild_steps.push_back(c->steps_done);
+        } else {
+            TRY(refresh_ghosts(c, false));
+        }
+        const bool sample = ee > 0 && (c->steps_done % ee) == 0;
+        const bool last = s == nsteps;
+        if (check && !last) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
+        TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last));
+        if (sample) {
+            TRY(finalize_energy(c, c->hist + 2 * nsamp));
+            ++nsamp;
+        }
+        if (!last) c->xc ^= 1;
+    }
+    TRY(pull_hist(c, nsamp));
+    TRY(collect_profile(c, first_launch));
+    TRY(sync_flags(c));
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_forces(ljmd_ctx* c, double* out) {
+    TRY(check_ctx(c));
+    if (!out) return LJMD_E_ARG;
+    const size_t oc = c->own_cap;
+    k_gather_soa<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->F, c->F + oc, c->F + 2 * oc, c->d_stage);
+    CKL();
+    return readback(c, c->d_stage, 3, out);
+}
+
+ljmd_status ljmd_get_velocities(ljmd_ctx* c, double* out) {
+    TRY(check_ctx(c));
+    if (!out) return LJMD_E_ARG;
+    const size_t oc = c->own_cap;
+    const double* v = c->v[c->oc_cur];
+    k_gather_soa<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, v, v + oc, v + 2 * oc, c->d_stage);
+    CKL();
+    return readback(c, c->d_stage, 3, out);
+}
+
+ljmd_status ljmd_get_positions(ljmd_ctx* c, double* out, int64_t wrapped) {
+    TRY(check_ctx(c));
+    if (!out) return LJMD_E_ARG;
+    k_gather_pos<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->x[c->xc], c->own_slot, c->d_stage);
+    CKL();
+    std::vector<double> tmp((size_t)3 * c->n_own);
+    std::vector<int> g(c->n_own);
+    CK(cudaMemcpyAsync(tmp.data(), c->d_stage, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g.data(), c->gid[c->oc_cur], sizeof(int) * g.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int t = 0; t < c->n_own; ++t)
+        for (int k = 0; k < 3; ++k) {
+            double x = tmp[(size_t)3 * t + k];
+            if (wrapped) {
+                double L = c->geo.L[k];
+                x = x - L * std::floor(x / L);
+                if (x < 0.0) x += L;
+                if (x >= L) x -= L;
+            }
+            out[(size_t)g[t] * 3 + k] = x;
+        }
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_particle_energy(ljmd_ctx* c, double* out) {
+    TRY(check_ctx(c));
+    if (!out) return LJMD_E_ARG;
+    TRY(launch_force(c, true, kStore, false));
+    return readback(c, c->e, 1, out);
+}
+
+ljmd_status ljmd_get_energy(ljmd_ctx* c, double* pe, double* ke) {
+    TRY(check_ctx(c));
+    TRY(launch_force(c, true, kStore, false));
+    TRY(ensure_hist(c, 1));
+    double* tmp = c->hist + 2 * (c->hist_cap - 1);
+    TRY(finalize_energy(c, tmp));
+    double h[2];
+    CK(cudaMemcpyAsync(h, tmp, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (pe) *pe = h[0];
+    if (ke) *ke = h[1];
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_energy_history(ljmd_ctx* c, double* pe, double* ke, int64_t cap, int64_t* count) {
+    TRY(check_ctx(c));
+    int64_t avail = (int64_t)c->h_hist.size() / 2;
+    if (count) *count = avail;
+    for (int64_t i = 0; i < std::min(cap, avail); ++i) {
+        if (pe) pe[i] = c->h_hist[2 * i];
+        if (ke) ke[i] = c->h_hist[2 * i + 1];
+    }
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, int64_t cap) {
+    TRY(check_ctx(c));
+    if (!offsets) return LJMD_E_ARG;
+    const int n = c->n_own;
+    std::vector<int> cnt(n), g(n);
+    CK(cudaMemcpyAsync(cnt.data(), c->ncount, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g.data(), c->gid[c->oc_cur], sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int64_t> rowcnt(c->n_global, 0);
+    for (int t = 0; t < n; ++t) rowcnt[g[t]] = std::min(cnt[t], c->K);
+    offsets[0] = 0;
+    for (int64_t i = 0; i < c->n_global; ++i) offsets[i + 1] = offsets[i] + rowcnt[i];
+    if (!gids || cap < offsets[c->n_global]) return LJMD_OK;
+    std::vector<long long> toff(n + 1, 0);
+    for (int t = 0; t < n; ++t) toff[t + 1] = toff[t] + std::min(cnt[t], c->K);
+    long long* d_off = nullptr;
+    long long* d_out = nullptr;
+    TRY(dalloc(c, &d_off, n + 1));
+    TRY(dalloc(c, &d_out, (size_t)std::max<long long>(toff[n], 1)));
+    CK(cudaMemcpyAsync(d_off, toff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+    k_list_gids<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->n_pad, c->nbr, c->ncount, c->slot_gid, d_off, d_out);
+    CKL();
+    std::vector<long long> h((size_t)toff[n]);
+    CK(cudaMemcpyAsync(h.data(), d_out, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d_off);
+    cudaFree(d_out);
+    for (int t = 0; t < n; ++t)
+        for (long long k = toff[t]; k < toff[t + 1]; ++k) gids[offsets[g[t]] + (k - toff[t])] = h[(size_t)k];
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_rebuild_steps(ljmd_ctx* c, int64_t* out, int64_t cap, int64_t* count) {
+    TRY(check_ctx(c));
+    int64_t n = (int64_t)c->rebuild_steps.size();
+    if (count) *count = n;
+    for (int64_t i = 0; out && i < std::min(n, cap); ++i) out[i] = c->rebuild_steps[(size_t)i];
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s) {
+    TRY(check_ctx(c));
+    if (!s) return LJMD_E_ARG;
+    std::memset(s, 0, sizeof *s);
+    s->steps_done = c->steps_done;
+    s->n_rebuilds = c->n_rebuilds;
+    s->n_owned = c->n_own;
+    s->n_ghost = c->n_slots - c->n_own;
+    s->nbr_capacity = c->K;
+    s->max_neighbours = c->max_nbr;
+    s->total_neighbours = (int64_t)c->total_nbr;
+    for (int d = 0; d < 3; ++d) s->n_cells[d] = c->geo.nc[d];
+    s->regrows = c->regrows;
+    s->force_launches = c->force_launches;
+    s->force_ms = c->force_ms;
+    s->energy_samples = (int64_t)c->h_hist.size() / 2;
+    s->kernel_launches = c->kernel_launches;
+    return LJMD_OK;
+}
+
+const char* ljmd_last_error(const ljmd_ctx* c) {
+    if (!c) return g_init_error.c_str();
+    return c->msg.c_str();
+}
+
+void ljmd_destroy(ljmd_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    void* ptrs[] = {c->x[0], c->x[1], c->xf, c->slot_gid, c->v[0], c->v[1], c->gid[0], c->gid[1],
+                    c->own_slot, c->ocell_of, c->F, c->e, c->xbuild, c->xw, c->cell_of, c->rank_in, c->perm,
+                    c->ocount, c->obegin, c->ecount, c->ebegin, c->ecell_src, c->gc_dst, c->gc_src, c->gc_shift,
+                    c->scan_tmp, c->nbr, c->ncount, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_fl) cudaFreeHost(c->h_fl);
+    if (c->h_slots) cudaFreeHost(c->h_slots);
+    for (auto e : c->ev) cudaEventDestroy(e);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+}  // extern "C"
+
+extern "C" ljmd_status ljmd_measure_fp64_peak(int64_t device, double* tflops) {
+    ljmd_ctx* c = nullptr;
+    if (!tflops) return LJMD_E_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_err(nullptr, LJMD_E_CUDA, "no CUDA device");
+    }
+    if (device >= 0) CK(cudaSetDevice((int)device));
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double* out = nullptr;
+    CK(cudaMalloc(&out, sizeof(double) * 4096));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = sms * 8, iters = 2048;
+    k_fp64_peak<<<blocks, 256>>>(out, 64, 0.999999, 1e-7);   // warm-up (clocks)
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        CK(cudaEventRecord(e0));
+        k_fp64_peak<<<blocks, 256>>>(out, iters, 0.999999, 1e-7);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    double flops = 2.0 * 8.0 * 16.0 * iters * (double)blocks * 256.0;
+    *tflops = flops / (best * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return LJMD_OK;
+}

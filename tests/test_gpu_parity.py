@@ -1,0 +1,291 @@
+"""GPU parity: libljmd.so (through the C ABI) against the CPU oracle on identical inputs.
+
+Parity contract:
+  * neighbour sets: identical sets of (gid_i, gid_j) built from identical positions;
+  * forces / energies: |dF_ik| <= 1e-10 S_i, |de_i| <= 1e-10 A_i / 2 (reading R16);
+  * global PE/KE: relative 1e-10 of sum |.|;
+  * 100-step trajectory energies within 1e-8 relative (same rebuild schedule).
+"""
+import numpy as np
+import pytest
+
+import ljinputs as li
+
+pytestmark = pytest.mark.gpu
+
+RC, DELTA = li.RC, li.DELTA
+RN = RC + DELTA
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_1704_03329_b200 import ljmd
+    ljmd.load()
+    return ljmd
+
+
+def lj_of(shift):
+    import oracle
+    return oracle.LJ(rc=RC, shift=shift)
+
+
+def gid_pairs(off, nbr):
+    n = len(off) - 1
+    rows = np.repeat(np.arange(n), np.diff(off))
+    return set(zip(rows.tolist(), nbr.tolist()))
+
+
+def check_forces(ctx, orc, pos, box, shift, rows=None):
+    """Compare GPU F and e_i with the oracle (brute force, minimum image) at pos."""
+    F = ctx.forces()
+    e = ctx.particle_energy()
+    if rows is None:
+        ref = orc.forces(pos, box, lj_of(shift))
+        Fg, eg = F, e
+    else:
+        ref = orc.forces_rows(pos, box, rows, lj_of(shift))
+        Fg, eg = F[rows], e[rows]
+    S = ref.S[:, None]
+    bad = np.abs(Fg - ref.F) > TOL * S + 1e-300
+    assert not bad.any(), f"force mismatch at rows {np.nonzero(bad.any(1))[0][:5]}: " \
+                          f"{np.abs(Fg - ref.F).max()} (S {S.max()})"
+    bad_e = np.abs(eg - ref.e) > TOL * 0.5 * ref.A + 1e-300
+    assert not bad_e.any(), f"energy mismatch {np.abs(eg - ref.e).max()}"
+    return ref
+
+
+def c1(sigma_d=0.05, t0=1.44, cells=10):
+    pos, box = li.fcc(cells, cells, cells)
+    if sigma_d:
+        pos = li.perturb(pos, sigma_d)
+    vel = li.velocities(len(pos), t0)
+    return pos, vel, box
+
+
+# ------------------------------------------------------------------------------ init
+
+def test_init_wrap_bitwise(eng, orc):
+    """Positions outside the box (shifted by +-L, tiny negatives) wrap exactly like O1."""
+    pos, vel, box = c1()
+    rng = np.random.default_rng(3)
+    shifted = pos + box * rng.integers(-2, 3, pos.shape)
+    shifted[:5, 0] = [-1e-17, -0.0, box[0], 2 * box[0], -box[0]]
+    with eng.LJMD(shifted, vel, box, dt=0.005) as ctx:
+        got = ctx.positions()
+    assert np.array_equal(got, orc.wrap(shifted, box))
+
+
+@pytest.mark.parametrize("cells", [6, 10])
+def test_init_neighbours_exact(eng, orc, cells):
+    pos, vel, box = c1(cells=cells)
+    with eng.LJMD(pos, vel, box) as ctx:
+        x = ctx.positions()
+        off, nbr = ctx.neighbours()
+        st = ctx.stats()
+    ref = orc.neighbours(x, box, RN, "brute")
+    assert gid_pairs(off, nbr) == gid_pairs(*ref)
+    assert st["total_neighbours"] == len(ref[1])
+    assert st["max_neighbours"] == np.diff(ref[0]).max()
+
+
+def test_tie_and_seam_fixture(eng, orc):
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tie_and_seam.json")))
+    pos, box = np.array(g["pos"]), np.array(g["box"])
+    with eng.LJMD(pos, np.zeros_like(pos), box, energy_shift=0.0) as ctx:
+        off, nbr = ctx.neighbours()
+        got = [sorted(nbr[off[i]:off[i + 1]].tolist()) for i in range(len(pos))]
+        assert got == g["nb_rbar"]
+        np.testing.assert_allclose(ctx.forces(), np.array(g["F"]), rtol=1e-14, atol=1e-15)
+        np.testing.assert_allclose(ctx.particle_energy(), np.array(g["e_shift0"]), rtol=1e-14, atol=1e-16)
+        pe, ke = ctx.energy()
+        assert pe == pytest.approx(g["pe_shift0"], rel=1e-14) and ke == 0.0
+
+
+@pytest.mark.parametrize("shift", [0.0, 0.25])
+def test_perfect_fcc(eng, orc, shift):
+    pos, box = li.fcc(10, 10, 10)
+    with eng.LJMD(pos, np.zeros_like(pos), box, energy_shift=shift) as ctx:
+        off, _ = ctx.neighbours()
+        assert np.all(np.diff(off) == 78)
+        pe, _ = ctx.energy()
+        ref = orc.forces(pos, box, lj_of(shift))
+        assert pe == pytest.approx(ref.pe, rel=1e-12)
+        assert np.abs(ctx.forces()).max() < 1e-12
+
+
+@pytest.mark.parametrize("shift", [0.25, 0.0])
+def test_init_forces_energies(eng, orc, shift):
+    pos, vel, box = c1()
+    with eng.LJMD(pos, vel, box, energy_shift=shift) as ctx:
+        x = ctx.positions()
+        ref = check_forces(ctx, orc, x, box, shift)
+        pe, ke = ctx.energy()
+        assert abs(pe - ref.pe) <= TOL * 0.5 * ref.A.sum()
+        assert ke == pytest.approx(orc.kinetic(vel), rel=1e-13)
+        hpe, hke = ctx.energy_history()
+        assert hpe[0] == pe and hke[0] == ke
+
+
+def test_random_uniform_box(eng, orc):
+    """Non-lattice input with ragged cell occupancy and a non-cubic 3 x 4 x 5 cell grid."""
+    box = np.array([8.5, 11.2, 14.1])
+    pos = li.uniform_random(900, box, seed=11, min_sep=0.8)
+    vel = li.velocities(len(pos), 1.0)
+    with eng.LJMD(pos, vel, box) as ctx:
+        x = ctx.positions()
+        off, nbr = ctx.neighbours()
+        assert gid_pairs(off, nbr) == gid_pairs(*orc.neighbours(x, box, RN, "brute"))
+        check_forces(ctx, orc, x, box, 0.25)
+
+
+# ------------------------------------------------------------------------------ stepping
+
+def test_one_step_forces(eng, orc):
+    pos, vel, box = c1()
+    with eng.LJMD(pos, vel, box) as ctx:
+        ctx.step(1)
+        x = ctx.positions()
+        check_forces(ctx, orc, x, box, 0.25)
+
+
+def test_rebuild_neighbours_after_steps(eng, orc):
+    """After 20 steps (one rebuild, Ns = 20) the new list equals the oracle's sets on the
+    GPU's (freshly wrapped) build positions; forces at step 20 within tolerance."""
+    pos, vel, box = c1()
+    with eng.LJMD(pos, vel, box) as ctx:
+        ctx.step(20)
+        assert ctx.rebuild_steps().tolist() == [20]
+        x = ctx.positions()
+        assert np.all((x >= 0) & (x < box))
+        off, nbr = ctx.neighbours()
+        assert gid_pairs(off, nbr) == gid_pairs(*orc.neighbours(x, box, RN, "brute"))
+        check_forces(ctx, orc, x, box, 0.25)
+        ctx.step(7)
+        check_forces(ctx, orc, ctx.positions(), box, 0.25)
+
+
+def test_vv_kick_drift_bitwise(eng, orc):
+    """With F = 0 (particles beyond rc) the GPU VV updates equal the oracle's bitwise."""
+    box = np.array([30.0, 30.0, 30.0])
+    pos = np.array([[1.0, 1.0, 1.0], [10.0, 10.0, 10.0], [20.0, 5.0, 25.0]])
+    vel = np.array([[0.5, -0.25, 0.125], [-1.0, 0.3, 2.0], [0.7, 0.1, -0.9]])
+    with eng.LJMD(pos, vel, box, dt=0.0625) as ctx:
+        ctx.step(13)
+        r = orc.run(pos, vel, box, 13, dt=0.0625, mode="list")
+        assert np.array_equal(ctx.velocities(), r.vel)
+        assert np.array_equal(ctx.positions(), r.pos)
+
+
+@pytest.mark.parametrize("check", [0, 1])
+def test_trajectory_energies_100_steps(eng, orc, check):
+    """C1 (N = 4000, 100 NVE steps): sampled PE/KE/E within 1e-8 relative of the oracle run
+    with the same schedule (paper fixed Ns = 20, or the displacement-checked policy)."""
+    pos, vel, box = c1(sigma_d=0.0)
+    with eng.LJMD(pos, vel, box, rebuild_check=check) as ctx:
+        ctx.step(100)
+        pe, ke = ctx.energy_history()
+        rs = ctx.rebuild_steps()
+    r = orc.run(pos, vel, box, 100, check=check, mode="list")
+    assert rs.tolist() == r.rebuild_steps.tolist()
+    assert len(pe) == len(r.pe) == 11
+    scale = np.abs(r.pe) + np.abs(r.ke)
+    assert np.all(np.abs(pe - r.pe) <= 1e-8 * scale)
+    assert np.all(np.abs(ke - r.ke) <= 1e-8 * scale)
+    assert np.all(np.abs((pe + ke) - (r.pe + r.ke)) <= 1e-8 * np.abs(r.pe + r.ke))
+
+
+def test_step_calls_compose(eng):
+    """step(10) twice == step(20) once, bitwise (the fused epilogue splits cleanly)."""
+    pos, vel, box = c1()
+    with eng.LJMD(pos, vel, box) as a, eng.LJMD(pos, vel, box) as b:
+        a.step(20)
+        b.step(10)
+        b.step(3)
+        b.step(7)
+        assert np.array_equal(a.positions(), b.positions())
+        assert np.array_equal(a.velocities(), b.velocities())
+        assert np.array_equal(a.forces(), b.forces())
+
+
+def test_deterministic(eng):
+    pos, vel, box = c1()
+    out = []
+    for _ in range(2):
+        with eng.LJMD(pos, vel, box) as ctx:
+            ctx.step(45)
+            out.append((ctx.positions(), ctx.forces(), ctx.energy()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
+def test_set_state(eng, orc):
+    pos, vel, box = c1()
+    with eng.LJMD(pos, vel, box) as ctx:
+        ctx.step(5)
+        ctx.set_state(pos, vel)
+        assert ctx.stats()["steps_done"] == 0
+        check_forces(ctx, orc, ctx.positions(), box, 0.25)
+
+
+# ------------------------------------------------------------------------------ capacity / errors
+
+def test_capacity_regrow(eng, orc):
+    pos, vel, box = c1()
+    with eng.LJMD(pos, vel, box, nbr_capacity=8) as ctx:
+        st = ctx.stats()
+        assert st["nbr_capacity"] >= st["max_neighbours"] > 8 and st["regrows"] >= 1
+        x = ctx.positions()
+        off, nbr = ctx.neighbours()
+        assert gid_pairs(off, nbr) == gid_pairs(*orc.neighbours(x, box, RN, "brute"))
+        ctx.step(25)
+        check_forces(ctx, orc, ctx.positions(), box, 0.25)
+
+
+def test_errors(eng):
+    pos, vel, box = c1(cells=6)
+    bad = pos.copy()
+    bad[17, 1] = np.nan
+    with pytest.raises(eng.LjmdError, match="NONFINITE.*17"):
+        eng.LJMD(bad, vel, box)
+    with pytest.raises(eng.LjmdError, match="E_BOX"):
+        eng.LJMD(pos[:10], vel[:10], [8.0, 9.0, 9.0])
+    dup = pos.copy()
+    dup[5] = dup[4]
+    with pytest.raises(eng.LjmdError, match="OVERLAP"):
+        eng.LJMD(dup, vel, box)
+    with pytest.raises(eng.LjmdError, match="E_ARG"):
+        eng.LJMD(pos, vel, box, rc=-1.0)
+
+
+# ------------------------------------------------------------------------------ full size
+
+@pytest.mark.parametrize("cfg", ["C2"])
+def test_full_size_sampled(eng, orc, cfg):
+    """BASELINE configs[1] (N = 1,048,576) in the bench's launch configuration: the
+    neighbour lists and forces of 64 sampled particles (incl. box corners, seams) equal the
+    oracle's brute force computed row by row; invariants at any size: sum F ~ 0."""
+    c = li.CONFIGS[cfg]
+    pos, vel, box = c.build()
+    with eng.LJMD(pos, vel, box) as ctx:
+        ctx.step(21)
+        x = ctx.positions()
+        n = len(x)
+        rng = np.random.default_rng(0)
+        rows = np.unique(np.concatenate([[0, 1, n - 1, n - 2, n // 2], rng.integers(0, n, 59)]))
+        F = ctx.forces()
+        e = ctx.particle_energy()
+        ref = orc.forces_rows(x, box, rows, lj_of(0.25))
+        assert np.all(np.abs(F[rows] - ref.F) <= TOL * ref.S[:, None])
+        assert np.all(np.abs(e[rows] - ref.e) <= TOL * 0.5 * ref.A)
+        assert np.abs(F.sum(axis=0)).max() < 1e-8
+    # the list was rebuilt at step 20 from positions one step older: compare the sets on a
+    # fresh state built from the wrapped x (init bins and lists exactly those positions)
+    xw = orc.wrap(x, box)
+    with eng.LJMD(xw, vel, box) as ctx2:
+        off, nbr = ctx2.neighbours()
+        o2, n2 = orc.neighbours_rows(xw, box, RN, rows)
+        for r, i in enumerate(rows):
+            assert sorted(nbr[off[i]:off[i + 1]].tolist()) == n2[o2[r]:o2[r + 1]].tolist()

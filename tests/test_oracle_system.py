@@ -213,3 +213,17 @@ def test_nve_drift_and_second_order(orc):
         devs.append(np.abs(E - E[0]).max() / abs(E[0]))
     assert devs[0] < 1e-4
     assert 3.0 < devs[0] / devs[1] < 5.0
+
+
+def test_row_sampled_equals_full(orc):
+    """The row-restricted brute force (used for full-size sampled checks) equals the full one."""
+    pos, box = li.fcc(5, 5, 6)
+    pos = orc.wrap(li.perturb(pos, 0.05), box)
+    rows = np.array([0, 7, 123, len(pos) - 1])
+    full = orc.forces(pos, box, orc.LJ())
+    part = orc.forces_rows(pos, box, rows, orc.LJ())
+    assert np.array_equal(part.F, full.F[rows]) and np.array_equal(part.e, full.e[rows])
+    off, nbr = orc.neighbours(pos, box, RN, "brute")
+    o2, n2 = orc.neighbours_rows(pos, box, RN, rows)
+    for r, i in enumerate(rows):
+        assert nbr[off[i]:off[i + 1]].tolist() == n2[o2[r]:o2[r + 1]].tolist()
