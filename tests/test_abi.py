@@ -18,7 +18,7 @@ def lib():
 
 def declared():
     src = open(os.path.join(ROOT, "include", "ljmd.h")).read()
-    return sorted(set(re.findall(r"\b(ljmd_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ljmd_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(lib):
