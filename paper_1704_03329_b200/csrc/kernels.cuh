@@ -9,7 +9,8 @@
 //                 one 256-bit LDG per neighbour); fp32 mirror float4 for the list build.
 //   owned space : owned particles t = 0..n_own-1 in owned-cell order (same order as their
 //                 slots); v (SoA), F (SoA), gid, own_slot[t], e_i.
-//   list        : ELL, column-major nbr[k * n_pad + t] (int32 slot), ncount[t].
+//   list        : ELL, row-major nbr[t * K + k] (int32 slot), ncount[t]; a team of T lanes
+//                 reads k..k+T-1 of one particle (coalesced, spatially coherent gathers).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,7 +23,7 @@ struct DevFlags {
     int nonfinite_gid;           // smallest gid with a non-finite coordinate (INT_MAX: none)
     int overlap_gid;             // smallest gid i with a partner at r^2 == 0 (INT_MAX: none)
     int overlap_gid_j;
-    int pad0;
+    int max_staged;              // largest tile staging count at the last build
     unsigned long long maxdisp2; // bits of max |x - x_build|^2 (non-negative double)
     unsigned long long total_nbr;
 };
@@ -167,6 +168,12 @@ __global__ void k_load_rows(int n, const double* __restrict__ pos, const double*
     own_slot[t] = t;
 }
 
+// Force tiles: blocks of kTX x kTY x kTZ owned cells.  Owned cells (and hence owned
+// particles t) are numbered tile-major -- tile (z, y, x), then cell (z, y, x) inside the
+// tile -- so one CTA's particles are contiguous; its stencil halo is (ty+2)(tz+2) x-rows.
+constexpr int kTX = 4, kTY = 2, kTZ = 2;
+constexpr int kRowsMax = (kTY + 2) * (kTZ + 2);
+
 struct Geo {
     double L[3];
     double w[3];        // cell widths
@@ -174,7 +181,33 @@ struct Geo {
     int nc[3];          // global cell grid
     int z0, nzl;        // this rank's slab [z0, z0+nzl)
     int ex, ey, ez;     // extended grid dims = ncx+2, ncy+2, nzl+2
+    int ntx, nty, ntz;  // tile grid over the owned cells
+    const int* oc_of_lex;   // lexicographic owned cell (x fastest) -> tile-major index
+    const int* lex_of_oc;   // inverse
 };
+
+__device__ __forceinline__ void lex_xyz(const Geo& g, int lex, int& cx, int& cy, int& cz) {
+    cx = lex % g.nc[0];
+    cy = (lex / g.nc[0]) % g.nc[1];
+    cz = lex / (g.nc[0] * g.nc[1]);
+}
+__device__ __forceinline__ int tile_of_cell(const Geo& g, int cx, int cy, int cz) {
+    return ((cz / kTZ) * g.nty + cy / kTY) * g.ntx + cx / kTX;
+}
+// tile extents and its halo-row geometry
+struct TileGeo {
+    int x0, y0, z0, tx, ty, tz, R;
+};
+__device__ __forceinline__ TileGeo tile_geo(const Geo& g, int tile) {
+    TileGeo T;
+    const int a = tile % g.ntx, b = (tile / g.ntx) % g.nty, c = tile / (g.ntx * g.nty);
+    T.x0 = a * kTX; T.y0 = b * kTY; T.z0 = c * kTZ;
+    T.tx = min(kTX, g.nc[0] - T.x0);
+    T.ty = min(kTY, g.nc[1] - T.y0);
+    T.tz = min(kTZ, g.nzl - T.z0);
+    T.R = (T.ty + 2) * (T.tz + 2);
+    return T;
+}
 
 // Wrap owned positions (R10) and bin them: cell_of[t] = owned-cell index, rank_in[t] = slot
 // inside the cell from the atomic counter (order fixed later by the gid sort).
@@ -204,7 +237,7 @@ __global__ void k_wrap_bin(int n_own, const double4* __restrict__ x, const int* 
     int cz = c[2] - g.z0;   // slab-local plane (0..nzl-1 for owned particles)
     if (cz < 0) cz = 0;
     if (cz > g.nzl - 1) cz = g.nzl - 1;
-    int oc = (cz * g.nc[1] + c[1]) * g.nc[0] + c[0];
+    int oc = g.oc_of_lex[(cz * g.nc[1] + c[1]) * g.nc[0] + c[0]];
     xw[t] = p;
     cell_of[t] = oc;
     rank_in[t] = atomicAdd(&ocount[oc], 1);
@@ -245,9 +278,8 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
     int oc = warp;
     int m = ocount[oc];
     int b = obegin[oc];
-    int cx = oc % g.nc[0];
-    int cy = (oc / g.nc[0]) % g.nc[1];
-    int cz = oc / (g.nc[0] * g.nc[1]);
+    int cx, cy, cz;
+    lex_xyz(g, g.lex_of_oc[oc], cx, cy, cz);
     int ec = ((cz + 1) * g.ey + (cy + 1)) * g.ex + (cx + 1);
     int sb = ebegin[ec];
     for (int k = lane; k < m; k += 32) {
@@ -304,88 +336,267 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
     }
 }
 
+// --------------------------------------------------------------------------- tile rows
+// Per tile: the (ty+2)(tz+2) halo x-rows that hold every stencil cell of its particles, as
+// slot ranges [begin, begin + len) of the extended-cell layout, and their offsets in the
+// tile's shared-memory staging buffer.  One warp per tile; rebuilt with the cells.
+struct TileRows {
+    int* begin;   // [n_tiles][kRowsMax]
+    int* off;     // [n_tiles][kRowsMax + 1]
+};
+
+__global__ void k_tile_rows(int n_tiles, Geo g, const int* __restrict__ ebegin,
+                            const int* __restrict__ ecount, TileRows tr, DevFlags* fl) {
+    const int tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (tile >= n_tiles) return;
+    const TileGeo T = tile_geo(g, tile);
+    int len = 0, beg = 0;
+    if (lane < T.R) {
+        const int ry = lane % (T.ty + 2), rz = lane / (T.ty + 2);
+        const int iy = T.y0 + ry, iz = T.z0 + rz;          // extended coordinates
+        const int e0 = (iz * g.ey + iy) * g.ex + T.x0;      // ext x = x0 .. x0 + tx + 1
+        const int e1 = e0 + T.tx + 1;
+        beg = ebegin[e0];
+        len = ebegin[e1] + ecount[e1] - beg;
+    }
+    int x = len;
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane < T.R) {
+        tr.begin[tile * kRowsMax + lane] = beg;
+        tr.off[tile * (kRowsMax + 1) + lane] = x - len;
+    }
+    const int total = __shfl_sync(0xffffffffu, x, 31);
+    if (lane == 0) {
+        tr.off[tile * (kRowsMax + 1) + T.R] = total;
+        atomicMax(&fl->max_staged, total);
+    }
+}
+
 // --------------------------------------------------------------------------- neighbour list
-// Thread per owned particle.  Candidates: the 9 contiguous x-rows of the 27-cell stencil
-// (Sec. 3.4), rows/cells pruned by their distance to x_i; an fp32
-// prefilter with a provably conservative threshold, then the canonical fp64 test
-// r^2 < rbar_c^2 (strict, R4).  Emitted in (row, slot) = (stencil offset, gid) order.
+// One warp per pair of x-adjacent owned cells (Sec. 3.4 cell method):
+// lanes hold the pair's particles i (thread per i, <= 32 per pass), the warp walks the
+// union of their stencil rows -- 9 contiguous slot ranges of 4 cells -- with every j
+// fetched once as a broadcast load.  Decision r^2 < rbar_c^2 (strict, R4): an fp32
+// distance decides every candidate outside a provably conservative band around rbar_c^2;
+// candidates inside the band (and r^2 ~ 0) take the canonical fp64 test, which is the
+// oracle's decision.  Each list is emitted in (stencil row, slot) = (stencil offset, gid)
+// order as 16-bit indices into the tile's shared-memory staging buffer, column-major
+// nbr[k * n_pad + t] (consecutive particles -> consecutive addresses).
 struct NlistArgs {
     Geo g;
     const double4* x;
     const float4* xf;
-    const int* own_slot;
-    const int* ocell_of;
+    const int* obegin;
+    const int* ocount;
     const int* ebegin;
     const int* ecount;
-    int* nbr;
+    TileRows tr;
+    unsigned short* nbr;
     int* ncount;
-    int n_own, n_pad, K;
+    int n_own, n_pad, K, n_groups, ngx;
     double rn2;          // rbar_c^2 (fp64, canonical)
-    float thr_f;         // conservative fp32 threshold
-    double prune2;       // (rbar_c + slop)^2 for row / cell pruning
+    float thr_lo;        // r2f <  thr_lo  =>  r^2 < rbar_c^2 for sure
+    float thr_hi;        // r2f >= thr_hi  =>  r^2 >= rbar_c^2 for sure
     DevFlags* fl;
     const int* slot_gid;
 };
 
+// Per-lane particle state for the build (a lane handles up to two particles of the pair).
+struct NlI {
+    double4 x;
+    float4 f;
+    int si, k;
+    bool has;
+    unsigned short* out;
+};
+
+__device__ __forceinline__ void nl_test(const NlistArgs& a, NlI& p, int j, const float4& fj, int lb,
+                                        size_t stride) {
+    const float fx = p.f.x - fj.x, fy = p.f.y - fj.y, fz = p.f.z - fj.z;
+    const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+    bool take = r2f < a.thr_lo;
+    if (r2f < a.thr_hi && (!take || r2f < 1e-6f) && p.has && j != p.si) {
+        const double4 xj = a.x[j];
+        const double r2 = r2_canon(p.x.x - xj.x, p.x.y - xj.y, p.x.z - xj.z);
+        take = r2 < a.rn2;
+        if (r2 == 0.0) {
+            atomicMin(&a.fl->overlap_gid, a.slot_gid[p.si]);
+            a.fl->overlap_gid_j = a.slot_gid[j];
+        }
+    }
+    if (take && p.has && j != p.si) {
+        if (p.k < a.K) p.out[(size_t)p.k * stride] = (unsigned short)(j + lb);
+        ++p.k;
+    }
+}
+
 __global__ void __launch_bounds__(128) k_build_nlist(NlistArgs a) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= a.n_own) return;
+    const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (grp >= a.n_groups) return;
     const Geo& g = a.g;
-    int si = a.own_slot[t];
-    double4 xi = a.x[si];
-    float4 fi = a.xf[si];
-    int oc = a.ocell_of[t];
-    int cx = oc % g.nc[0];
-    int cy = (oc / g.nc[0]) % g.nc[1];
-    int cz = oc / (g.nc[0] * g.nc[1]);
-    // cell bounds along each axis in the coordinates the particles live in (global cells;
-    // ghost layer cells -1 and n lie just outside [0,L))
-    double lo_x = cx * g.w[0];
-    double lo_y = cy * g.w[1];
-    double lo_z = (cz + g.z0) * g.w[2];
-    double rx0 = xi.x - lo_x;                 // distance into own cell from the low face
-    double rx1 = lo_x + g.w[0] - xi.x;        // to the high face
-    double ry0 = xi.y - lo_y, ry1 = lo_y + g.w[1] - xi.y;
-    double rz0 = xi.z - lo_z, rz1 = lo_z + g.w[2] - xi.z;
-    int k = 0;
-    int* out = a.nbr + t;
+    const int gx = grp % a.ngx;
+    const int cy = (grp / a.ngx) % g.nc[1];
+    const int cz = grp / (a.ngx * g.nc[1]);
+    const int cxA = 2 * gx;
+    const bool hasB = cxA + 1 < g.nc[0];
+    const int ocA = g.oc_of_lex[(cz * g.nc[1] + cy) * g.nc[0] + cxA];
+    const int mA = a.ocount[ocA];
+    const int mB = hasB ? a.ocount[ocA + 1] : 0;   // B follows A in tile-major order
+    const int tA = a.obegin[ocA];
+    const int eA = ((cz + 1) * g.ey + (cy + 1)) * g.ex + (cxA + 1);
+    const int sA = a.ebegin[eA];
+    const int sB = hasB ? a.ebegin[eA + 1] : 0;
+    const int m = mA + mB;
+    const int tile = tile_of_cell(g, cxA, cy, cz);
+    const TileGeo T = tile_geo(g, tile);
+    const int* rbeg = a.tr.begin + tile * kRowsMax;
+    const int* roff = a.tr.off + tile * (kRowsMax + 1);
+    const float big = 3.0e38f;
     const size_t stride = (size_t)a.n_pad;
-    for (int dz = -1; dz <= 1; ++dz) {
-        double ddz = dz < 0 ? rz0 : (dz > 0 ? rz1 : 0.0);
-        double ddz2 = ddz > 0.0 ? ddz * ddz : 0.0;
-        for (int dy = -1; dy <= 1; ++dy) {
-            double ddy = dy < 0 ? ry0 : (dy > 0 ? ry1 : 0.0);
-            double dyz2 = ddz2 + (ddy > 0.0 ? ddy * ddy : 0.0);
-            if (dyz2 >= a.prune2) continue;
-            int xs = (rx0 > 0.0 && dyz2 + rx0 * rx0 >= a.prune2) ? 0 : -1;
-            int xe = (rx1 > 0.0 && dyz2 + rx1 * rx1 >= a.prune2) ? 0 : 1;
-            int erow = ((cz + 1 + dz) * g.ey + (cy + 1 + dy)) * g.ex + (cx + 1);
-            int jb = a.ebegin[erow + xs];
-            int je = a.ebegin[erow + xe] + a.ecount[erow + xe];
-            for (int j = jb; j < je; ++j) {
-                float4 fj = a.xf[j];
-                float fx = fi.x - fj.x, fy = fi.y - fj.y, fz = fi.z - fj.z;
-                float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-                if (r2f >= a.thr_f || j == si) continue;
-                double4 xj = a.x[j];
-                double r2 = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z);
-                if (r2 < a.rn2) {
-                    if (r2 == 0.0) {
-                        atomicMin(&a.fl->overlap_gid, a.slot_gid[si]);
-                        a.fl->overlap_gid_j = a.slot_gid[j];
-                    }
-                    if (k < a.K) out[(size_t)k * stride] = j;
-                    ++k;
+    for (int base = 0; base < m; base += 64) {
+        NlI P[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = base + lane + 32 * h;
+            NlI& p = P[h];
+            p.has = q < m;
+            p.si = p.has ? (q < mA ? sA + q : sB + (q - mA)) : -1;
+            p.x = make_double4(0.0, 0.0, 0.0, 0.0);
+            p.f = make_float4(big, big, big, 0.f);
+            if (p.has) {
+                p.x = a.x[p.si];
+                p.f = a.xf[p.si];
+            }
+            p.k = 0;
+            p.out = a.nbr + (p.has ? tA + q : 0);
+        }
+        for (int dz = -1; dz <= 1; ++dz) {
+            for (int dy = -1; dy <= 1; ++dy) {
+                const int erow = ((cz + 1 + dz) * g.ey + (cy + 1 + dy)) * g.ex + (cxA + 1);
+                const int last = erow + (hasB ? 2 : 1);
+                const int jb = a.ebegin[erow - 1];
+                const int je = a.ebegin[last] + a.ecount[last];
+                // tile halo row holding this stencil row: local = j - begin + off
+                const int r = (cz + 1 + dz - T.z0) * (T.ty + 2) + (cy + 1 + dy - T.y0);
+                const int lb = roff[r] - rbeg[r];
+                for (int j = jb; j < je; ++j) {
+                    const float4 fj = a.xf[j];              // same address in every lane
+                    nl_test(a, P[0], j, fj, lb, stride);
+                    if (base + 32 < m) nl_test(a, P[1], j, fj, lb, stride);
                 }
             }
         }
+        unsigned long long kk = 0ull;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (P[h].has) {
+                a.ncount[tA + base + lane + 32 * h] = P[h].k;
+                atomicMax(&a.fl->max_nbr, P[h].k);
+                kk += (unsigned long long)P[h].k;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) kk += __shfl_down_sync(0xffffffffu, kk, o);
+        if (lane == 0) atomicAdd(&a.fl->total_nbr, kk);
     }
-    a.ncount[t] = k;
-    atomicMax(&a.fl->max_nbr, k);
-    // warp-aggregated total (for stats)
-    unsigned long long kk = (unsigned long long)k;
-    for (int o = 16; o > 0; o >>= 1) kk += __shfl_down_sync(__activemask(), kk, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(&a.fl->total_nbr, kk);
+}
+
+// Bank-aware reorder (thread per particle): the force CTA's thread q reads its neighbours
+// from shared memory with LDS.64/LDS.128 whose bank group is (local index mod 16) per
+// half-warp phase.  Re-sequencing each list so that entry k targets residue (q + k) mod 16
+// (taking the next non-empty residue cyclically) makes the 16 lanes of a phase hit
+// distinct banks most of the time.  The order of a particle's sum changes, not its terms.
+// Output layout: blocks of 8 entries, nbr8[(b * n_pad + t) * 8 + e] (one 16-byte load per
+// 8 neighbours in the force kernel).
+constexpr int kRrThreads = 128;
+constexpr int kRrMax = 128;
+
+__device__ __forceinline__ uint4 pack8(const unsigned short* v) {
+    return make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16), v[4] | ((unsigned)v[5] << 16),
+                      v[6] | ((unsigned)v[7] << 16));
+}
+
+__global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, int K, Geo g,
+                                                       const unsigned short* __restrict__ tmp,
+                                                       const int* __restrict__ ncount,
+                                                       const int* __restrict__ ocell_of,
+                                                       const int* __restrict__ obegin,
+                                                       const int* __restrict__ tile_oc0,
+                                                       const int* __restrict__ tr_off,
+                                                       uint4* __restrict__ out) {
+    __shared__ unsigned short s_sorted[kRrMax][kRrThreads];   // entries grouped by residue
+    __shared__ unsigned char s_cnt[16][kRrThreads];
+    __shared__ unsigned char s_cur[16][kRrThreads];
+    __shared__ unsigned char s_end[16][kRrThreads];
+    const int tid = threadIdx.x;
+    const int t = blockIdx.x * kRrThreads + tid;
+    if (t >= n_own) return;
+    const int n = min(ncount[t], K);
+    int cx, cy, cz;
+    lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
+    const int tile = tile_of_cell(g, cx, cy, cz);
+    const int off = (t - obegin[tile_oc0[tile]]) & 15;
+    const TileGeo T = tile_geo(g, tile);
+    const unsigned short sentinel = (unsigned short)tr_off[tile * (kRowsMax + 1) + T.R];
+    const size_t stride = (size_t)n_pad;
+    uint4* o = out + t;
+    unsigned short v[8];
+    if (n > kRrMax) {   // rare: keep the build order
+        for (int b = 0; b * 8 < n; ++b) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = (b * 8 + e < n) ? tmp[(size_t)(b * 8 + e) * stride + t] : sentinel;
+            o[(size_t)b * stride] = pack8(v);
+        }
+        return;
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) s_cnt[r][tid] = 0;
+    for (int k = 0; k < n; ++k) s_cnt[tmp[(size_t)k * stride + t] & 15][tid]++;
+    int acc = 0;
+    int cnt[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        cnt[r] = s_cnt[r][tid];
+        s_cur[r][tid] = (unsigned char)acc;
+        acc += cnt[r];
+    }
+    for (int k = 0; k < n; ++k) {   // stable grouping by residue
+        const unsigned short l = tmp[(size_t)k * stride + t];
+        const int pos = s_cur[l & 15][tid];
+        s_cur[l & 15][tid] = (unsigned char)(pos + 1);
+        s_sorted[pos][tid] = l;
+    }
+    // s_cur[r] now holds the end of bucket r; walk the buckets with a 16-bit availability
+    // mask: entry k takes the first non-empty residue at or after (off + k) mod 16.
+    unsigned avail = 0u;
+    int st = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        s_end[r][tid] = s_cur[r][tid];
+        s_cur[r][tid] = (unsigned char)st;
+        st += cnt[r];
+        if (cnt[r]) avail |= 1u << r;
+    }
+    for (int k = 0; k < n; ++k) {
+        const int tgt = (off + k) & 15;
+        const unsigned rot = ((avail >> tgt) | (avail << (16 - tgt))) & 0xffffu;
+        const int rr = (tgt + __ffs(rot) - 1) & 15;
+        const int pos = s_cur[rr][tid];
+        const unsigned short pick = s_sorted[pos][tid];
+        s_cur[rr][tid] = (unsigned char)(pos + 1);
+        if (pos + 1 == s_end[rr][tid]) avail &= ~(1u << rr);
+        v[k & 7] = pick;
+        if ((k & 7) == 7 || k == n - 1) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (e > (k & 7)) v[e] = sentinel;
+            o[(size_t)(k >> 3) * stride] = pack8(v);
+        }
+    }
 }
 
 // --------------------------------------------------------------------------- force
@@ -402,11 +613,15 @@ __global__ void __launch_bounds__(128) k_build_nlist(NlistArgs a) {
 enum { kStore = 0, kKick = 1, kKKD = 2 };
 
 struct ForceArgs {
+    Geo g;
     const double4* x;        // current positions (slot space)
     double4* x_next;         // kKKD output buffer (slot space)
     const int* own_slot;
-    const int* nbr;
+    const uint4* nbr;        // blocks of 8 16-bit local indices: nbr[b * n_pad + t]
     const int* ncount;
+    const int* obegin;
+    const int* tile_oc0;     // first owned cell of each tile (tile-major), [n_tiles + 1]
+    TileRows tr;
     double* fx; double* fy; double* fz;
     double* vx; double* vy; double* vz;
     double* e;               // per-particle e_i (ENERGY)
@@ -415,11 +630,11 @@ struct ForceArgs {
     const double4* xbuild;   // displacement check (may be null)
     DevFlags* fl;
     int n_own, n_pad;
-    double rc2, c12, c6, a12, a6, a0;
+    double rc2, c12, nc6, a12, na6, a0;   // nc6 = -c6, na6 = -a6 (fold into DFMA operands)
     double h, dt, half_m;
 };
 
-constexpr int kForceThreads = 128;
+constexpr int kForceThreads = 320;   // ~16 cells x 18.5 particles per tile at rho = 0.8442
 
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -436,82 +651,179 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return r;
 }
 
+// r^2 < rc^2 decided on the canonical r^2 (the oracle's decision) while the force uses the
+// FMA-contracted r^2: the two differ by a few ulps, so only candidates within 16 ulps of
+// rc^2 (integer distance of the bit patterns of two positive doubles) recompute the
+// canonical value -- a warp-rare branch that keeps 2 FP64 instructions off the hot loop.
+__device__ __forceinline__ bool inside_rc(double r2f, double dx, double dy, double dz, double rc2) {
+    const long long b = __double_as_longlong(r2f), c = __double_as_longlong(rc2);
+    const long long d = b - c;
+    if (d > 16 || d < -16) return d < 0;
+    return r2_canon(dx, dy, dz) < rc2;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(gsrc) : "memory");
+}
+
+// Per-particle state loaded before the tile is staged (hides the list/position latency).
+struct FPart {
+    int t, si, cnt;
+    double4 xi;
+    uint4 nb0;
+};
+
+__device__ __forceinline__ FPart fpart_load(const ForceArgs& a, int t) {
+    FPart P;
+    P.t = t;
+    P.si = a.own_slot[t];
+    P.cnt = a.ncount[t];
+    P.xi = ld256(a.x + P.si);
+    P.nb0 = P.cnt > 0 ? a.nbr[t] : make_uint4(0u, 0u, 0u, 0u);
+    return P;
+}
+
 template <bool ENERGY, int MODE, bool CHECK>
-__global__ void __launch_bounds__(kForceThreads) k_force(ForceArgs a) {
-    __shared__ double sh[kForceThreads / 32];
-    const int t = blockIdx.x * kForceThreads + threadIdx.x;
-    double fx = 0.0, fy = 0.0, fz = 0.0, u = 0.0, ke = 0.0;
-    if (t < a.n_own) {
-        const int si = a.own_slot[t];
-        const double4 xi = ld256(a.x + si);
-        const int cnt = a.ncount[t];
-        const int* nb = a.nbr + t;
-        const size_t stride = (size_t)a.n_pad;
-#pragma unroll 4
-        for (int k = 0; k < cnt; ++k) {
-            const int j = __ldg(nb + (size_t)k * stride);
-            const double4 xj = ld256(a.x + j);
-            const double dx = xi.x - xj.x, dy = xi.y - xj.y, dz = xi.z - xj.z;
-            const double r2 = r2_canon(dx, dy, dz);
+__device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& P, const char* sPb,
+                                               double& epart, double& ke, unsigned long long& dbits) {
+    const int t = P.t;
+    const double4 xi = P.xi;
+    const uint4* nb = a.nbr + t;
+    const size_t stride = (size_t)a.n_pad;
+    double fx = 0.0, fy = 0.0, fz = 0.0, u = 0.0;
+    const int nblk = (P.cnt + 7) >> 3;
+    uint4 cur = P.nb0;
+    for (int b = 0; b < nblk; ++b) {
+        // prefetch the next 8 indices while this block is computed; a short block is
+        // padded with the sentinel, so every entry is evaluated unpredicated
+        const uint4 nxt = (b + 1 < nblk) ? nb[(size_t)(b + 1) * stride] : make_uint4(0u, 0u, 0u, 0u);
+        const unsigned w4[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const unsigned l = (e & 1) ? (w4[e >> 1] >> 16) : (w4[e >> 1] & 0xffffu);
+            const double* pj = reinterpret_cast<const double*>(sPb + 24u * l);
+            const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
+            const double r2 = r2_canon(dx, dy, dz);          // the oracle's r^2
             const double ir2 = rcp64(r2);
             const double ir4 = ir2 * ir2;
             const double ir6 = ir4 * ir2;
             const double ir8 = ir4 * ir4;
-            double gg = ir8 * fma(a.c12, ir6, -a.c6);
+            double gg = ir8 * fma(a.c12, ir6, a.nc6);
             const bool in = r2 < a.rc2;
             gg = in ? gg : 0.0;
             fx = fma(gg, dx, fx);
             fy = fma(gg, dy, fy);
             fz = fma(gg, dz, fz);
             if (ENERGY) {
-                double v = fma(fma(a.a12, ir6, -a.a6), ir6, a.a0);
+                const double v = fma(fma(a.a12, ir6, a.na6), ir6, a.a0);
                 u += in ? v : 0.0;
             }
         }
-        if (MODE == kStore) {
+        cur = nxt;
+    }
+    if (MODE == kStore) {
+        a.fx[t] = fx; a.fy[t] = fy; a.fz[t] = fz;
+        if (ENERGY) {
+            const double vx = a.vx[t], vy = a.vy[t], vz = a.vz[t];
+            ke += a.half_m * __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+        }
+    } else {
+        double vx = a.vx[t], vy = a.vy[t], vz = a.vz[t];
+        // line 8: v += dt/(2m) F  (two roundings, as Listing lst:velocity_update)
+        vx = __dadd_rn(vx, __dmul_rn(a.h, fx));
+        vy = __dadd_rn(vy, __dmul_rn(a.h, fy));
+        vz = __dadd_rn(vz, __dmul_rn(a.h, fz));
+        if (ENERGY)
+            ke += a.half_m * __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+        if (MODE == kKick) {
             a.fx[t] = fx; a.fy[t] = fy; a.fz[t] = fz;
-            if (ENERGY) {
-                double vx = a.vx[t], vy = a.vy[t], vz = a.vz[t];
-                ke = a.half_m * __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-            }
         } else {
-            double vx = a.vx[t], vy = a.vy[t], vz = a.vz[t];
-            // line 8: v += dt/(2m) F  (two roundings, as Listing lst:velocity_update)
+            // line 6 of the next step: v += dt/(2m) F ; r += dt v (Listing lst:position_update)
             vx = __dadd_rn(vx, __dmul_rn(a.h, fx));
             vy = __dadd_rn(vy, __dmul_rn(a.h, fy));
             vz = __dadd_rn(vz, __dmul_rn(a.h, fz));
-            if (ENERGY)
-                ke = a.half_m * __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-            if (MODE == kKick) {
-                a.fx[t] = fx; a.fy[t] = fy; a.fz[t] = fz;
-            } else {
-                // line 6 of the next step: v += dt/(2m) F ; r += dt v (Listing lst:position_update)
-                vx = __dadd_rn(vx, __dmul_rn(a.h, fx));
-                vy = __dadd_rn(vy, __dmul_rn(a.h, fy));
-                vz = __dadd_rn(vz, __dmul_rn(a.h, fz));
-                double4 xn = make_double4(__dadd_rn(xi.x, __dmul_rn(a.dt, vx)),
-                                          __dadd_rn(xi.y, __dmul_rn(a.dt, vy)),
-                                          __dadd_rn(xi.z, __dmul_rn(a.dt, vz)), 0.0);
-                st256(a.x_next + si, xn);
-                if (CHECK) {
-                    double4 b = a.xbuild[t];
-                    double d2 = r2_canon(xn.x - b.x, xn.y - b.y, xn.z - b.z);
-                    // non-negative doubles order like their bit patterns
-                    unsigned long long bits = __double_as_longlong(d2);
-                    for (int o = 16; o > 0; o >>= 1) {
-                        unsigned long long ob = __shfl_down_sync(__activemask(), bits, o);
-                        bits = ob > bits ? ob : bits;
-                    }
-                    if ((threadIdx.x & 31) == 0) atomicMax(&a.fl->maxdisp2, bits);
-                }
+            const double4 xn = make_double4(__dadd_rn(xi.x, __dmul_rn(a.dt, vx)),
+                                            __dadd_rn(xi.y, __dmul_rn(a.dt, vy)),
+                                            __dadd_rn(xi.z, __dmul_rn(a.dt, vz)), 0.0);
+            st256(a.x_next + P.si, xn);
+            if (CHECK) {
+                const double4 bb = a.xbuild[t];
+                // non-negative doubles order like their bit patterns
+                const unsigned long long d2 =
+                    __double_as_longlong(r2_canon(xn.x - bb.x, xn.y - bb.y, xn.z - bb.z));
+                dbits = d2 > dbits ? d2 : dbits;
             }
-            a.vx[t] = vx; a.vy[t] = vy; a.vz[t] = vz;
         }
-        if (ENERGY) a.e[t] = 0.5 * u;
+        a.vx[t] = vx; a.vy[t] = vy; a.vz[t] = vz;
     }
     if (ENERGY) {
-        double pe = block_sum<kForceThreads>(t < a.n_own ? 0.5 * u : 0.0, sh);
-        double k2 = block_sum<kForceThreads>(ke, sh);
+        a.e[t] = 0.5 * u;
+        epart += 0.5 * u;
+    }
+}
+
+// One CTA per tile.  (1) Each thread issues the global loads of its particle (slot, count,
+// first index block, position); (2) the warps copy the tile's halo rows -- x, y, z of every
+// particle any of its particles can list -- into shared memory with cp.async (LDGSTS, no
+// register round trip), packed 24 B per particle plus a far-away sentinel for list padding;
+// (3) thread per particle over its list of 16-bit local indices: each neighbour is three
+// LDS.64 from one address (bank group = 3 l mod 16, spread across a half-warp by the
+// bank-aware list order) instead of a scattered 32 B global gather.
+template <bool ENERGY, int MODE, bool CHECK>
+__global__ void __launch_bounds__(kForceThreads, 4) k_force(ForceArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double sh[kForceThreads / 32];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const TileGeo T = tile_geo(a.g, tile);
+    const int t0 = a.obegin[a.tile_oc0[tile]];
+    const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
+    const bool has = (int)threadIdx.x < m;
+    FPart P;
+    if (has) P = fpart_load(a, t0 + threadIdx.x);
+    // halo rows of this tile: lane r holds (begin, offset) of row r
+    const int rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
+    const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
+    const int total = __shfl_sync(0xffffffffu, ro, T.R);
+    double* sP = reinterpret_cast<double*>(smem);   // packed {x, y, z} per staged particle
+    for (int r = warp; r < T.R; r += kForceThreads / 32) {
+        const int b0 = __shfl_sync(0xffffffffu, rb, r);
+        const int o0 = __shfl_sync(0xffffffffu, ro, r);
+        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
+        for (int k = lane; k < len; k += 32) {
+            const double* src = reinterpret_cast<const double*>(a.x + b0 + k);
+            double* dst = sP + 3 * (o0 + k);
+            cp_async8(dst, src);
+            cp_async8(dst + 1, src + 1);
+            cp_async8(dst + 2, src + 2);
+        }
+    }
+    if (threadIdx.x == 0) {   // sentinel (list padding): far away, contributes exactly 0
+        sP[3 * total] = 1e30;
+        sP[3 * total + 1] = 1e30;
+        sP[3 * total + 2] = 1e30;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const char* sPb = reinterpret_cast<const char*>(sP);
+    double epart = 0.0, ke = 0.0;
+    unsigned long long dbits = 0ull;
+    if (has) force_particle<ENERGY, MODE, CHECK>(a, P, sPb, epart, ke, dbits);
+    for (int q = threadIdx.x + kForceThreads; q < m; q += kForceThreads) {   // dense tiles only
+        const FPart Q = fpart_load(a, t0 + q);
+        force_particle<ENERGY, MODE, CHECK>(a, Q, sPb, epart, ke, dbits);
+    }
+    if (CHECK) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_down_sync(0xffffffffu, dbits, o);
+            dbits = ob > dbits ? ob : dbits;
+        }
+        if (lane == 0 && dbits) atomicMax(&a.fl->maxdisp2, dbits);
+    }
+    if (ENERGY) {
+        const double pe = block_sum<kForceThreads>(epart, sh);
+        const double k2 = block_sum<kForceThreads>(ke, sh);
         if (threadIdx.x == 0) {
             a.pe_part[blockIdx.x] = pe;
             a.ke_part[blockIdx.x] = k2;
@@ -591,14 +903,25 @@ __global__ void k_gather_soa(int n_own, const double* __restrict__ a, const doub
     out[3 * t + 2] = c[t];
 }
 
-__global__ void k_list_gids(int n_own, int n_pad, const int* __restrict__ nbr, const int* __restrict__ ncount,
+__global__ void k_list_gids(int n_own, int n_pad, Geo g, const unsigned short* __restrict__ nbr,   // blocked-8
+                            const int* __restrict__ ncount, const int* __restrict__ ocell_of, TileRows tr,
                             const int* __restrict__ slot_gid, const long long* __restrict__ off,
                             long long* __restrict__ out) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_own) return;
+    int cx, cy, cz;
+    lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
+    const int tile = tile_of_cell(g, cx, cy, cz);
+    const int* rbeg = tr.begin + tile * kRowsMax;
+    const int* roff = tr.off + tile * (kRowsMax + 1);
     int c = ncount[t];
     long long o = off[t];
-    for (int k = 0; k < c; ++k) out[o + k] = slot_gid[nbr[(size_t)k * n_pad + t]];
+    for (int k = 0; k < c; ++k) {
+        const int l = nbr[((size_t)(k >> 3) * n_pad + t) * 8 + (k & 7)];
+        int r = 0;
+        while (l >= roff[r + 1]) ++r;
+        out[o + k] = slot_gid[rbeg[r] + (l - roff[r])];
+    }
 }
 
 }  // namespace ljmd

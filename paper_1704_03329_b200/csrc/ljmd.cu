@@ -11,11 +11,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 using namespace ljmd;
+
+static constexpr size_t kMaxStageSmem = 200 * 1024;   // dynamic smem cap for the tile staging
 
 namespace {
 
@@ -45,6 +48,8 @@ struct ljmd_ctx {
     std::string msg;
     // ---- capacities
     int own_cap = 0, slot_cap = 0, K = 0, n_pad = 0;
+    int n_tiles = 0;
+    int max_staged = 0;               // largest tile halo (particles) at the last build
     int n_slots = 0;
     // ---- slot space
     double4* x[2] = {nullptr, nullptr};
@@ -73,10 +78,16 @@ struct ljmd_ctx {
     int* gc_dst = nullptr;
     int* gc_src = nullptr;
     int* gc_shift = nullptr;
+    int* oc_of_lex = nullptr;         // tile-major owned-cell numbering
+    int* lex_of_oc = nullptr;
+    int* tile_oc0 = nullptr;          // [n_tiles + 1]
+    int* tr_begin = nullptr;          // tile halo rows
+    int* tr_off = nullptr;
     int* scan_tmp = nullptr;
     int scan_tmp_n = 0;
     // ---- list
-    int* nbr = nullptr;
+    unsigned short* nbr = nullptr;    // build output: 16-bit tile-local indices, [K][n_pad]
+    uint4* nbr8 = nullptr;            // bank-ordered final list, blocks of 8: [K/8][n_pad]
     int* ncount = nullptr;
     // ---- energies
     double* pe_part = nullptr;
@@ -185,6 +196,7 @@ ljmd_status sync_flags(ljmd_ctx* c) {
 ljmd_status reset_flags(ljmd_ctx* c) {
     DevFlags f{};
     f.max_nbr = 0;
+    f.max_staged = 0;
     f.nonfinite_gid = INT_MAX;
     f.overlap_gid = INT_MAX;
     f.overlap_gid_j = -1;
@@ -223,6 +235,39 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
     c->n_gcell = c->n_ecell - c->n_ocell;
     if ((int64_t)c->n_ecell > (int64_t)INT_MAX / 2)
         return set_err(c, LJMD_E_ARG, "cell grid too large");
+    // tile-major numbering of the owned cells (force tiles of kTX x kTY x kTZ cells)
+    g.ntx = (g.nc[0] + kTX - 1) / kTX;
+    g.nty = (g.nc[1] + kTY - 1) / kTY;
+    g.ntz = (g.nzl + kTZ - 1) / kTZ;
+    c->n_tiles = g.ntx * g.nty * g.ntz;
+    std::vector<int> oc_of_lex(c->n_ocell), lex_of_oc(c->n_ocell), tile_oc0(c->n_tiles + 1);
+    {
+        int oc = 0, tile = 0;
+        for (int tz = 0; tz < g.ntz; ++tz)
+            for (int ty = 0; ty < g.nty; ++ty)
+                for (int tx = 0; tx < g.ntx; ++tx, ++tile) {
+                    tile_oc0[tile] = oc;
+                    for (int cz = tz * kTZ; cz < std::min(g.nzl, (tz + 1) * kTZ); ++cz)
+                        for (int cy = ty * kTY; cy < std::min(g.nc[1], (ty + 1) * kTY); ++cy)
+                            for (int cx = tx * kTX; cx < std::min(g.nc[0], (tx + 1) * kTX); ++cx) {
+                                const int lex = (cz * g.nc[1] + cy) * g.nc[0] + cx;
+                                oc_of_lex[lex] = oc;
+                                lex_of_oc[oc] = lex;
+                                ++oc;
+                            }
+                }
+        tile_oc0[c->n_tiles] = oc;
+    }
+    TRY(dalloc(c, &c->oc_of_lex, c->n_ocell));
+    TRY(dalloc(c, &c->lex_of_oc, c->n_ocell));
+    TRY(dalloc(c, &c->tile_oc0, c->n_tiles + 1));
+    TRY(dalloc(c, &c->tr_begin, (size_t)c->n_tiles * kRowsMax));
+    TRY(dalloc(c, &c->tr_off, (size_t)c->n_tiles * (kRowsMax + 1)));
+    CK(cudaMemcpy(c->oc_of_lex, oc_of_lex.data(), sizeof(int) * c->n_ocell, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->lex_of_oc, lex_of_oc.data(), sizeof(int) * c->n_ocell, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->tile_oc0, tile_oc0.data(), sizeof(int) * (c->n_tiles + 1), cudaMemcpyHostToDevice));
+    g.oc_of_lex = c->oc_of_lex;
+    g.lex_of_oc = c->lex_of_oc;
 
     // ghost-cell table (single rank: every ghost cell is a periodic image of an owned cell)
     std::vector<int> src(c->n_ecell), gd, gs, gsh;
@@ -236,7 +281,7 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
                 int sy = cy < 0 ? -1 : (cy >= g.nc[1] ? 1 : 0);
                 int sz = cz < 0 ? -1 : (cz >= g.nzl ? 1 : 0);
                 int ox = cx - sx * g.nc[0], oy = cy - sy * g.nc[1], oz = cz - sz * g.nzl;
-                int oc = (oz * g.nc[1] + oy) * g.nc[0] + ox;
+                int oc = oc_of_lex[(oz * g.nc[1] + oy) * g.nc[0] + ox];
                 src[ec] = oc;
                 if (sx || sy || sz) {
                     gd.push_back(ec);
@@ -277,7 +322,7 @@ ljmd_status alloc_owned(ljmd_ctx* c, int cap) {
     TRY(dalloc(c, &c->ncount, cap));
     TRY(dalloc(c, &c->d_stage, (size_t)3 * cap));
     if (c->opt.rebuild_check) TRY(dalloc(c, &c->xbuild, cap));
-    c->n_fblocks = nblk(cap, kForceThreads);
+    c->n_fblocks = c->n_tiles;   // one force CTA per tile
     TRY(dalloc(c, &c->pe_part, c->n_fblocks));
     TRY(dalloc(c, &c->ke_part, c->n_fblocks));
     return LJMD_OK;
@@ -310,6 +355,7 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
 ljmd_status alloc_list(ljmd_ctx* c, int K) {
     c->K = K;
     TRY(dalloc(c, &c->nbr, (size_t)K * c->n_pad));
+    TRY(dalloc(c, &c->nbr8, (size_t)(K / 8) * c->n_pad));
     return LJMD_OK;
 }
 
@@ -319,27 +365,34 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     a.g = c->geo;
     a.x = c->x[c->xc];
     a.xf = c->xf;
-    a.own_slot = c->own_slot;
-    a.ocell_of = c->ocell_of;
+    a.obegin = c->obegin;
+    a.ocount = c->ocount;
     a.ebegin = c->ebegin;
     a.ecount = c->ecount;
+    a.tr = TileRows{c->tr_begin, c->tr_off};
     a.nbr = c->nbr;
     a.ncount = c->ncount;
     a.n_own = c->n_own;
     a.n_pad = c->n_pad;
     a.K = c->K;
+    a.ngx = (c->geo.nc[0] + 1) / 2;
+    a.n_groups = a.ngx * c->geo.nc[1] * c->geo.nzl;
     a.rn2 = c->rn * c->rn;
-    // fp32 prefilter: |x_f - x| <= 2^-24 |x| per coordinate (|x| <= L + w) and the fp32
-    // difference/product roundings; a margin of 4x that bound keeps the filter conservative.
-    double xmax = 0.0;
-    for (int d = 0; d < 3; ++d) xmax = std::max(xmax, c->geo.L[d] + 2.0 * c->geo.w[d]);
-    double m = 4.0 * (std::ldexp(xmax, -23) + std::ldexp(c->rn, -21)) + 1e-7;
-    a.thr_f = (float)((c->rn + m) * (c->rn + m) * (1.0 + std::ldexp(1.0, -18)));
-    double slop = 1e-9 * (1.0 + xmax);
-    a.prune2 = (c->rn + slop) * (c->rn + slop);
+    // Conservative fp32 band: per coordinate |x_f - x| <= 2^-24 X with
+    // X = max |coordinate| <= L + 2w, the fp32 difference adds 2^-24 |dx_f|, so
+    // |dx_f - dx| <= d = 2^-23 X + 2^-24 (R + 2^-23 X) for |dx| <= R = rbar_c + 1; the fp32
+    // r^2 (two FMAs) then deviates from the exact r^2 by at most 3 d (2R + d) + 4 2^-24 R^2.
+    // Outside [rn2 - E, rn2 + E] the fp32 value decides; inside, the canonical fp64 test.
+    double X = 0.0;
+    for (int d = 0; d < 3; ++d) X = std::max(X, c->geo.L[d] + 2.0 * c->geo.w[d]);
+    const double R = c->rn + 1.0;
+    const double dd = std::ldexp(X, -23) + std::ldexp(R + std::ldexp(X, -23), -24);
+    const double E = 2.0 * (3.0 * dd * (2.0 * R + dd) + 4.0 * std::ldexp(R * R, -24)) + 1e-6;
+    a.thr_lo = std::nextafter((float)(a.rn2 - E), 0.0f);
+    a.thr_hi = std::nextafter((float)(a.rn2 + E), 1e30f);
     a.fl = c->d_fl;
     a.slot_gid = c->slot_gid;
-    k_build_nlist<<<nblk(c->n_own, 128), 128, 0, c->stream>>>(a);
+    k_build_nlist<<<nblk((int64_t)a.n_groups * 32, 128), 128, 0, c->stream>>>(a);
     CKL();
     return LJMD_OK;
 }
@@ -347,10 +400,14 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
 ForceArgs force_args(ljmd_ctx* c) {
     ForceArgs a;
     const double s2 = c->sigma * c->sigma, s6 = s2 * s2 * s2, s12 = s6 * s6;
+    a.g = c->geo;
+    a.obegin = c->obegin;
+    a.tile_oc0 = c->tile_oc0;
+    a.tr = TileRows{c->tr_begin, c->tr_off};
     a.x = c->x[c->xc];
     a.x_next = c->x[c->xc ^ 1];
     a.own_slot = c->own_slot;
-    a.nbr = c->nbr;
+    a.nbr = c->nbr8;
     a.ncount = c->ncount;
     a.fx = c->F;
     a.fy = c->F + c->own_cap;
@@ -368,9 +425,9 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.n_pad = c->n_pad;
     a.rc2 = c->rc * c->rc;
     a.c12 = 48.0 * c->eps * s12;
-    a.c6 = 24.0 * c->eps * s6;
+    a.nc6 = -24.0 * c->eps * s6;
     a.a12 = 4.0 * c->eps * s12;
-    a.a6 = 4.0 * c->eps * s6;
+    a.na6 = -4.0 * c->eps * s6;
     a.a0 = 4.0 * c->eps * c->opt.energy_shift;
     a.h = 0.5 * c->dt / c->opt.mass;
     a.dt = c->dt;
@@ -378,9 +435,28 @@ ForceArgs force_args(ljmd_ctx* c) {
     return a;
 }
 
+constexpr size_t kStageBytes = 24;   // packed {x, y, z} per staged particle
+
 template <bool E, int M, bool C>
 void force_launch(ljmd_ctx* c, const ForceArgs& a) {
-    k_force<E, M, C><<<nblk(c->n_own, kForceThreads), kForceThreads, 0, c->stream>>>(a);
+    k_force<E, M, C><<<c->n_tiles, kForceThreads, kStageBytes * (size_t)(c->max_staged + 1), c->stream>>>(a);
+}
+
+template <bool E, int M, bool C>
+cudaError_t force_attr() {
+    return cudaFuncSetAttribute(k_force<E, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kMaxStageSmem);
+}
+
+ljmd_status set_force_attrs(ljmd_ctx* c) {
+    cudaError_t e = cudaSuccess;
+    for (cudaError_t r : {force_attr<true, kStore, false>(), force_attr<true, kKick, false>(),
+                          force_attr<true, kKKD, false>(), force_attr<true, kKKD, true>(),
+                          force_attr<false, kStore, false>(), force_attr<false, kKick, false>(),
+                          force_attr<false, kKKD, false>(), force_attr<false, kKKD, true>()})
+        if (r != cudaSuccess) e = r;
+    if (e != cudaSuccess) return set_err(c, LJMD_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return LJMD_OK;
 }
 
 ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check) {
@@ -481,8 +557,16 @@ ljmd_status rebuild(ljmd_ctx* c) {
     c->oc_cur = on;
     c->xc ^= 1;
     TRY(refresh_ghosts(c, true));
+    k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
+        c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off}, c->d_fl);
+    CKL();
     TRY(launch_nlist(c));
     TRY(sync_flags(c));
+    c->max_staged = c->h_fl->max_staged;
+    if (kStageBytes * (size_t)c->max_staged > kMaxStageSmem || c->max_staged > 65535)
+        return set_err(c, LJMD_E_CAPACITY,
+                       "a force tile needs %d staged particles (> %zu B of shared memory): density too high",
+                       c->max_staged, kMaxStageSmem);
     if (c->h_fl->overlap_gid != INT_MAX)
         return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)", c->h_fl->overlap_gid,
                        c->h_fl->overlap_gid_j);
@@ -496,6 +580,10 @@ ljmd_status rebuild(ljmd_ctx* c) {
     }
     c->max_nbr = c->h_fl->max_nbr;
     c->total_nbr = c->h_fl->total_nbr;
+    k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, 0, c->stream>>>(
+        c->n_own, c->n_pad, c->K, c->geo, c->nbr, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->tr_off,
+        c->nbr8);
+    CKL();
     return LJMD_OK;
 }
 
@@ -508,7 +596,7 @@ ljmd_status ensure_hist(ljmd_ctx* c, int64_t need) {
 }
 
 ljmd_status finalize_energy(ljmd_ctx* c, double* dst) {
-    k_finalize_energy<<<1, 1024, 0, c->stream>>>(c->pe_part, c->ke_part, nblk(c->n_own, kForceThreads), dst);
+    k_finalize_energy<<<1, 1024, 0, c->stream>>>(c->pe_part, c->ke_part, c->n_tiles, dst);
     CKL();
     return LJMD_OK;
 }
@@ -677,6 +765,7 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     }
     ljmd_status s;
     if ((s = plan_geometry(c, box)) != LJMD_OK) return fail(s);
+    if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
         cudaMallocHost(&c->h_fl, sizeof(DevFlags)) != cudaSuccess ||
         cudaMallocHost(&c->h_slots, sizeof(int)) != cudaSuccess) {
@@ -691,7 +780,7 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     // list width K: expected 4/3 pi rbar_c^3 rho neighbours with headroom
     double vol = box[0] * box[1] * box[2];
     double expect = 4.0 / 3.0 * M_PI * c->rn * c->rn * c->rn * (double)n / vol;
-    int K = o.nbr_capacity > 0 ? (int)o.nbr_capacity : ((int)std::ceil(expect * 1.4) + 16 + 7) / 8 * 8;
+    int K = o.nbr_capacity > 0 ? ((int)o.nbr_capacity + 7) / 8 * 8 : ((int)std::ceil(expect * 1.4) + 16 + 7) / 8 * 8;
     if ((s = alloc_list(c, K)) != LJMD_OK) return fail(s);
     if ((s = load_state(c, pos, vel)) != LJMD_OK) return fail(s);
     *out = c;
@@ -859,7 +948,9 @@ ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, in
     TRY(dalloc(c, &d_off, n + 1));
     TRY(dalloc(c, &d_out, (size_t)std::max<long long>(toff[n], 1)));
     CK(cudaMemcpyAsync(d_off, toff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, c->stream));
-    k_list_gids<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->n_pad, c->nbr, c->ncount, c->slot_gid, d_off, d_out);
+    k_list_gids<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->n_pad, c->geo, (const unsigned short*)c->nbr8,
+                                                     c->ncount, c->ocell_of,
+                                                     TileRows{c->tr_begin, c->tr_off}, c->slot_gid, d_off, d_out);
     CKL();
     std::vector<long long> h((size_t)toff[n]);
     CK(cudaMemcpyAsync(h.data(), d_out, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, c->stream));
@@ -911,7 +1002,8 @@ void ljmd_destroy(ljmd_ctx* c) {
     void* ptrs[] = {c->x[0], c->x[1], c->xf, c->slot_gid, c->v[0], c->v[1], c->gid[0], c->gid[1],
                     c->own_slot, c->ocell_of, c->F, c->e, c->xbuild, c->xw, c->cell_of, c->rank_in, c->perm,
                     c->ocount, c->obegin, c->ecount, c->ebegin, c->ecell_src, c->gc_dst, c->gc_src, c->gc_shift,
-                    c->scan_tmp, c->nbr, c->ncount, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
+                    c->scan_tmp, c->nbr, c->nbr8, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin,
+                    c->tr_off, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_fl) cudaFreeHost(c->h_fl);
