@@ -260,8 +260,10 @@ __global__ void k_scatter(int n_own, const int* __restrict__ cell_of, const int*
     perm[obegin[cell_of[t]] + rank_in[t]] = t;
 }
 
-// One warp per owned cell: order members by gid (deterministic layout, reading R15),
-// write the new owned-space arrays and the owned slots of the new slot space.
+// One warp per owned cell: order members by (x, gid) -- deterministic (reading R15), and
+// every 3-cell stencil row of the extended layout is then sorted by x, so the list build
+// can binary-search each particle's x-window -- and write the new owned-space arrays and
+// the owned slots of the new slot space.
 __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
                             const int* __restrict__ ocount, const int* __restrict__ ebegin,
                             const int* __restrict__ perm, const int* __restrict__ gid_old,
@@ -285,8 +287,14 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
     for (int k = lane; k < m; k += 32) {
         int t_old = perm[b + k];
         int gk = gid_old[t_old];
+        const double xk = xw[t_old].x;
         int r = 0;
-        for (int s = 0; s < m; ++s) r += (gid_old[perm[b + s]] < gk);
+        for (int s = 0; s < m; ++s) {
+            const int ts = perm[b + s];
+            const double xs = xw[ts].x;
+            const int gs = gid_old[ts];
+            r += (xs < xk) || (xs == xk && gs < gk);
+        }
         int t = b + r;
         int slot = sb + r;
         double4 p = xw[t_old];
@@ -384,8 +392,9 @@ __global__ void k_tile_rows(int n_tiles, Geo g, const int* __restrict__ ebegin,
 // distance decides every candidate outside a provably conservative band around rbar_c^2;
 // candidates inside the band (and r^2 ~ 0) take the canonical fp64 test, which is the
 // oracle's decision.  Each list is emitted in (stencil row, slot) = (stencil offset, gid)
-// order as 16-bit indices into the tile's shared-memory staging buffer, column-major
-// nbr[k * n_pad + t] (consecutive particles -> consecutive addresses).
+// order as 16-bit indices into the tile's shared-memory staging buffer, in blocks of 8
+// (nbr8[b * n_pad + t], one 16-byte load per 8 neighbours in the force kernel; the last
+// block is padded with the tile's sentinel index).
 struct NlistArgs {
     Geo g;
     const double4* x;
@@ -394,9 +403,15 @@ struct NlistArgs {
     const int* ocount;
     const int* ebegin;
     const int* ecount;
+    const int* own_slot;
+    const int* ocell_of;
+    const int* tile_oc0;
     TileRows tr;
-    unsigned short* nbr;
+    uint4* nbr8;         // blocks of 8 16-bit local indices, nbr8[b * n_pad + t] (force layout)
     int* ncount;
+    const float* ylo_f;  // fp32 faces of the owned cells along y: ylo_f[cy] = cy * w_y, cy = 0..ncy
+    const float* zlo_f;  // along z, slab-local: zlo_f[cz] = (z0 + cz) * w_z, cz = 0..nzl
+    float slop_f;        // fp32 margin for the row / x-window pruning (conservative)
     int n_own, n_pad, K, n_groups, ngx;
     double rn2;          // rbar_c^2 (fp64, canonical)
     float thr_lo;        // r2f <  thr_lo  =>  r^2 < rbar_c^2 for sure
@@ -405,198 +420,132 @@ struct NlistArgs {
     const int* slot_gid;
 };
 
-// Per-lane particle state for the build (a lane handles up to two particles of the pair).
-struct NlI {
-    double4 x;
-    float4 f;
-    int si, k;
-    bool has;
-    unsigned short* out;
-};
+// One CTA per force tile (the same halo rows and local numbering as k_force): the fp32
+// mirror of the halo is staged in shared memory with cp.async, then thread per particle
+// walks its 9 stencil rows as local-index ranges.  Lanes of one cell walk the same j
+// sequence (broadcast LDS).  Output: build-order (stencil row, slot) local indices,
+// blocks of 8 entries written with 16-byte stores from registers.
+constexpr int kBuildThreads = 320;
 
-__device__ __forceinline__ void nl_test(const NlistArgs& a, NlI& p, int j, const float4& fj, int lb,
-                                        size_t stride) {
-    const float fx = p.f.x - fj.x, fy = p.f.y - fj.y, fz = p.f.z - fj.z;
-    const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-    bool take = r2f < a.thr_lo;
-    if (r2f < a.thr_hi && (!take || r2f < 1e-6f) && p.has && j != p.si) {
-        const double4 xj = a.x[j];
-        const double r2 = r2_canon(p.x.x - xj.x, p.x.y - xj.y, p.x.z - xj.z);
-        take = r2 < a.rn2;
-        if (r2 == 0.0) {
-            atomicMin(&a.fl->overlap_gid, a.slot_gid[p.si]);
-            a.fl->overlap_gid_j = a.slot_gid[j];
-        }
-    }
-    if (take && p.has && j != p.si) {
-        if (p.k < a.K) p.out[(size_t)p.k * stride] = (unsigned short)(j + lb);
-        ++p.k;
-    }
-}
-
-__global__ void __launch_bounds__(128) k_build_nlist(NlistArgs a) {
-    const int grp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (grp >= a.n_groups) return;
+__global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Geo& g = a.g;
-    const int gx = grp % a.ngx;
-    const int cy = (grp / a.ngx) % g.nc[1];
-    const int cz = grp / (a.ngx * g.nc[1]);
-    const int cxA = 2 * gx;
-    const bool hasB = cxA + 1 < g.nc[0];
-    const int ocA = g.oc_of_lex[(cz * g.nc[1] + cy) * g.nc[0] + cxA];
-    const int mA = a.ocount[ocA];
-    const int mB = hasB ? a.ocount[ocA + 1] : 0;   // B follows A in tile-major order
-    const int tA = a.obegin[ocA];
-    const int eA = ((cz + 1) * g.ey + (cy + 1)) * g.ex + (cxA + 1);
-    const int sA = a.ebegin[eA];
-    const int sB = hasB ? a.ebegin[eA + 1] : 0;
-    const int m = mA + mB;
-    const int tile = tile_of_cell(g, cxA, cy, cz);
     const TileGeo T = tile_geo(g, tile);
-    const int* rbeg = a.tr.begin + tile * kRowsMax;
-    const int* roff = a.tr.off + tile * (kRowsMax + 1);
-    const float big = 3.0e38f;
-    const size_t stride = (size_t)a.n_pad;
-    for (int base = 0; base < m; base += 64) {
-        NlI P[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int q = base + lane + 32 * h;
-            NlI& p = P[h];
-            p.has = q < m;
-            p.si = p.has ? (q < mA ? sA + q : sB + (q - mA)) : -1;
-            p.x = make_double4(0.0, 0.0, 0.0, 0.0);
-            p.f = make_float4(big, big, big, 0.f);
-            if (p.has) {
-                p.x = a.x[p.si];
-                p.f = a.xf[p.si];
-            }
-            p.k = 0;
-            p.out = a.nbr + (p.has ? tA + q : 0);
+    const int t0 = a.obegin[a.tile_oc0[tile]];
+    const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
+    const int rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
+    const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
+    float4* sF = reinterpret_cast<float4*>(smem);
+    for (int r = warp; r < T.R; r += kBuildThreads / 32) {
+        const int b0 = __shfl_sync(0xffffffffu, rb, r);
+        const int o0 = __shfl_sync(0xffffffffu, ro, r);
+        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
+        for (int k = lane; k < len; k += 32) {
+            const unsigned d = (unsigned)__cvta_generic_to_shared(sF + o0 + k);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" :: "r"(d), "l"(a.xf + b0 + k) : "memory");
         }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const size_t stride = (size_t)a.n_pad;
+    unsigned long long kk = 0ull;
+    for (int q = threadIdx.x; q < m; q += kBuildThreads) {
+        const int t = t0 + q;
+        const int si = a.own_slot[t];
+        int cx, cy, cz;
+        lex_xyz(g, g.lex_of_oc[a.ocell_of[t]], cx, cy, cz);
+        const double4 xi = a.x[si];
+        // own row (dy = dz = 0) gives the particle's own local index (self exclusion)
+        const int r0 = (cz + 1 - T.z0) * (T.ty + 2) + (cy + 1 - T.y0);
+        const int li = a.tr.off[tile * (kRowsMax + 1) + r0] + si - a.tr.begin[tile * kRowsMax + r0];
+        const float4 fi = sF[li];
+        uint4* out = a.nbr8 + t;
+        unsigned pk[4] = {0u, 0u, 0u, 0u};   // 8 pending 16-bit entries -> one 16-byte store
+        int k = 0;
         for (int dz = -1; dz <= 1; ++dz) {
+            const float ddz = dz < 0 ? fi.z - a.zlo_f[cz] : (dz > 0 ? a.zlo_f[cz + 1] - fi.z : 0.f);
             for (int dy = -1; dy <= 1; ++dy) {
-                const int erow = ((cz + 1 + dz) * g.ey + (cy + 1 + dy)) * g.ex + (cxA + 1);
-                const int last = erow + (hasB ? 2 : 1);
-                const int jb = a.ebegin[erow - 1];
-                const int je = a.ebegin[last] + a.ecount[last];
-                // tile halo row holding this stencil row: local = j - begin + off
+                const float ddy = dy < 0 ? fi.y - a.ylo_f[cy] : (dy > 0 ? a.ylo_f[cy + 1] - fi.y : 0.f);
+                // conservative x half-width of the sphere slice through this row
+                const float dyz2 = fmaxf(ddy - a.slop_f, 0.f) * fmaxf(ddy - a.slop_f, 0.f) +
+                                   fmaxf(ddz - a.slop_f, 0.f) * fmaxf(ddz - a.slop_f, 0.f);
+                if (dyz2 >= a.thr_hi) continue;
+                const float xw = sqrtf(a.thr_hi - dyz2) + a.slop_f;
                 const int r = (cz + 1 + dz - T.z0) * (T.ty + 2) + (cy + 1 + dy - T.y0);
-                const int lb = roff[r] - rbeg[r];
-                for (int j = jb; j < je; ++j) {
-                    const float4 fj = a.xf[j];              // same address in every lane
-                    nl_test(a, P[0], j, fj, lb, stride);
-                    if (base + 32 < m) nl_test(a, P[1], j, fj, lb, stride);
+                const int rbeg = a.tr.begin[tile * kRowsMax + r];
+                const int roff = a.tr.off[tile * (kRowsMax + 1) + r];
+                const int e0 = ((cz + 1 + dz) * g.ey + (cy + 1 + dy)) * g.ex + cx;   // ext x = cx
+                int lo = roff + a.ebegin[e0] - rbeg;
+                int hi = roff + a.ebegin[e0 + 2] + a.ecount[e0 + 2] - rbeg;
+                // the row is sorted by x: first j with x_j >= x_i - xw, first j with x_j > x_i + xw
+                {
+                    const float xl = fi.x - xw, xh = fi.x + xw;
+                    int l0 = lo, l1 = hi;
+                    while (l0 < l1) {
+                        const int mid = (l0 + l1) >> 1;
+                        if (sF[mid].x < xl) l0 = mid + 1; else l1 = mid;
+                    }
+                    int h0 = l0, h1 = hi;
+                    while (h0 < h1) {
+                        const int mid = (h0 + h1) >> 1;
+                        if (sF[mid].x <= xh) h0 = mid + 1; else h1 = mid;
+                    }
+                    lo = l0;
+                    hi = h0;
+                }
+                for (int jl = lo; jl < hi; ++jl) {
+                    const float4 fj = sF[jl];
+                    const float fx = fi.x - fj.x, fy = fi.y - fj.y, fz = fi.z - fj.z;
+                    const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+                    if (r2f >= a.thr_hi || jl == li) continue;
+                    bool take = r2f < a.thr_lo;
+                    if (!take || r2f < 1e-6f) {          // rare: decide in fp64 (the oracle's test)
+                        const int j = rbeg + (jl - roff);
+                        const double4 xj = a.x[j];
+                        const double r2 = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z);
+                        take = r2 < a.rn2;
+                        if (r2 == 0.0) {
+                            atomicMin(&a.fl->overlap_gid, a.slot_gid[si]);
+                            a.fl->overlap_gid_j = a.slot_gid[j];
+                        }
+                    }
+                    if (take) {
+                        if (k < a.K) {
+                            const int e = k & 7;
+                            const unsigned sh = (e & 1) * 16;
+                            const unsigned val = (unsigned)jl << sh;
+                            const unsigned msk = ~(0xffffu << sh);
+                            if ((e >> 1) == 0) pk[0] = (pk[0] & msk) | val;
+                            if ((e >> 1) == 1) pk[1] = (pk[1] & msk) | val;
+                            if ((e >> 1) == 2) pk[2] = (pk[2] & msk) | val;
+                            if ((e >> 1) == 3) pk[3] = (pk[3] & msk) | val;
+                            if (e == 7) out[(size_t)(k >> 3) * stride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        }
+                        ++k;
+                    }
                 }
             }
         }
-        unsigned long long kk = 0ull;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (P[h].has) {
-                a.ncount[tA + base + lane + 32 * h] = P[h].k;
-                atomicMax(&a.fl->max_nbr, P[h].k);
-                kk += (unsigned long long)P[h].k;
+        if ((k & 7) && k < a.K) {   // pad the last block with the tile's sentinel index
+            const unsigned sen = (unsigned)a.tr.off[tile * (kRowsMax + 1) + T.R];
+            for (int e = k & 7; e < 8; ++e) {
+                const unsigned sh = (e & 1) * 16;
+                const unsigned msk = ~(0xffffu << sh);
+                if ((e >> 1) == 0) pk[0] = (pk[0] & msk) | (sen << sh);
+                if ((e >> 1) == 1) pk[1] = (pk[1] & msk) | (sen << sh);
+                if ((e >> 1) == 2) pk[2] = (pk[2] & msk) | (sen << sh);
+                if ((e >> 1) == 3) pk[3] = (pk[3] & msk) | (sen << sh);
             }
+            out[(size_t)(k >> 3) * stride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
-        for (int o = 16; o > 0; o >>= 1) kk += __shfl_down_sync(0xffffffffu, kk, o);
-        if (lane == 0) atomicAdd(&a.fl->total_nbr, kk);
+        a.ncount[t] = k;
+        atomicMax(&a.fl->max_nbr, k);
+        kk += (unsigned long long)k;
     }
-}
-
-// Bank-aware reorder (thread per particle): the force CTA's thread q reads its neighbours
-// from shared memory with LDS.64/LDS.128 whose bank group is (local index mod 16) per
-// half-warp phase.  Re-sequencing each list so that entry k targets residue (q + k) mod 16
-// (taking the next non-empty residue cyclically) makes the 16 lanes of a phase hit
-// distinct banks most of the time.  The order of a particle's sum changes, not its terms.
-// Output layout: blocks of 8 entries, nbr8[(b * n_pad + t) * 8 + e] (one 16-byte load per
-// 8 neighbours in the force kernel).
-constexpr int kRrThreads = 128;
-constexpr int kRrMax = 128;
-
-__device__ __forceinline__ uint4 pack8(const unsigned short* v) {
-    return make_uint4(v[0] | ((unsigned)v[1] << 16), v[2] | ((unsigned)v[3] << 16), v[4] | ((unsigned)v[5] << 16),
-                      v[6] | ((unsigned)v[7] << 16));
-}
-
-__global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, int K, Geo g,
-                                                       const unsigned short* __restrict__ tmp,
-                                                       const int* __restrict__ ncount,
-                                                       const int* __restrict__ ocell_of,
-                                                       const int* __restrict__ obegin,
-                                                       const int* __restrict__ tile_oc0,
-                                                       const int* __restrict__ tr_off,
-                                                       uint4* __restrict__ out) {
-    __shared__ unsigned short s_sorted[kRrMax][kRrThreads];   // entries grouped by residue
-    __shared__ unsigned char s_cnt[16][kRrThreads];
-    __shared__ unsigned char s_cur[16][kRrThreads];
-    __shared__ unsigned char s_end[16][kRrThreads];
-    const int tid = threadIdx.x;
-    const int t = blockIdx.x * kRrThreads + tid;
-    if (t >= n_own) return;
-    const int n = min(ncount[t], K);
-    int cx, cy, cz;
-    lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
-    const int tile = tile_of_cell(g, cx, cy, cz);
-    const int off = (t - obegin[tile_oc0[tile]]) & 15;
-    const TileGeo T = tile_geo(g, tile);
-    const unsigned short sentinel = (unsigned short)tr_off[tile * (kRowsMax + 1) + T.R];
-    const size_t stride = (size_t)n_pad;
-    uint4* o = out + t;
-    unsigned short v[8];
-    if (n > kRrMax) {   // rare: keep the build order
-        for (int b = 0; b * 8 < n; ++b) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[e] = (b * 8 + e < n) ? tmp[(size_t)(b * 8 + e) * stride + t] : sentinel;
-            o[(size_t)b * stride] = pack8(v);
-        }
-        return;
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) s_cnt[r][tid] = 0;
-    for (int k = 0; k < n; ++k) s_cnt[tmp[(size_t)k * stride + t] & 15][tid]++;
-    int acc = 0;
-    int cnt[16];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        cnt[r] = s_cnt[r][tid];
-        s_cur[r][tid] = (unsigned char)acc;
-        acc += cnt[r];
-    }
-    for (int k = 0; k < n; ++k) {   // stable grouping by residue
-        const unsigned short l = tmp[(size_t)k * stride + t];
-        const int pos = s_cur[l & 15][tid];
-        s_cur[l & 15][tid] = (unsigned char)(pos + 1);
-        s_sorted[pos][tid] = l;
-    }
-    // s_cur[r] now holds the end of bucket r; walk the buckets with a 16-bit availability
-    // mask: entry k takes the first non-empty residue at or after (off + k) mod 16.
-    unsigned avail = 0u;
-    int st = 0;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        s_end[r][tid] = s_cur[r][tid];
-        s_cur[r][tid] = (unsigned char)st;
-        st += cnt[r];
-        if (cnt[r]) avail |= 1u << r;
-    }
-    for (int k = 0; k < n; ++k) {
-        const int tgt = (off + k) & 15;
-        const unsigned rot = ((avail >> tgt) | (avail << (16 - tgt))) & 0xffffu;
-        const int rr = (tgt + __ffs(rot) - 1) & 15;
-        const int pos = s_cur[rr][tid];
-        const unsigned short pick = s_sorted[pos][tid];
-        s_cur[rr][tid] = (unsigned char)(pos + 1);
-        if (pos + 1 == s_end[rr][tid]) avail &= ~(1u << rr);
-        v[k & 7] = pick;
-        if ((k & 7) == 7 || k == n - 1) {
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-                if (e > (k & 7)) v[e] = sentinel;
-            o[(size_t)(k >> 3) * stride] = pack8(v);
-        }
-    }
+    for (int o = 16; o > 0; o >>= 1) kk += __shfl_down_sync(0xffffffffu, kk, o);
+    if (lane == 0 && kk) atomicAdd(&a.fl->total_nbr, kk);
 }
 
 // --------------------------------------------------------------------------- force

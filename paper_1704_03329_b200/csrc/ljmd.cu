@@ -82,12 +82,13 @@ struct ljmd_ctx {
     int* lex_of_oc = nullptr;
     int* tile_oc0 = nullptr;          // [n_tiles + 1]
     int* tr_begin = nullptr;          // tile halo rows
+    float* ylo_f = nullptr;           // fp32 cell faces (list-build pruning)
+    float* zlo_f = nullptr;
     int* tr_off = nullptr;
     int* scan_tmp = nullptr;
     int scan_tmp_n = 0;
     // ---- list
-    unsigned short* nbr = nullptr;    // build output: 16-bit tile-local indices, [K][n_pad]
-    uint4* nbr8 = nullptr;            // bank-ordered final list, blocks of 8: [K/8][n_pad]
+    uint4* nbr8 = nullptr;            // 16-bit tile-local indices in blocks of 8: [K/8][n_pad]
     int* ncount = nullptr;
     // ---- energies
     double* pe_part = nullptr;
@@ -268,6 +269,15 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
     CK(cudaMemcpy(c->tile_oc0, tile_oc0.data(), sizeof(int) * (c->n_tiles + 1), cudaMemcpyHostToDevice));
     g.oc_of_lex = c->oc_of_lex;
     g.lex_of_oc = c->lex_of_oc;
+    {
+        std::vector<float> yf(g.nc[1] + 1), zf(g.nzl + 1);
+        for (int k = 0; k <= g.nc[1]; ++k) yf[k] = (float)(k * g.w[1]);
+        for (int k = 0; k <= g.nzl; ++k) zf[k] = (float)((g.z0 + k) * g.w[2]);
+        TRY(dalloc(c, &c->ylo_f, yf.size()));
+        TRY(dalloc(c, &c->zlo_f, zf.size()));
+        CK(cudaMemcpy(c->ylo_f, yf.data(), sizeof(float) * yf.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->zlo_f, zf.data(), sizeof(float) * zf.size(), cudaMemcpyHostToDevice));
+    }
 
     // ghost-cell table (single rank: every ghost cell is a periodic image of an owned cell)
     std::vector<int> src(c->n_ecell), gd, gs, gsh;
@@ -354,7 +364,6 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
 
 ljmd_status alloc_list(ljmd_ctx* c, int K) {
     c->K = K;
-    TRY(dalloc(c, &c->nbr, (size_t)K * c->n_pad));
     TRY(dalloc(c, &c->nbr8, (size_t)(K / 8) * c->n_pad));
     return LJMD_OK;
 }
@@ -370,7 +379,7 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     a.ebegin = c->ebegin;
     a.ecount = c->ecount;
     a.tr = TileRows{c->tr_begin, c->tr_off};
-    a.nbr = c->nbr;
+    a.nbr8 = c->nbr8;
     a.ncount = c->ncount;
     a.n_own = c->n_own;
     a.n_pad = c->n_pad;
@@ -392,7 +401,15 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     a.thr_hi = std::nextafter((float)(a.rn2 + E), 1e30f);
     a.fl = c->d_fl;
     a.slot_gid = c->slot_gid;
-    k_build_nlist<<<nblk((int64_t)a.n_groups * 32, 128), 128, 0, c->stream>>>(a);
+    a.own_slot = c->own_slot;
+    a.ocell_of = c->ocell_of;
+    a.tile_oc0 = c->tile_oc0;
+    a.ylo_f = c->ylo_f;
+    a.zlo_f = c->zlo_f;
+    // fp32 pruning margin: position conversion (2^-24 X twice), face conversion, sqrt/fma
+    // roundings -- 16 x the coordinate ulp plus an absolute floor
+    a.slop_f = (float)(16.0 * std::ldexp(X, -23) + 1e-5);
+    k_build_nlist<<<c->n_tiles, kBuildThreads, sizeof(float4) * (size_t)c->max_staged, c->stream>>>(a);
     CKL();
     return LJMD_OK;
 }
@@ -449,7 +466,7 @@ cudaError_t force_attr() {
 }
 
 ljmd_status set_force_attrs(ljmd_ctx* c) {
-    cudaError_t e = cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_build_nlist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStageSmem);
     for (cudaError_t r : {force_attr<true, kStore, false>(), force_attr<true, kKick, false>(),
                           force_attr<true, kKKD, false>(), force_attr<true, kKKD, true>(),
                           force_attr<false, kStore, false>(), force_attr<false, kKick, false>(),
@@ -560,13 +577,14 @@ ljmd_status rebuild(ljmd_ctx* c) {
     k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
         c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off}, c->d_fl);
     CKL();
-    TRY(launch_nlist(c));
     TRY(sync_flags(c));
     c->max_staged = c->h_fl->max_staged;
-    if (kStageBytes * (size_t)c->max_staged > kMaxStageSmem || c->max_staged > 65535)
+    if (16 * (size_t)(c->max_staged + 1) > kMaxStageSmem || c->max_staged > 65535)
         return set_err(c, LJMD_E_CAPACITY,
                        "a force tile needs %d staged particles (> %zu B of shared memory): density too high",
                        c->max_staged, kMaxStageSmem);
+    TRY(launch_nlist(c));
+    TRY(sync_flags(c));
     if (c->h_fl->overlap_gid != INT_MAX)
         return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)", c->h_fl->overlap_gid,
                        c->h_fl->overlap_gid_j);
@@ -580,10 +598,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     }
     c->max_nbr = c->h_fl->max_nbr;
     c->total_nbr = c->h_fl->total_nbr;
-    k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, 0, c->stream>>>(
-        c->n_own, c->n_pad, c->K, c->geo, c->nbr, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->tr_off,
-        c->nbr8);
-    CKL();
+
     return LJMD_OK;
 }
 
@@ -1002,7 +1017,7 @@ void ljmd_destroy(ljmd_ctx* c) {
     void* ptrs[] = {c->x[0], c->x[1], c->xf, c->slot_gid, c->v[0], c->v[1], c->gid[0], c->gid[1],
                     c->own_slot, c->ocell_of, c->F, c->e, c->xbuild, c->xw, c->cell_of, c->rank_in, c->perm,
                     c->ocount, c->obegin, c->ecount, c->ebegin, c->ecell_src, c->gc_dst, c->gc_src, c->gc_shift,
-                    c->scan_tmp, c->nbr, c->nbr8, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin,
+                    c->scan_tmp, c->nbr8, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin, c->ylo_f, c->zlo_f,
                     c->tr_off, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
