@@ -148,6 +148,14 @@ void ljmd_destroy(ljmd_ctx* c);
 /* Library version string, e.g. "ljmd 0.1 sm_100a". */
 const char* ljmd_version(void);
 
+/* Multi-GPU plumbing: fill out128 with a fresh ncclUniqueId (NCCL is loaded with dlopen;
+ * the copy torch already mapped is reused).  Rank 0 calls it and broadcasts the 128
+ * bytes (e.g. with torch.distributed) into ljmd_options.nccl_id on every rank.  An id
+ * that starts with "LJMDLOCAL" instead selects the in-process loopback transport (several
+ * contexts of one process exchanging through device copies; used by the tests to run the
+ * multi-rank path on one GPU). */
+ljmd_status ljmd_nccl_unique_id(void* out128);
+
 /* Measurement utility (bench.py roofline denominator): FP64 FMA throughput of the
  * device, from a DFMA-chain probe kernel timed with CUDA events (best of 5), in
  * TFLOP/s (2 flops per FMA).  device = -1: current device. */

@@ -24,6 +24,8 @@ struct DevFlags {
     int overlap_gid;             // smallest gid i with a partner at r^2 == 0 (INT_MAX: none)
     int overlap_gid_j;
     int max_staged;              // largest tile staging count at the last build
+    int migrate_gid;             // a particle that moved further than one cell plane (INT_MAX: none)
+    int pad1;
     unsigned long long maxdisp2; // bits of max |x - x_build|^2 (non-negative double)
     unsigned long long total_nbr;
 };
@@ -150,21 +152,23 @@ __global__ void k_scan_down(const int* __restrict__ in, int n, const int* __rest
 
 // --------------------------------------------------------------------------- init / binning
 // Load caller rows [n][3] (pos, vel) into owned space with identity order (t = gid).
+// gid_in: caller row of each loaded particle (nullptr: identity, single rank)
 __global__ void k_load_rows(int n, const double* __restrict__ pos, const double* __restrict__ vel,
                             double4* __restrict__ x, double* __restrict__ vx, double* __restrict__ vy,
                             double* __restrict__ vz, int* __restrict__ gid, int* __restrict__ own_slot,
-                            DevFlags* fl) {
+                            const int* __restrict__ gid_in, DevFlags* fl) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     double a = pos[3 * t], b = pos[3 * t + 1], c = pos[3 * t + 2];
     double p = vel[3 * t], q = vel[3 * t + 1], r = vel[3 * t + 2];
+    const int gi = gid_in ? gid_in[t] : t;
     if (!(isfinite(a) && isfinite(b) && isfinite(c) && isfinite(p) && isfinite(q) && isfinite(r)))
-        atomicMin(&fl->nonfinite_gid, t);
+        atomicMin(&fl->nonfinite_gid, gi);
     x[t] = make_double4(a, b, c, 0.0);
     vx[t] = p;
     vy[t] = q;
     vz[t] = r;
-    gid[t] = t;
+    gid[t] = gi;
     own_slot[t] = t;
 }
 
@@ -245,12 +249,15 @@ __global__ void k_wrap_bin(int n_own, const double4* __restrict__ x, const int* 
 
 // Extended-cell counts: owned cells take their own count, ghost cells the count of
 // their source cell (ghost table built on the host at init).
+// ecell_src[ec] >= 0: owned cell whose particles (or periodic images) fill ec;
+// ecell_src[ec] < 0: cell -(src+1) of the planes received from the z neighbours (nranks > 1).
 __global__ void k_ext_counts(int n_ecell, const int* __restrict__ ocount, Geo g,
-                             const int* __restrict__ ecell_src, int* __restrict__ ecount) {
+                             const int* __restrict__ ecell_src, const int* __restrict__ recv_cnt,
+                             int* __restrict__ ecount) {
     int ec = blockIdx.x * blockDim.x + threadIdx.x;
     if (ec >= n_ecell) return;
-    int src = ecell_src[ec];   // owned-cell index whose particles fill this cell
-    ecount[ec] = ocount[src];
+    int src = ecell_src[ec];
+    ecount[ec] = src >= 0 ? ocount[src] : recv_cnt[-src - 1];
 }
 
 __global__ void k_scatter(int n_own, const int* __restrict__ cell_of, const int* __restrict__ rank_in,
@@ -321,15 +328,27 @@ struct GhostCells {
     int n;
 };
 
+// Sources: gc.src >= 0 -> extended cell (local owned slots); gc.src < 0 -> received plane
+// cell -(src+1), stored after the slot range at n_slots + recv_off[cell] (nranks > 1).
 template <bool AT_BUILD>
 __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
                                 const int* __restrict__ ecount, Geo g, double4* __restrict__ x,
-                                float4* __restrict__ xf, int* __restrict__ slot_gid) {
+                                float4* __restrict__ xf, int* __restrict__ slot_gid,
+                                const int* __restrict__ recv_cnt, const int* __restrict__ recv_off,
+                                int n_slots) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= gc.n) return;
     int d = gc.dst[warp], s = gc.src[warp], code = gc.shift[warp];
-    int db = ebegin[d], sb = ebegin[s], m = ecount[s];
+    int db = ebegin[d];
+    int sb, m;
+    if (s >= 0) {
+        sb = ebegin[s];
+        m = ecount[s];
+    } else {
+        sb = n_slots + recv_off[-s - 1];
+        m = recv_cnt[-s - 1];
+    }
     double sx = (double)((code & 3) - 1), sy = (double)(((code >> 2) & 3) - 1),
            sz = (double)(((code >> 4) & 3) - 1);
     double Lx = sx * g.L[0], Ly = sy * g.L[1], Lz = sz * g.L[2];   // exact
@@ -342,6 +361,128 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
             slot_gid[db + k] = slot_gid[sb + k];
         }
     }
+}
+
+// --------------------------------------------------------------------------- z-slab decomposition
+// (spatial decomposition, halo cells, particle migration every n steps)
+struct MigRec {           // one migrating particle: wrapped position, velocity, gid (64 B)
+    double x, y, z, vx, vy, vz;
+    long long gid;
+    long long pad;
+};
+
+// Wrap every owned particle (R10), find its owner slab by global cell plane; stayers are
+// copied to the compact arrays (atomic slot, order fixed later by the cell sort), leavers
+// to the send buffer of the lower / upper neighbour.
+__global__ void k_migrate_mark(int n_own, const double4* __restrict__ x, const int* __restrict__ own_slot,
+                               const double* __restrict__ vx, const double* __restrict__ vy,
+                               const double* __restrict__ vz, const int* __restrict__ gid, Geo g,
+                               double4* __restrict__ xs, double* __restrict__ vxs, double* __restrict__ vys,
+                               double* __restrict__ vzs, int* __restrict__ gids, MigRec* __restrict__ lo,
+                               MigRec* __restrict__ hi, int cap_mig, int* __restrict__ counters,
+                               DevFlags* fl) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_own) return;
+    double4 p = x[own_slot[t]];
+    if (!(isfinite(p.x) && isfinite(p.y) && isfinite(p.z))) {
+        atomicMin(&fl->nonfinite_gid, gid[t]);
+        p = make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+    p.x = wrap_coord(p.x, g.L[0]);
+    p.y = wrap_coord(p.y, g.L[1]);
+    p.z = wrap_coord(p.z, g.L[2]);
+    p.w = 0.0;
+    int cz = (int)floor(__ddiv_rn(p.z, g.w[2]));
+    cz = cz < 0 ? 0 : (cz > g.nc[2] - 1 ? g.nc[2] - 1 : cz);
+    int dir = 0;
+    if (cz < g.z0 || cz >= g.z0 + g.nzl) {
+        // only the adjacent planes are reachable between rebuilds (displacement < w)
+        if (cz == (g.z0 - 1 + g.nc[2]) % g.nc[2]) dir = -1;
+        else if (cz == (g.z0 + g.nzl) % g.nc[2]) dir = 1;
+        else {
+            atomicMin(&fl->migrate_gid, gid[t]);
+            dir = -1;
+        }
+    }
+    if (dir == 0) {
+        const int k = atomicAdd(&counters[0], 1);
+        xs[k] = p;
+        vxs[k] = vx[t];
+        vys[k] = vy[t];
+        vzs[k] = vz[t];
+        gids[k] = gid[t];
+    } else {
+        const int k = atomicAdd(&counters[dir < 0 ? 1 : 2], 1);
+        if (k < cap_mig) {
+            MigRec r;
+            r.x = p.x; r.y = p.y; r.z = p.z;
+            r.vx = vx[t]; r.vy = vy[t]; r.vz = vz[t];
+            r.gid = gid[t];
+            r.pad = 0;
+            (dir < 0 ? lo : hi)[k] = r;
+        }
+    }
+}
+
+// append the received migrants after the n_stay stayers
+__global__ void k_migrate_append(int n_in, int base, const MigRec* __restrict__ in, double4* __restrict__ xs,
+                                 double* __restrict__ vxs, double* __restrict__ vys, double* __restrict__ vzs,
+                                 int* __restrict__ gids) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_in) return;
+    const MigRec r = in[k];
+    xs[base + k] = make_double4(r.x, r.y, r.z, 0.0);
+    vxs[base + k] = r.vx;
+    vys[base + k] = r.vy;
+    vzs[base + k] = r.vz;
+    gids[base + k] = (int)r.gid;
+}
+
+__global__ void k_iota(int n, int* __restrict__ out) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) out[k] = k;
+}
+
+// per-cell counts of the bottom (side 0) and top (side 1) owned planes, lex (cy, cx) order
+__global__ void k_plane_counts(Geo g, const int* __restrict__ ocount, int* __restrict__ send_cnt) {
+    const int npc = g.nc[0] * g.nc[1];
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= 2 * npc) return;
+    const int side = k / npc, c = k % npc;
+    const int cz = side == 0 ? 0 : g.nzl - 1;
+    send_cnt[k] = ocount[g.oc_of_lex[cz * npc + c]];
+}
+
+// slot index of every particle of the two boundary planes, in (cy, cx, cell order)
+__global__ void k_plane_index(Geo g, const int* __restrict__ send_cnt, const int* __restrict__ send_off,
+                              const int* __restrict__ ebegin, int* __restrict__ send_idx) {
+    const int npc = g.nc[0] * g.nc[1];
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= 2 * npc) return;
+    const int side = warp / npc, c = warp % npc;
+    const int cx = c % g.nc[0], cy = c / g.nc[0];
+    const int iz = side == 0 ? 1 : g.nzl;
+    const int ec = (iz * g.ey + (cy + 1)) * g.ex + (cx + 1);
+    const int b = ebegin[ec], m = send_cnt[warp], o = send_off[warp];
+    for (int k = lane; k < m; k += 32) send_idx[o + k] = b + k;
+}
+
+// gather the boundary-plane positions (w = gid) into the send buffer
+__global__ void k_pack(int n, const int* __restrict__ idx, const double4* __restrict__ x,
+                       const int* __restrict__ slot_gid, double4* __restrict__ out) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int s = idx[k];
+    double4 p = ld256(x + s);
+    p.w = (double)slot_gid[s];
+    st256(out + k, p);
+}
+
+// received plane particles: gid from the w component (at build)
+__global__ void k_unpack_gid(int n, const double4* __restrict__ xr, int* __restrict__ gid_out) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) gid_out[k] = (int)xr[k].w;
 }
 
 // --------------------------------------------------------------------------- tile rows

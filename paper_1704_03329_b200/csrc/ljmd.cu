@@ -3,6 +3,7 @@
 // and the velocity-Verlet step loop (Alg. alg:VelocityVerlet).
 #include "../../include/ljmd.h"
 #include "kernels.cuh"
+#include "transport.h"
 
 #include <cuda_runtime.h>
 
@@ -112,6 +113,27 @@ struct ljmd_ctx {
     int64_t force_launches = 0;
     double force_ms = 0.0;
     int64_t kernel_launches = 0;   // launches of this library's kernels (CKL after each)
+    // ---- z-slab decomposition (nranks > 1)
+    Transport* tr = nullptr;
+    int rank = 0, nranks = 1, lo_rank = 0, hi_rank = 0, npc = 0;
+    int* send_cnt = nullptr;      // [2 * npc] bottom / top plane cell counts
+    int* send_off = nullptr;      // [2 * npc + 1]
+    int* recv_cnt = nullptr;      // [2 * npc] lower / upper ghost plane cell counts
+    int* recv_off = nullptr;      // [2 * npc + 1]
+    int* send_idx = nullptr;      // slot of every boundary-plane particle
+    double4* send_buf = nullptr;
+    int send_cap = 0;
+    int n_send[2] = {0, 0}, n_recv[2] = {0, 0};
+    MigRec* mig_send[2] = {nullptr, nullptr};
+    MigRec* mig_recv[2] = {nullptr, nullptr};
+    int mig_cap = 0;
+    int* mig_cnt = nullptr;       // device [3]: stay, lo, hi ; [3..5]: received counts
+    int* h_mig = nullptr;         // pinned mirror
+    double4* xs = nullptr;        // compacted (post-migration) positions / velocities / gids
+    double* vs = nullptr;
+    int* gs = nullptr;
+    int* iota = nullptr;
+    int* h_tot = nullptr;         // pinned: send/recv plane totals
 };
 
 namespace {
@@ -198,6 +220,7 @@ ljmd_status reset_flags(ljmd_ctx* c) {
     DevFlags f{};
     f.max_nbr = 0;
     f.max_staged = 0;
+    f.migrate_gid = INT_MAX;
     f.nonfinite_gid = INT_MAX;
     f.overlap_gid = INT_MAX;
     f.overlap_gid_j = -1;
@@ -279,9 +302,14 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
         CK(cudaMemcpy(c->zlo_f, zf.data(), sizeof(float) * zf.size(), cudaMemcpyHostToDevice));
     }
 
-    // ghost-cell table (single rank: every ghost cell is a periodic image of an owned cell)
+    // ghost-cell table.  Single rank: every ghost cell is a periodic image of an owned cell.
+    // nranks > 1: the two z-ghost planes hold the neighbours' boundary planes (received each
+    // step, source index -(cell + 1) into the receive region; images in x/y of those cells
+    // too); the periodic z shift applies on the ranks at z = 0 and z = Lz.
     std::vector<int> src(c->n_ecell), gd, gs, gsh;
     gd.reserve(c->n_gcell);
+    const int npc = g.nc[0] * g.nc[1];
+    const bool split = c->opt.nranks > 1;
     for (int iz = 0; iz < g.ez; ++iz)
         for (int iy = 0; iy < g.ey; ++iy)
             for (int ix = 0; ix < g.ex; ++ix) {
@@ -291,6 +319,15 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
                 int sy = cy < 0 ? -1 : (cy >= g.nc[1] ? 1 : 0);
                 int sz = cz < 0 ? -1 : (cz >= g.nzl ? 1 : 0);
                 int ox = cx - sx * g.nc[0], oy = cy - sy * g.nc[1], oz = cz - sz * g.nzl;
+                if (split && sz != 0) {
+                    const int rc = (sz < 0 ? 0 : npc) + oy * g.nc[0] + ox;
+                    const int zs = (sz < 0 && g.z0 == 0) ? -1 : ((sz > 0 && g.z0 + g.nzl == g.nc[2]) ? 1 : 0);
+                    src[ec] = -(rc + 1);
+                    gd.push_back(ec);
+                    gs.push_back(-(rc + 1));
+                    gsh.push_back((sx + 1) | ((sy + 1) << 2) | ((zs + 1) << 4));
+                    continue;
+                }
                 int oc = oc_of_lex[(oz * g.nc[1] + oy) * g.nc[0] + ox];
                 src[ec] = oc;
                 if (sx || sy || sz) {
@@ -299,6 +336,13 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
                     gsh.push_back((sx + 1) | ((sy + 1) << 2) | ((sz + 1) << 4));
                 }
             }
+    c->npc = npc;
+    if (split) {
+        TRY(dalloc(c, &c->send_cnt, 2 * npc));
+        TRY(dalloc(c, &c->send_off, 2 * npc + 1));
+        TRY(dalloc(c, &c->recv_cnt, 2 * npc));
+        TRY(dalloc(c, &c->recv_off, 2 * npc + 1));
+    }
     TRY(dalloc(c, &c->ecell_src, c->n_ecell));
     TRY(dalloc(c, &c->gc_dst, c->n_gcell));
     TRY(dalloc(c, &c->gc_src, c->n_gcell));
@@ -519,17 +563,96 @@ ljmd_status collect_profile(ljmd_ctx* c, int64_t first_launch) {
     return LJMD_OK;
 }
 
+// Grouped exchange with the z neighbours, in the fixed order that also pairs correctly for
+// nranks = 2 (both neighbours are the same rank): send (up, down), receive (from below,
+// from above).  hi/lo payloads: what goes to the upper / lower neighbour.
+ljmd_status exchange(ljmd_ctx* c, void* to_hi, size_t b_hi, void* to_lo, size_t b_lo, void* from_lo, size_t r_lo,
+                     void* from_hi, size_t r_hi) {
+    std::vector<Xfer> sends{{c->hi_rank, to_hi, b_hi}, {c->lo_rank, to_lo, b_lo}};
+    std::vector<Xfer> recvs{{c->lo_rank, from_lo, r_lo}, {c->hi_rank, from_hi, r_hi}};
+    std::string err;
+    if (!c->tr->exchange(c->stream, sends, recvs, err)) return set_err(c, LJMD_E_NCCL, "%s", err.c_str());
+    return LJMD_OK;
+}
+
+ljmd_status allreduce(ljmd_ctx* c, double* dbuf, int n, bool max) {
+    if (!c->tr) return LJMD_OK;
+    std::string err;
+    if (!c->tr->allreduce(c->stream, dbuf, n, max, err)) return set_err(c, LJMD_E_NCCL, "%s", err.c_str());
+    return LJMD_OK;
+}
+
+// Halo: the boundary planes' positions travel to the neighbours' ghost planes, received
+// after the slot range of the current position buffer (nranks > 1, every step).
+ljmd_status halo_exchange(ljmd_ctx* c) {
+    const int ns = c->n_send[0] + c->n_send[1];
+    if (ns) {
+        k_pack<<<nblk(ns, 256), 256, 0, c->stream>>>(ns, c->send_idx, c->x[c->xc], c->slot_gid, c->send_buf);
+        CKL();
+    }
+    double4* rx = c->x[c->xc] + c->n_slots;
+    const size_t e = sizeof(double4);
+    return exchange(c, c->send_buf + c->n_send[0], e * c->n_send[1], c->send_buf, e * c->n_send[0], rx,
+                    e * c->n_recv[0], rx + c->n_recv[0], e * c->n_recv[1]);
+}
+
 ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
     GhostCells gc{c->gc_dst, c->gc_src, c->gc_shift, c->n_gcell};
     int blocks = nblk((int64_t)c->n_gcell * 32, 256);
     if (c->n_gcell == 0) return LJMD_OK;
     if (at_build)
         k_ghost_refresh<true><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo, c->x[c->xc],
-                                                             c->xf, c->slot_gid);
+                                                             c->xf, c->slot_gid, c->recv_cnt, c->recv_off,
+                                                             c->n_slots);
     else
         k_ghost_refresh<false><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo,
-                                                              c->x[c->xc], c->xf, c->slot_gid);
+                                                              c->x[c->xc], c->xf, c->slot_gid, c->recv_cnt,
+                                                              c->recv_off, c->n_slots);
     CKL();
+    return LJMD_OK;
+}
+
+// Particle migration: leavers of the slab go to the adjacent rank; stayers and
+// arrivals are compacted into (xs, vs, gs), the input of the binning below.
+ljmd_status migrate(ljmd_ctx* c) {
+    const int n = c->n_own;
+    CK(cudaMemsetAsync(c->mig_cnt, 0, sizeof(int) * 6, c->stream));
+    const double* v = c->v[c->oc_cur];
+    const size_t oc = c->own_cap;
+    k_migrate_mark<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc,
+                                                       c->gid[c->oc_cur], c->geo, c->xs, c->vs, c->vs + oc,
+                                                       c->vs + 2 * oc, c->gs, c->mig_send[0], c->mig_send[1],
+                                                       c->mig_cap, c->mig_cnt, c->d_fl);
+    CKL();
+    TRY(exchange(c, c->mig_cnt + 2, sizeof(int), c->mig_cnt + 1, sizeof(int), c->mig_cnt + 3, sizeof(int),
+                 c->mig_cnt + 4, sizeof(int)));
+    CK(cudaMemcpyAsync(c->h_mig, c->mig_cnt, sizeof(int) * 6, cudaMemcpyDeviceToHost, c->stream));
+    TRY(sync_flags(c));
+    if (c->h_fl->migrate_gid != INT_MAX)
+        return set_err(c, LJMD_E_ARG, "particle %d moved more than one cell plane between rebuilds",
+                       c->h_fl->migrate_gid);
+    const int stay = c->h_mig[0], out_lo = c->h_mig[1], out_hi = c->h_mig[2];
+    const int in_lo = c->h_mig[3], in_hi = c->h_mig[4];
+    if (out_lo > c->mig_cap || out_hi > c->mig_cap || in_lo > c->mig_cap || in_hi > c->mig_cap)
+        return set_err(c, LJMD_E_CAPACITY, "migration buffer overflow (%d/%d/%d/%d > %d)", out_lo, out_hi, in_lo,
+                       in_hi, c->mig_cap);
+    if (stay + in_lo + in_hi > c->own_cap)
+        return set_err(c, LJMD_E_CAPACITY, "rank %d would own %d particles (capacity %d)", c->rank,
+                       stay + in_lo + in_hi, c->own_cap);
+    const size_t r = sizeof(MigRec);
+    TRY(exchange(c, c->mig_send[1], r * out_hi, c->mig_send[0], r * out_lo, c->mig_recv[0], r * in_lo,
+                 c->mig_recv[1], r * in_hi));
+    if (in_lo) {
+        k_migrate_append<<<nblk(in_lo, 256), 256, 0, c->stream>>>(in_lo, stay, c->mig_recv[0], c->xs, c->vs,
+                                                                  c->vs + oc, c->vs + 2 * oc, c->gs);
+        CKL();
+    }
+    if (in_hi) {
+        k_migrate_append<<<nblk(in_hi, 256), 256, 0, c->stream>>>(in_hi, stay + in_lo, c->mig_recv[1], c->xs,
+                                                                  c->vs, c->vs + oc, c->vs + 2 * oc, c->gs);
+        CKL();
+    }
+    c->n_own = stay + in_lo + in_hi;
     return LJMD_OK;
 }
 
@@ -538,14 +661,40 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
 ljmd_status rebuild(ljmd_ctx* c) {
     TRY(reset_flags(c));
     CK(cudaMemsetAsync(c->ocount, 0, sizeof(int) * c->n_ocell, c->stream));
-    const int n = c->n_own;
+    // input of the binning: the current owned particles, or the post-migration compaction
+    const double4* xin = c->x[c->xc];
+    const int* slot_in = c->own_slot;
+    const double* vo = c->v[c->oc_cur];
     const int* gid_old = c->gid[c->oc_cur];
-    k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, c->geo, c->xw, c->ocount,
-                                                    c->cell_of, c->rank_in, gid_old, c->d_fl);
+    if (c->nranks > 1) {
+        TRY(migrate(c));
+        k_iota<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->iota);
+        CKL();
+        xin = c->xs;
+        slot_in = c->iota;
+        vo = c->vs;
+        gid_old = c->gs;
+    }
+    const int n = c->n_own;
+    k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, xin, slot_in, c->geo, c->xw, c->ocount, c->cell_of,
+                                                    c->rank_in, gid_old, c->d_fl);
     CKL();
+    if (c->nranks > 1) {   // boundary-plane cell counts -> the neighbours' ghost planes
+        const int npc = c->npc;
+        k_plane_counts<<<nblk(2 * npc, 256), 256, 0, c->stream>>>(c->geo, c->ocount, c->send_cnt);
+        CKL();
+        TRY(exchange(c, c->send_cnt + npc, sizeof(int) * npc, c->send_cnt, sizeof(int) * npc, c->recv_cnt,
+                     sizeof(int) * npc, c->recv_cnt + npc, sizeof(int) * npc));
+        TRY(scan(c, c->send_cnt, 2 * npc, c->send_off));
+        TRY(scan(c, c->recv_cnt, 2 * npc, c->recv_off));
+        CK(cudaMemcpyAsync(c->h_tot, c->send_off + npc, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_tot + 1, c->send_off + 2 * npc, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_tot + 2, c->recv_off + npc, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->h_tot + 3, c->recv_off + 2 * npc, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    }
     TRY(scan(c, c->ocount, c->n_ocell, c->obegin));
     k_ext_counts<<<nblk(c->n_ecell, 256), 256, 0, c->stream>>>(c->n_ecell, c->ocount, c->geo, c->ecell_src,
-                                                              c->ecount);
+                                                              c->recv_cnt, c->ecount);
     CKL();
     TRY(scan(c, c->ecount, c->n_ecell, c->ebegin));
     CK(cudaMemcpyAsync(c->h_slots, c->ebegin + c->n_ecell, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -554,15 +703,28 @@ ljmd_status rebuild(ljmd_ctx* c) {
         return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
                        c->h_fl->nonfinite_gid);
     const int need = *c->h_slots;
-    if (need > c->slot_cap) {
-        TRY(alloc_slots(c, (int)std::min<int64_t>((int64_t)need * 5 / 4 + 1024, INT_MAX), true));
+    int n_recv_tot = 0;
+    if (c->nranks > 1) {
+        c->n_send[0] = c->h_tot[0];
+        c->n_send[1] = c->h_tot[1] - c->h_tot[0];
+        c->n_recv[0] = c->h_tot[2];
+        c->n_recv[1] = c->h_tot[3] - c->h_tot[2];
+        n_recv_tot = c->h_tot[3];
+        const int ns = c->h_tot[1];
+        if (ns > c->send_cap) {
+            c->send_cap = ns * 5 / 4 + 1024;
+            TRY(dalloc(c, &c->send_idx, c->send_cap));
+            TRY(dalloc(c, &c->send_buf, c->send_cap));
+        }
+    }
+    if (need + n_recv_tot > c->slot_cap) {
+        TRY(alloc_slots(c, (int)std::min<int64_t>((int64_t)(need + n_recv_tot) * 5 / 4 + 1024, INT_MAX), true));
         ++c->regrows;
     }
     c->n_slots = need;
     k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm);
     CKL();
     const int on = c->oc_cur ^ 1;
-    const double* vo = c->v[c->oc_cur];
     double* vn = c->v[on];
     const size_t oc = c->own_cap;
     double4* xn = c->x[c->xc ^ 1];
@@ -573,6 +735,18 @@ ljmd_status rebuild(ljmd_ctx* c) {
     CKL();
     c->oc_cur = on;
     c->xc ^= 1;
+    if (c->nranks > 1) {   // ghost planes: positions + gids of the neighbours' boundary planes
+        k_plane_index<<<nblk((int64_t)2 * c->npc * 32, 256), 256, 0, c->stream>>>(c->geo, c->send_cnt,
+                                                                                  c->send_off, c->ebegin,
+                                                                                  c->send_idx);
+        CKL();
+        TRY(halo_exchange(c));
+        if (n_recv_tot) {
+            k_unpack_gid<<<nblk(n_recv_tot, 256), 256, 0, c->stream>>>(n_recv_tot, c->x[c->xc] + c->n_slots,
+                                                                        c->slot_gid + c->n_slots);
+            CKL();
+        }
+    }
     TRY(refresh_ghosts(c, true));
     k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
         c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off}, c->d_fl);
@@ -627,24 +801,56 @@ ljmd_status pull_hist(ljmd_ctx* c, int64_t count) {
 
 // init sequence shared by ljmd_init and ljmd_set_state
 ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
-    const int64_t n = c->n_global;
+    int64_t n = c->n_global;
+    std::vector<double> fp, fv;
+    std::vector<int> fg;
+    if (c->nranks > 1) {
+        // initial owner by z plane, computed on the host; the first rebuild's migration
+        // corrects the rare plane-boundary disagreement with the device binning
+        const Geo& g = c->geo;
+        for (int64_t i = 0; i < n; ++i) {
+            double z = pos[3 * i + 2];
+            if (!std::isfinite(z)) return set_err(c, LJMD_E_NONFINITE, "non-finite position at particle %lld",
+                                                  (long long)i);
+            z = z - g.L[2] * std::floor(z / g.L[2]);
+            int cz = (int)std::floor(z / g.w[2]);
+            cz = std::min(std::max(cz, 0), g.nc[2] - 1);
+            if (cz < g.z0 || cz >= g.z0 + g.nzl) continue;
+            for (int d = 0; d < 3; ++d) {
+                fp.push_back(pos[3 * i + d]);
+                fv.push_back(vel[3 * i + d]);
+            }
+            fg.push_back((int)i);
+        }
+        n = (int64_t)fg.size();
+        if (n > c->own_cap) return set_err(c, LJMD_E_CAPACITY, "slab holds %lld particles (capacity %d)",
+                                           (long long)n, c->own_cap);
+        pos = fp.data();
+        vel = fv.data();
+    }
     double* dpos = nullptr;
     double* dvel = nullptr;
+    int* dg = nullptr;
     TRY(dalloc(c, &dpos, (size_t)3 * n));
     TRY(dalloc(c, &dvel, (size_t)3 * n));
     CK(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dvel, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    if (c->nranks > 1) {
+        TRY(dalloc(c, &dg, (size_t)n));
+        CK(cudaMemcpyAsync(dg, fg.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    }
     TRY(reset_flags(c));
     c->oc_cur = 0;
     c->xc = 0;
     double* v = c->v[0];
     const size_t oc = c->own_cap;
     k_load_rows<<<nblk(n, 256), 256, 0, c->stream>>>((int)n, dpos, dvel, c->x[0], v, v + oc, v + 2 * oc,
-                                                    c->gid[0], c->own_slot, c->d_fl);
+                                                    c->gid[0], c->own_slot, dg, c->d_fl);
     CKL();
     TRY(sync_flags(c));
     cudaFree(dpos);
     cudaFree(dvel);
+    if (dg) cudaFree(dg);
     if (c->h_fl->nonfinite_gid != INT_MAX)
         return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
                        c->h_fl->nonfinite_gid);
@@ -658,6 +864,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
     TRY(ensure_hist(c, 1));
     TRY(launch_force(c, true, kStore, false));
     TRY(finalize_energy(c, c->hist));
+    TRY(allreduce(c, c->hist, 2, false));
     TRY(pull_hist(c, 1));
     return LJMD_OK;
 }
@@ -742,8 +949,9 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     if (opt) o = *opt;
     if (!(o.delta >= 0.0) || o.rebuild_every < 1 || !(o.mass > 0.0) || o.energy_every < 0)
         return set_err(nullptr, LJMD_E_ARG, "ljmd_init: bad options (delta >= 0, rebuild_every >= 1, mass > 0)");
-    if (o.nranks != 1)
-        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: nranks > 1 requires the NCCL build (not in this library)");
+    if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks)
+        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: bad rank %lld / nranks %lld", (long long)o.rank,
+                       (long long)o.nranks);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -779,6 +987,18 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         c->own_stream = true;
     }
     ljmd_status s;
+    c->rank = (int)o.rank;
+    c->nranks = (int)o.nranks;
+    c->lo_rank = (c->rank - 1 + c->nranks) % c->nranks;
+    c->hi_rank = (c->rank + 1) % c->nranks;
+    if (c->nranks > 1) {
+        std::string terr;
+        c->tr = make_transport(o.nccl_id, c->rank, c->nranks, c->device, terr);
+        if (!c->tr) {
+            set_err(c, LJMD_E_NCCL, "%s", terr.c_str());
+            return fail(LJMD_E_NCCL);
+        }
+    }
     if ((s = plan_geometry(c, box)) != LJMD_OK) return fail(s);
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
@@ -787,14 +1007,32 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         set_err(c, LJMD_E_CUDA, "flag allocation failed");
         return fail(LJMD_E_CUDA);
     }
-    const int cap = (int)n;
+    // owned capacity: the whole system on one rank; a slab's share + 25 % headroom otherwise
+    const double share = (double)c->geo.nzl / (double)c->geo.nc[2];
+    const int cap = c->nranks == 1 ? (int)n : (int)std::min<int64_t>(n, (int64_t)(n * share * 1.25) + 4096);
     if ((s = alloc_owned(c, cap)) != LJMD_OK) return fail(s);
+    if (c->nranks > 1) {
+        c->mig_cap = cap / 8 + 1024;
+        for (int b = 0; b < 2; ++b) {
+            if ((s = dalloc(c, &c->mig_send[b], c->mig_cap)) != LJMD_OK) return fail(s);
+            if ((s = dalloc(c, &c->mig_recv[b], c->mig_cap)) != LJMD_OK) return fail(s);
+        }
+        if ((s = dalloc(c, &c->mig_cnt, 8)) != LJMD_OK || (s = dalloc(c, &c->xs, cap)) != LJMD_OK ||
+            (s = dalloc(c, &c->vs, (size_t)3 * cap)) != LJMD_OK || (s = dalloc(c, &c->gs, cap)) != LJMD_OK ||
+            (s = dalloc(c, &c->iota, cap)) != LJMD_OK)
+            return fail(s);
+        if (cudaMallocHost(&c->h_mig, sizeof(int) * 8) != cudaSuccess ||
+            cudaMallocHost(&c->h_tot, sizeof(int) * 4) != cudaSuccess) {
+            set_err(c, LJMD_E_CUDA, "pinned allocation failed");
+            return fail(LJMD_E_CUDA);
+        }
+    }
     const double ghost_ratio = (double)c->n_ecell / (double)c->n_ocell;
-    int64_t scap = (int64_t)std::ceil(n * ghost_ratio * 1.15) + 4096;
+    int64_t scap = (int64_t)std::ceil(cap * ghost_ratio * 1.15) + 4096;
     if ((s = alloc_slots(c, (int)std::min<int64_t>(scap, INT_MAX / 2), false)) != LJMD_OK) return fail(s);
     // list width K: expected 4/3 pi rbar_c^3 rho neighbours with headroom
     double vol = box[0] * box[1] * box[2];
-    double expect = 4.0 / 3.0 * M_PI * c->rn * c->rn * c->rn * (double)n / vol;
+    double expect = 4.0 / 3.0 * M_PI * c->rn * c->rn * c->rn * (double)n / vol;   // P:95
     int K = o.nbr_capacity > 0 ? ((int)o.nbr_capacity + 7) / 8 * 8 : ((int)std::ceil(expect * 1.4) + 16 + 7) / 8 * 8;
     if ((s = alloc_list(c, K)) != LJMD_OK) return fail(s);
     if ((s = load_state(c, pos, vel)) != LJMD_OK) return fail(s);
@@ -839,6 +1077,8 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         ++c->steps_done;
         bool due = c->since >= c->opt.rebuild_every;
         if (!due && check) {
+            // global max displacement (non-negative doubles: max of the bit patterns)
+            TRY(allreduce(c, reinterpret_cast<double*>(&c->d_fl->maxdisp2), 1, true));
             TRY(sync_flags(c));
             double m2;
             std::memcpy(&m2, &c->h_fl->maxdisp2, sizeof m2);
@@ -850,6 +1090,7 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
             ++c->n_rebuilds;
             c->rebuild_steps.push_back(c->steps_done);
         } else {
+            if (c->nranks > 1) TRY(halo_exchange(c));
             TRY(refresh_ghosts(c, false));
         }
         const bool sample = ee > 0 && (c->steps_done % ee) == 0;
@@ -858,6 +1099,7 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last));
         if (sample) {
             TRY(finalize_energy(c, c->hist + 2 * nsamp));
+            TRY(allreduce(c, c->hist + 2 * nsamp, 2, false));
             ++nsamp;
         }
         if (!last) c->xc ^= 1;
@@ -924,6 +1166,7 @@ ljmd_status ljmd_get_energy(ljmd_ctx* c, double* pe, double* ke) {
     TRY(ensure_hist(c, 1));
     double* tmp = c->hist + 2 * (c->hist_cap - 1);
     TRY(finalize_energy(c, tmp));
+    TRY(allreduce(c, tmp, 2, false));
     double h[2];
     CK(cudaMemcpyAsync(h, tmp, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1021,6 +1264,13 @@ void ljmd_destroy(ljmd_ctx* c) {
                     c->tr_off, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    void* ptrs2[] = {c->send_cnt, c->send_off, c->recv_cnt, c->recv_off, c->send_idx, c->send_buf, c->mig_send[0],
+                     c->mig_send[1], c->mig_recv[0], c->mig_recv[1], c->mig_cnt, c->xs, c->vs, c->gs, c->iota};
+    for (void* p : ptrs2)
+        if (p) cudaFree(p);
+    if (c->h_mig) cudaFreeHost(c->h_mig);
+    if (c->h_tot) cudaFreeHost(c->h_tot);
+    delete c->tr;
     if (c->h_fl) cudaFreeHost(c->h_fl);
     if (c->h_slots) cudaFreeHost(c->h_slots);
     for (auto e : c->ev) cudaEventDestroy(e);
@@ -1029,6 +1279,13 @@ void ljmd_destroy(ljmd_ctx* c) {
 }
 
 }  // extern "C"
+
+extern "C" ljmd_status ljmd_nccl_unique_id(void* out128) {
+    if (!out128) return LJMD_E_ARG;
+    std::string err;
+    if (!nccl_unique_id(out128, err)) return set_err(nullptr, LJMD_E_NCCL, "%s", err.c_str());
+    return LJMD_OK;
+}
 
 extern "C" ljmd_status ljmd_measure_fp64_peak(int64_t device, double* tflops) {
     ljmd_ctx* c = nullptr;

@@ -28,7 +28,7 @@ EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "
            "ljmd_get_positions", "ljmd_get_velocities", "ljmd_get_particle_energy", "ljmd_get_energy",
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
-           "ljmd_measure_fp64_peak")
+           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id")
 
 
 class LjmdError(RuntimeError):
@@ -95,6 +95,7 @@ def load(path: str = LIB_PATH):
         "ljmd_plan_cells": ([_D, ctypes.c_double, _I], ctypes.c_int),
         "ljmd_plan_slab": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I, _I], ctypes.c_int),
         "ljmd_measure_fp64_peak": ([ctypes.c_int64, _D], ctypes.c_int),
+        "ljmd_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -151,6 +152,23 @@ def measure_fp64_peak(device: int = -1) -> float:
     return t.value
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    s = load().ljmd_nccl_unique_id(buf)
+    if s != 0:
+        raise LjmdError(s, load().ljmd_last_error(None).decode())
+    return buf.raw
+
+
+def local_group_id(key: str) -> bytes:
+    """Id of an in-process loopback group (several contexts of this process, one GPU)."""
+    b = ("LJMDLOCAL:" + key).encode()
+    if len(b) > 127:
+        raise ValueError("key too long")
+    return b + b"\0" * (128 - len(b))
+
+
 def version() -> str:
     return load().ljmd_version().decode()
 
@@ -164,7 +182,11 @@ class LJMD:
         self.n = pos.shape[0]
         vel = _rows(vel, self.n)
         box = np.ascontiguousarray(box, dtype=np.float64).reshape(3)
+        nccl_id = kw.pop("nccl_id", None)
         opt = options if options is not None else default_options(**kw)
+        if nccl_id is not None:
+            self._id_buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            opt.nccl_id = ctypes.cast(self._id_buf, ctypes.c_void_p)
         h = ctypes.c_void_p()
         s = lib.ljmd_init(ctypes.byref(h), self.n, _dp(pos), _dp(vel), _dp(box), float(rc), float(epsilon),
                           float(sigma), float(dt), ctypes.byref(opt))
