@@ -188,33 +188,59 @@ def main():
     local = env_int("LOCAL_RANK", 0)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    if world > 1:
-        raise SystemExit("multi-GPU slab decomposition not built in this revision")
     torch.cuda.set_device(local)
     from paper_1704_03329_b200 import LJMD, ljmd
+
+    dist = None
+    id_buf = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # the engine's own NCCL communicator: rank 0 creates the id, torch broadcasts it
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(ljmd.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        import ctypes
+        id_buf = ctypes.create_string_buffer(bytes(idt.cpu().numpy().tobytes()), 128)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     pos, vel, box = cfg.build()
     n = len(pos)
     stream = torch.cuda.current_stream()
     opts = ljmd.default_options(device=local, stream=stream.cuda_stream, profile=1,
-                                rebuild_check=args.check)
+                                rebuild_check=args.check, rank=rank, nranks=world)
+    if id_buf is not None:
+        import ctypes
+        opts.nccl_id = ctypes.cast(id_buf, ctypes.c_void_p)
     ctx = LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=opts)
     for _ in range(args.warmup):
         ctx.step(MD_PER_STEP)
-    torch.cuda.synchronize()
+    barrier()
     st0 = ctx.stats()
     clk_path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv") if os.path.isdir(
         os.path.join(ROOT, "gpurun_out")) else f"/tmp/ljmd_clocks_{os.getpid()}.csv"
     clk = (None, None) if args.no_clocks else clocks_start(clk_path)
     time.sleep(0.3 if clk[0] is not None else 0.0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    barrier()
     ev0.record(stream)
     for _ in range(args.steps):
         ctx.step(MD_PER_STEP)
     ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     clocks = clocks_stop(clk, clk_path, local) if clk[0] is not None else None
     st1 = ctx.stats()
     md_steps = args.steps * MD_PER_STEP
@@ -222,6 +248,7 @@ def main():
 
     # dominant kernel: the force kernel (CUDA events around each launch on the same stream)
     launches = st1["force_launches"] - st0["force_launches"]
+    # per-rank force figures (rank 0's slab; the slabs are equal by construction)
     f_ms = (st1["force_ms"] - st0["force_ms"]) / max(launches, 1)
     cand = st1["total_neighbours"]
     e_frac = 1.0 / 10.0
@@ -244,7 +271,7 @@ def main():
         k_e2e = max(2, min(args.steps, 10))
         ctx.set_state_ptr(hp.data_ptr(), hv.data_ptr())
         ctx.step(MD_PER_STEP)
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -256,7 +283,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        ms_e2e = max(e0.elapsed_time(e1), wall * 1e3)
+        ms_e2e = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3))
         e2e = {"value": n * MD_PER_STEP * k_e2e / (ms_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(2 * 24 * n), "d2h_bytes_per_step": int(24 * n + 16),
                "steps": k_e2e}
@@ -282,6 +309,7 @@ def main():
                    "l2": "working set > L2 (list %.0f MB + positions %.0f MB)" % (
                        4 * cand / 1e6, 32 * (n + st1["n_ghost"]) / 1e6)},
         "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
+        "transport": "nccl" if world > 1 else "none",
         "roofline": {"bound": "alu", "kernel": "k_force (fp64 LJ pair loop)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                      "flops_per_launch": flops, "avg_launch_ms": f_ms, "peak_source": peak_src,
@@ -295,6 +323,9 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 
