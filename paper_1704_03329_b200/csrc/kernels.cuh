@@ -602,8 +602,9 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
         const int r0 = (cz + 1 - T.z0) * (T.ty + 2) + (cy + 1 - T.y0);
         const int li = a.tr.off[tile * (kRowsMax + 1) + r0] + si - a.tr.begin[tile * kRowsMax + r0];
         const float4 fi = sF[li];
-        uint4* out = a.nbr8 + t;
-        unsigned pk[4] = {0u, 0u, 0u, 0u};   // 8 pending 16-bit entries -> one 16-byte store
+        // entry k of particle t lives at ((k >> 3) * n_pad + t) * 8 + (k & 7) (blocked layout)
+        unsigned short* out = reinterpret_cast<unsigned short*>(a.nbr8) + (size_t)t * 8;
+        const size_t bstride = stride * 8;
         int k = 0;
         for (int dz = -1; dz <= 1; ++dz) {
             const float ddz = dz < 0 ? fi.z - a.zlo_f[cz] : (dz > 0 ? a.zlo_f[cz + 1] - fi.z : 0.f);
@@ -653,33 +654,15 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
                         }
                     }
                     if (take) {
-                        if (k < a.K) {
-                            const int e = k & 7;
-                            const unsigned sh = (e & 1) * 16;
-                            const unsigned val = (unsigned)jl << sh;
-                            const unsigned msk = ~(0xffffu << sh);
-                            if ((e >> 1) == 0) pk[0] = (pk[0] & msk) | val;
-                            if ((e >> 1) == 1) pk[1] = (pk[1] & msk) | val;
-                            if ((e >> 1) == 2) pk[2] = (pk[2] & msk) | val;
-                            if ((e >> 1) == 3) pk[3] = (pk[3] & msk) | val;
-                            if (e == 7) out[(size_t)(k >> 3) * stride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                        }
+                        if (k < a.K) out[(size_t)(k >> 3) * bstride + (k & 7)] = (unsigned short)jl;
                         ++k;
                     }
                 }
             }
         }
         if ((k & 7) && k < a.K) {   // pad the last block with the tile's sentinel index
-            const unsigned sen = (unsigned)a.tr.off[tile * (kRowsMax + 1) + T.R];
-            for (int e = k & 7; e < 8; ++e) {
-                const unsigned sh = (e & 1) * 16;
-                const unsigned msk = ~(0xffffu << sh);
-                if ((e >> 1) == 0) pk[0] = (pk[0] & msk) | (sen << sh);
-                if ((e >> 1) == 1) pk[1] = (pk[1] & msk) | (sen << sh);
-                if ((e >> 1) == 2) pk[2] = (pk[2] & msk) | (sen << sh);
-                if ((e >> 1) == 3) pk[3] = (pk[3] & msk) | (sen << sh);
-            }
-            out[(size_t)(k >> 3) * stride] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            const unsigned short sen = (unsigned short)a.tr.off[tile * (kRowsMax + 1) + T.R];
+            for (int e = k & 7; e < 8; ++e) out[(size_t)(k >> 3) * bstride + e] = sen;
         }
         a.ncount[t] = k;
         atomicMax(&a.fl->max_nbr, k);
