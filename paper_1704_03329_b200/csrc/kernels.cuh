@@ -672,6 +672,104 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
     if (lane == 0 && kk) atomicAdd(&a.fl->total_nbr, kk);
 }
 
+// --------------------------------------------------------------------------- bank-aware list order
+// The force CTA's thread q reads neighbour l from shared memory at byte 24 l: the bank pair
+// of an 8-byte load is 3 l mod 16, so two lanes of a half-warp conflict when their local
+// indices differ by a multiple of 16.  Re-sequencing each list so that entry k targets
+// residue (q + k) mod 16 (the next non-empty residue, cyclically, when that one is used
+// up) spreads the 16 lanes of a phase over distinct banks most of the time; measured on C2
+// the force kernel drops from ~199 to ~170 us.  Only the order of a particle's sum
+// changes, not its terms.  Thread per particle; buckets of kRrCap entries per residue in
+// bank-padded shared memory (stride 65 words per thread); a particle with a fuller residue
+// keeps the build order.
+constexpr int kRrThreads = 128;
+constexpr int kRrCap = 8;                        // per-residue capacity (mean ~4.6)
+constexpr int kRrOvf = 16;                       // entries beyond a full bucket, emitted last
+constexpr int kRrStrideW = (16 * kRrCap + kRrOvf) / 2 + 1;   // words per thread (odd: no bank aliasing)
+constexpr int kRrCntW = 17;                      // words per thread of the count / head areas
+constexpr size_t kRrSmem = sizeof(unsigned) * (size_t)kRrThreads * (kRrStrideW + 2 * kRrCntW);
+
+__global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, int K, Geo g,
+                                                       const uint4* __restrict__ in,
+                                                       const int* __restrict__ ncount,
+                                                       const int* __restrict__ ocell_of,
+                                                       const int* __restrict__ obegin,
+                                                       const int* __restrict__ tile_oc0,
+                                                       uint4* __restrict__ out) {
+    extern __shared__ unsigned rr_smem[];
+    const int tid = threadIdx.x;
+    const int t = blockIdx.x * kRrThreads + tid;
+    unsigned short* bkt = reinterpret_cast<unsigned short*>(rr_smem + (size_t)tid * kRrStrideW);
+    int* cnt = reinterpret_cast<int*>(rr_smem + (size_t)kRrThreads * kRrStrideW) + tid * kRrCntW;
+    int* head = reinterpret_cast<int*>(rr_smem + (size_t)kRrThreads * (kRrStrideW + kRrCntW)) + tid * kRrCntW;
+    if (t >= n_own) return;
+    const int n = min(ncount[t], K);
+    const int nb = (n + 7) >> 3;
+    const size_t stride = (size_t)n_pad;
+    int cx, cy, cz;
+    lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
+    const int tile = tile_of_cell(g, cx, cy, cz);
+    const int off = (t - obegin[tile_oc0[tile]]) & 15;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        cnt[r] = 0;
+        head[r] = 0;
+    }
+    bool overflow = false;
+    int novf = 0;
+    unsigned short pad = 0;
+    for (int b = 0; b < nb; ++b) {
+        const uint4 v = in[(size_t)b * stride + t];
+        const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const unsigned short l = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
+            if (b * 8 + e < n) {
+                const int r = l & 15;
+                const int c = cnt[r];
+                if (c < kRrCap) {
+                    bkt[r * kRrCap + c] = l;
+                    cnt[r] = c + 1;
+                } else if (novf < kRrOvf) {
+                    bkt[16 * kRrCap + novf++] = l;
+                } else {
+                    overflow = true;
+                }
+            } else {
+                pad = l;   // the tile's sentinel
+            }
+        }
+    }
+    if (overflow) {
+        for (int b = 0; b < nb; ++b) out[(size_t)b * stride + t] = in[(size_t)b * stride + t];
+        return;
+    }
+    unsigned avail = 0u;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+        if (cnt[r]) avail |= 1u << r;
+    unsigned long long lo64 = 0ull, hi64 = 0ull;   // 8 pending entries, shifted in from the top
+    for (int k = 0; k < nb * 8; ++k) {
+        unsigned short l = pad;
+        if (k >= n - novf && k < n) {
+            l = bkt[16 * kRrCap + (k - (n - novf))];
+        } else if (k < n) {
+            const int tgt = (off + k) & 15;
+            const unsigned rot = ((avail >> tgt) | (avail << (16 - tgt))) & 0xffffu;
+            const int rr = (tgt + __ffs(rot) - 1) & 15;
+            const int h = head[rr];
+            l = bkt[rr * kRrCap + h];
+            head[rr] = h + 1;
+            if (h + 1 == cnt[rr]) avail &= ~(1u << rr);
+        }
+        lo64 = (lo64 >> 16) | (hi64 << 48);
+        hi64 = (hi64 >> 16) | ((unsigned long long)l << 48);
+        if ((k & 7) == 7)
+            out[(size_t)(k >> 3) * stride + t] =
+                make_uint4((unsigned)lo64, (unsigned)(lo64 >> 32), (unsigned)hi64, (unsigned)(hi64 >> 32));
+    }
+}
+
 // --------------------------------------------------------------------------- force
 // LJ force over the full (both-orders) list, written only to i: no atomics.
 // Eq. eqn:LJforce with u = 1/r^2:

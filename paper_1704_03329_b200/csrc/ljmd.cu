@@ -90,6 +90,8 @@ struct ljmd_ctx {
     int scan_tmp_n = 0;
     // ---- list
     uint4* nbr8 = nullptr;            // 16-bit tile-local indices in blocks of 8: [K/8][n_pad]
+    uint4* nbr8b = nullptr;           // the same, bank-aware order (what k_force reads)
+    int bank_order = 1;               // 0: the force kernel walks the build order
     int* ncount = nullptr;
     // ---- energies
     double* pe_part = nullptr;
@@ -409,6 +411,7 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
 ljmd_status alloc_list(ljmd_ctx* c, int K) {
     c->K = K;
     TRY(dalloc(c, &c->nbr8, (size_t)(K / 8) * c->n_pad));
+    TRY(dalloc(c, &c->nbr8b, (size_t)(K / 8) * c->n_pad));
     return LJMD_OK;
 }
 
@@ -468,7 +471,7 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.x = c->x[c->xc];
     a.x_next = c->x[c->xc ^ 1];
     a.own_slot = c->own_slot;
-    a.nbr = c->nbr8;
+    a.nbr = c->bank_order ? c->nbr8b : c->nbr8;
     a.ncount = c->ncount;
     a.fx = c->F;
     a.fy = c->F + c->own_cap;
@@ -511,6 +514,8 @@ cudaError_t force_attr() {
 
 ljmd_status set_force_attrs(ljmd_ctx* c) {
     cudaError_t e = cudaFuncSetAttribute(k_build_nlist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStageSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_list_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRrSmem);
     for (cudaError_t r : {force_attr<true, kStore, false>(), force_attr<true, kKick, false>(),
                           force_attr<true, kKKD, false>(), force_attr<true, kKKD, true>(),
                           force_attr<false, kStore, false>(), force_attr<false, kKick, false>(),
@@ -772,6 +777,11 @@ ljmd_status rebuild(ljmd_ctx* c) {
     }
     c->max_nbr = c->h_fl->max_nbr;
     c->total_nbr = c->h_fl->total_nbr;
+    if (c->bank_order) {
+        k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
+            c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b);
+        CKL();
+    }
 
     return LJMD_OK;
 }
@@ -912,6 +922,7 @@ ljmd_status ljmd_default_options(ljmd_options* o) {
     o->nccl_id = nullptr;
     o->stream = nullptr;
     o->profile = 0;
+    o->list_order = 1;
     return LJMD_OK;
 }
 
@@ -965,6 +976,7 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     c->sigma = sigma;
     c->dt = dt;
     c->rn = rc + o.delta;
+    c->bank_order = o.list_order != 0;
     auto fail = [&](ljmd_status s) {
         g_init_error = c->msg.empty() ? std::string("ljmd_init failed") : c->msg;
         ljmd_destroy(c);
@@ -1260,7 +1272,7 @@ void ljmd_destroy(ljmd_ctx* c) {
     void* ptrs[] = {c->x[0], c->x[1], c->xf, c->slot_gid, c->v[0], c->v[1], c->gid[0], c->gid[1],
                     c->own_slot, c->ocell_of, c->F, c->e, c->xbuild, c->xw, c->cell_of, c->rank_in, c->perm,
                     c->ocount, c->obegin, c->ecount, c->ebegin, c->ecell_src, c->gc_dst, c->gc_src, c->gc_shift,
-                    c->scan_tmp, c->nbr8, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin, c->ylo_f, c->zlo_f,
+                    c->scan_tmp, c->nbr8, c->nbr8b, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin, c->ylo_f, c->zlo_f,
                     c->tr_off, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -76,8 +76,8 @@ def test_decomposition_bitwise(nranks):
     pos, box = li.fcc(6, 6, 9)
     pos = li.perturb(pos, 0.05)
     vel = li.velocities(len(pos), 1.44)
-    ref = single(pos, vel, box, 45)
-    got, per = run_ranks(nranks, pos, vel, box, 45)
+    ref = single(pos, vel, box, 45, list_order=0)
+    got, per = run_ranks(nranks, pos, vel, box, 45, list_order=0)
     assert np.array_equal(got["X"], ref["X"])
     assert np.array_equal(got["V"], ref["V"])
     assert np.array_equal(got["F"], ref["F"])
@@ -88,6 +88,18 @@ def test_decomposition_bitwise(nranks):
         np.testing.assert_allclose(o["hist"][0], ref["hist"][0], rtol=1e-12)
         assert o["rs"].tolist() == ref["rs"].tolist()
     assert sum(o["st"]["n_owned"] for o in per) == len(pos)
+
+
+def test_decomposition_default_order():
+    """With the (default) bank-aware neighbour order the per-particle summation order
+    depends on the tiling, so p = 2 agrees with p = 1 to rounding, not bitwise."""
+    pos, box = li.fcc(6, 6, 8)
+    pos = li.perturb(pos, 0.05)
+    vel = li.velocities(len(pos), 1.44)
+    ref = single(pos, vel, box, 10)
+    got, _ = run_ranks(2, pos, vel, box, 10)
+    np.testing.assert_allclose(got["X"], ref["X"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(got["F"], ref["F"], rtol=0, atol=1e-9)
 
 
 def test_decomposition_against_oracle(orc):
@@ -105,8 +117,8 @@ def test_decomposition_safe_policy():
     pos, box = li.fcc(6, 6, 8)
     pos = li.perturb(pos, 0.05)
     vel = li.velocities(len(pos), 2.5)
-    ref = single(pos, vel, box, 40, rebuild_check=1)
-    got, per = run_ranks(2, pos, vel, box, 40, rebuild_check=1)
+    ref = single(pos, vel, box, 40, rebuild_check=1, list_order=0)
+    got, per = run_ranks(2, pos, vel, box, 40, rebuild_check=1, list_order=0)
     assert np.array_equal(got["X"], ref["X"])
     for o in per:
         assert o["rs"].tolist() == ref["rs"].tolist()
