@@ -186,6 +186,8 @@ def main():
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    if os.environ.get("LJMD_BENCH_DEVICE") is not None:   # debugging: all ranks on one GPU
+        local = env_int("LJMD_BENCH_DEVICE", 0)
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)

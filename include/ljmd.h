@@ -74,6 +74,8 @@ typedef struct {
     int64_t list_order;     /* 1 (default): bank-aware neighbour order (fastest); 0: build order
                                (stencil row, slot) -- results then do not depend on the number
                                of slabs (bitwise), at ~15 % more force-kernel time          */
+    int64_t split_self;     /* 1: with nranks = 1, still run the slab-exchange path (halo
+                               planes sent to itself through the transport; testing)        */
 } ljmd_options;
 
 typedef struct {

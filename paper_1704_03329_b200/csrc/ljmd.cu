@@ -118,6 +118,7 @@ struct ljmd_ctx {
     // ---- z-slab decomposition (nranks > 1)
     Transport* tr = nullptr;
     int rank = 0, nranks = 1, lo_rank = 0, hi_rank = 0, npc = 0;
+    bool split = false;           // run the slab-exchange path (nranks > 1, or split_self)
     int* send_cnt = nullptr;      // [2 * npc] bottom / top plane cell counts
     int* send_off = nullptr;      // [2 * npc + 1]
     int* recv_cnt = nullptr;      // [2 * npc] lower / upper ghost plane cell counts
@@ -311,7 +312,7 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
     std::vector<int> src(c->n_ecell), gd, gs, gsh;
     gd.reserve(c->n_gcell);
     const int npc = g.nc[0] * g.nc[1];
-    const bool split = c->opt.nranks > 1;
+    const bool split = c->opt.nranks > 1 || c->opt.split_self;
     for (int iz = 0; iz < g.ez; ++iz)
         for (int iy = 0; iy < g.ey; ++iy)
             for (int ix = 0; ix < g.ex; ++ix) {
@@ -671,7 +672,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     const int* slot_in = c->own_slot;
     const double* vo = c->v[c->oc_cur];
     const int* gid_old = c->gid[c->oc_cur];
-    if (c->nranks > 1) {
+    if (c->split) {
         TRY(migrate(c));
         k_iota<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->iota);
         CKL();
@@ -684,7 +685,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, xin, slot_in, c->geo, c->xw, c->ocount, c->cell_of,
                                                     c->rank_in, gid_old, c->d_fl);
     CKL();
-    if (c->nranks > 1) {   // boundary-plane cell counts -> the neighbours' ghost planes
+    if (c->split) {   // boundary-plane cell counts -> the neighbours' ghost planes
         const int npc = c->npc;
         k_plane_counts<<<nblk(2 * npc, 256), 256, 0, c->stream>>>(c->geo, c->ocount, c->send_cnt);
         CKL();
@@ -709,7 +710,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
                        c->h_fl->nonfinite_gid);
     const int need = *c->h_slots;
     int n_recv_tot = 0;
-    if (c->nranks > 1) {
+    if (c->split) {
         c->n_send[0] = c->h_tot[0];
         c->n_send[1] = c->h_tot[1] - c->h_tot[0];
         c->n_recv[0] = c->h_tot[2];
@@ -740,7 +741,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     CKL();
     c->oc_cur = on;
     c->xc ^= 1;
-    if (c->nranks > 1) {   // ghost planes: positions + gids of the neighbours' boundary planes
+    if (c->split) {   // ghost planes: positions + gids of the neighbours' boundary planes
         k_plane_index<<<nblk((int64_t)2 * c->npc * 32, 256), 256, 0, c->stream>>>(c->geo, c->send_cnt,
                                                                                   c->send_off, c->ebegin,
                                                                                   c->send_idx);
@@ -814,7 +815,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
     int64_t n = c->n_global;
     std::vector<double> fp, fv;
     std::vector<int> fg;
-    if (c->nranks > 1) {
+    if (c->split) {
         // initial owner by z plane, computed on the host; the first rebuild's migration
         // corrects the rare plane-boundary disagreement with the device binning
         const Geo& g = c->geo;
@@ -845,7 +846,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
     TRY(dalloc(c, &dvel, (size_t)3 * n));
     CK(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dvel, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
-    if (c->nranks > 1) {
+    if (c->split) {
         TRY(dalloc(c, &dg, (size_t)n));
         CK(cudaMemcpyAsync(dg, fg.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
     }
@@ -923,6 +924,7 @@ ljmd_status ljmd_default_options(ljmd_options* o) {
     o->stream = nullptr;
     o->profile = 0;
     o->list_order = 1;
+    o->split_self = 0;
     return LJMD_OK;
 }
 
@@ -1003,7 +1005,8 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     c->nranks = (int)o.nranks;
     c->lo_rank = (c->rank - 1 + c->nranks) % c->nranks;
     c->hi_rank = (c->rank + 1) % c->nranks;
-    if (c->nranks > 1) {
+    c->split = c->nranks > 1 || o.split_self != 0;
+    if (c->split) {
         std::string terr;
         c->tr = make_transport(o.nccl_id, c->rank, c->nranks, c->device, terr);
         if (!c->tr) {
@@ -1023,7 +1026,7 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     const double share = (double)c->geo.nzl / (double)c->geo.nc[2];
     const int cap = c->nranks == 1 ? (int)n : (int)std::min<int64_t>(n, (int64_t)(n * share * 1.25) + 4096);
     if ((s = alloc_owned(c, cap)) != LJMD_OK) return fail(s);
-    if (c->nranks > 1) {
+    if (c->split) {
         c->mig_cap = cap / 8 + 1024;
         for (int b = 0; b < 2; ++b) {
             if ((s = dalloc(c, &c->mig_send[b], c->mig_cap)) != LJMD_OK) return fail(s);
@@ -1102,7 +1105,7 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
             ++c->n_rebuilds;
             c->rebuild_steps.push_back(c->steps_done);
         } else {
-            if (c->nranks > 1) TRY(halo_exchange(c));
+            if (c->split) TRY(halo_exchange(c));
             TRY(refresh_ghosts(c, false));
         }
         const bool sample = ee > 0 && (c->steps_done % ee) == 0;

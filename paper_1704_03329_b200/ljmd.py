@@ -44,7 +44,8 @@ class Options(ctypes.Structure):
                 ("device", ctypes.c_int64), ("nbr_capacity", ctypes.c_int64),
                 ("rank", ctypes.c_int64), ("nranks", ctypes.c_int64),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
-                ("profile", ctypes.c_int64), ("list_order", ctypes.c_int64)]
+                ("profile", ctypes.c_int64), ("list_order", ctypes.c_int64),
+                ("split_self", ctypes.c_int64)]
 
 
 class Stats(ctypes.Structure):

@@ -122,3 +122,22 @@ def test_decomposition_safe_policy():
     assert np.array_equal(got["X"], ref["X"])
     for o in per:
         assert o["rs"].tolist() == ref["rs"].tolist()
+
+
+@pytest.mark.parametrize("transport", ["nccl", "local"])
+def test_split_self_transport(transport):
+    """nranks = 1 with split_self: the slab-exchange path (plane counts, halo planes, gids,
+    all-reduces) runs through the real transport -- NCCL self send/recv on one GPU, or the
+    loopback -- and reproduces the plain single-rank run bitwise."""
+    from paper_1704_03329_b200 import ljmd
+    pos, box = li.fcc(6, 6, 7)
+    pos = li.perturb(pos, 0.05)
+    vel = li.velocities(len(pos), 1.44)
+    ref = single(pos, vel, box, 30, list_order=0)
+    nid = ljmd.nccl_unique_id() if transport == "nccl" else ljmd.local_group_id(uuid.uuid4().hex)
+    with ljmd.LJMD(pos, vel, box, split_self=1, nccl_id=nid, list_order=0) as ctx:
+        ctx.step(30)
+        assert np.array_equal(ctx.positions(), ref["X"])
+        assert np.array_equal(ctx.forces(), ref["F"])
+        pe, ke = ctx.energy()
+        assert pe == pytest.approx(ref["e"][0], rel=1e-13) and ke == pytest.approx(ref["e"][1], rel=1e-13)
