@@ -61,7 +61,7 @@ def clocks_start(path):
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     try:
         f = open(path, "w")
-        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "50"],
                              stdout=f, stderr=subprocess.DEVNULL)
         return p, f
     except Exception:
@@ -221,8 +221,9 @@ def main():
     pos, vel, box = cfg.build()
     n = len(pos)
     stream = torch.cuda.current_stream()
+    check = 1 if (args.check or cfg.rebuild_check) else 0
     opts = ljmd.default_options(device=local, stream=stream.cuda_stream, profile=1,
-                                rebuild_check=args.check, rank=rank, nranks=world)
+                                rebuild_check=check, rank=rank, nranks=world)
     if id_buf is not None:
         import ctypes
         opts.nccl_id = ctypes.cast(id_buf, ctypes.c_void_p)
@@ -256,6 +257,15 @@ def main():
     e_frac = 1.0 / 10.0
     flops = cand * (FLOPS_PER_CAND * (1 - e_frac) + FLOPS_PER_CAND_E * e_frac)
     achieved = flops / (f_ms * 1e-3) / 1e12
+    # DRAM bytes per force launch from the committed ncu --set full capture of this config
+    traffic, traffic_src = None, None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "force_traffic.json")))
+        if tj.get("workload") == cfg.name:
+            traffic = tj["dram_bytes_per_launch"]
+            traffic_src = tj["source"]
+    except (OSError, ValueError, KeyError):
+        pass
     try:
         peak = ljmd.measure_fp64_peak(local)
         peak_src = "measured (DFMA-chain probe, ljmd_measure_fp64_peak)"
@@ -306,14 +316,15 @@ def main():
         "data": "synthetic FCC crystal (ljinputs: rho 0.8442, PCG64 seeds 87287/1704)",
         "config": {"workload": cfg.name, "n_particles": n, "rho": li.RHO, "rc": li.RC,
                    "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "energy_every": 10, "dt": li.DT,
-                   "t0": cfg.t0, "rebuild_policy": "safe" if args.check else "paper-fixed-20",
+                   "t0": cfg.t0, "rebuild_policy": "safe" if check else "paper-fixed-20",
                    "parallelism": f"z-slab x{world}",
                    "l2": "working set > L2 (list %.0f MB + positions %.0f MB)" % (
                        4 * cand / 1e6, 32 * (n + st1["n_ghost"]) / 1e6)},
         "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
         "transport": "nccl" if world > 1 else "none",
         "roofline": {"bound": "alu", "kernel": "k_force (fp64 LJ pair loop)", "achieved": achieved,
-                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                     "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "flops_per_launch": flops, "avg_launch_ms": f_ms, "peak_source": peak_src,
                      "flop_count": "Listing 9: 21 flops per list candidate (+5 with PE every 10th step)"},
         "force_share": (st1["force_ms"] - st0["force_ms"]) / ms,
