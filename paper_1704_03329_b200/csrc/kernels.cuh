@@ -833,6 +833,12 @@ __device__ __forceinline__ bool inside_rc(double r2f, double dx, double dy, doub
     return r2_canon(dx, dy, dz) < rc2;
 }
 
+// L1 prefetch (no register): the list blocks stream from DRAM, and the compiler sinks the
+// register "prefetch" of the next block to the end of the loop under register pressure.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" :: "l"(p) : "memory");   // pinned: no sinking
+}
+
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(gsrc) : "memory");
@@ -852,6 +858,7 @@ __device__ __forceinline__ FPart fpart_load(const ForceArgs& a, int t) {
     P.cnt = a.ncount[t];
     P.xi = ld256(a.x + P.si);
     P.nb0 = P.cnt > 0 ? a.nbr[t] : make_uint4(0u, 0u, 0u, 0u);
+    if (P.cnt > 8) prefetch_l1(a.nbr + (size_t)a.n_pad + t);
     return P;
 }
 
@@ -866,8 +873,9 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
     const int nblk = (P.cnt + 7) >> 3;
     uint4 cur = P.nb0;
     for (int b = 0; b < nblk; ++b) {
-        // prefetch the next 8 indices while this block is computed; a short block is
-        // padded with the sentinel, so every entry is evaluated unpredicated
+        // block b+2 into L1 now, block b+1 into registers; a short block is padded with the
+        // sentinel, so every entry is evaluated unpredicated
+        if (b + 2 < nblk) prefetch_l1(nb + (size_t)(b + 2) * stride);
         const uint4 nxt = (b + 1 < nblk) ? nb[(size_t)(b + 1) * stride] : make_uint4(0u, 0u, 0u, 0u);
         const unsigned w4[4] = {cur.x, cur.y, cur.z, cur.w};
 #pragma unroll
