@@ -175,6 +175,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-boa", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -300,6 +301,23 @@ def main():
                "h2d_bytes_per_step": int(2 * 24 * n), "d2h_bytes_per_step": int(24 * n + 16),
                "steps": k_e2e}
 
+    # §8(f) NEXT-2 bond-order analysis on the same state (not part of the headline metric):
+    # Q_6 with the first-shell cutoff 1.5 sigma, CUDA events around the call (kernel +
+    # D2H of Q and |N(i)| + host scatter into caller order)
+    boa = None
+    if not args.no_boa:
+        ctx.boa(6, 1.5)
+        torch.cuda.synchronize()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        nb = 3
+        for _ in range(nb):
+            Qb, _nn = ctx.boa(6, 1.5)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        boa = {"ell": 6, "rcut": 1.5, "ms_per_call_incl_readback": b0.elapsed_time(b1) / nb,
+               "mean_Q6": float(np.mean(Qb))}
+
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         cores, model = cpu_info()
@@ -331,6 +349,7 @@ def main():
         "neighbours_per_particle": cand / n,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "boa": boa,
         "clocks": clocks,
     }
     if rank == 0:

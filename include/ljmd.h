@@ -153,6 +153,15 @@ void ljmd_destroy(ljmd_ctx* c);
 /* Library version string, e.g. "ljmd 0.1 sm_100a". */
 const char* ljmd_version(void);
 
+/* Bond-order analysis (Sec. 4.1): Steinhardt
+ * Q_ell of every owned particle at the current positions,
+ *   q_lm(i) = (1/|N(i)|) sum_{j in N(i)} Y_l^m(r_hat_ij)          (Eq. eqn:qellm)
+ *   Q_l(i)  = sqrt(4 pi/(2 l + 1) sum_m |q_lm(i)|^2)             (Eq. eqn:Qell)
+ * with N(i) = { j : r_ij < rcut } taken from the engine's Verlet list, so rcut <= rc is
+ * required (LJMD_E_ARG otherwise); 0 <= ell <= 12.  Q[n] (and nnb[n] = |N(i)| if non-NULL)
+ * in the caller's order; with nranks > 1 only owned rows are written; |N(i)| = 0 -> 0. */
+ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q, int64_t* nnb);
+
 /* Multi-GPU plumbing: fill out128 with a fresh ncclUniqueId (NCCL is loaded with dlopen;
  * the copy torch already mapped is reused).  Rank 0 calls it and broadcasts the 128
  * bytes (e.g. with torch.distributed) into ljmd_options.nccl_id on every rank.  An id

@@ -124,3 +124,24 @@ CONFIGS = {
 def weak_config(n_gpus: int) -> Config:
     """Weak scaling at 1,048,576 particles per GPU: 64 x 64 x (64*n) FCC cells (z-slabs)."""
     return Config(f"C2x{n_gpus}", (64, 64, 64 * n_gpus), 1.44, md_steps=1000)
+
+
+def hcp(nx: int, ny: int, nz: int, d: float = 1.0):
+    """Ideal hcp (c/a = sqrt(8/3)) with nearest-neighbour distance d, orthohexagonal cell
+    (d, sqrt(3) d, sqrt(8/3) d) holding 4 atoms; returns (pos, box)."""
+    basis = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.0], [0.0, 1.0 / 3.0, 0.5], [0.5, 5.0 / 6.0, 0.5]])
+    cell = np.array([d, np.sqrt(3.0) * d, np.sqrt(8.0 / 3.0) * d])
+    cz, cy, cx = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    cells = np.stack([cx.ravel(), cy.ravel(), cz.ravel()], axis=1).astype(np.float64)
+    pos = ((cells[:, None, :] + basis[None, :, :]) * cell).reshape(-1, 3)
+    return np.ascontiguousarray(pos), cell * np.array([nx, ny, nz], dtype=np.float64)
+
+
+def bcc(nx: int, ny: int, nz: int, d: float = 1.0):
+    """bcc with nearest-neighbour distance d (cube edge 2 d / sqrt(3)); returns (pos, box)."""
+    a = 2.0 * d / np.sqrt(3.0)
+    basis = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.5]])
+    cz, cy, cx = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    cells = np.stack([cx.ravel(), cy.ravel(), cz.ravel()], axis=1).astype(np.float64)
+    pos = ((cells[:, None, :] + basis[None, :, :]) * a).reshape(-1, 3)
+    return np.ascontiguousarray(pos), np.array([nx, ny, nz], dtype=np.float64) * a

@@ -1122,3 +1122,118 @@ __global__ void __launch_bounds__(256) k_fp64_peak(double* out, int iters, doubl
     if (s == 12345.678) out[blockIdx.x] = s;   // keep the chains alive
 }
 }  // namespace ljmd
+
+namespace ljmd {
+// ----------------------------------------------------------------------------- bond order
+// Steinhardt bond-order parameters (Sec. 4.1, Eqs. eqn:qellm / eqn:Qell)
+// as a second Local Particle Pair Loop over the engine's lists (Alg. alg:sph_I), then the
+// particle loop Q_l = sqrt(4 pi/(2l+1) sum_m |q_lm|^2) (Alg. alg:sph_II).  Neighbours: the
+// list entries with canonical r^2 < rcut^2 (rcut <= rc keeps the Verlet list complete).
+// Y_l^m(r_hat) = K_lm Pbar_l^m(z) (x + i y)^m with Pbar_l^m = P_l^m / (1 - z^2)^{m/2}
+// (three-term recurrence in l), m >= 0 only: |q_{l,-m}| = |q_{l,m}|; the Condon-Shortley
+// sign is dropped (Q_l depends on |q_lm| only).
+constexpr int kBoaMaxL = 12;
+
+struct BoaArgs {
+    Geo g;
+    const double4* x;
+    const int* own_slot;
+    const uint4* nbr;
+    const int* ncount;
+    const int* obegin;
+    const int* tile_oc0;
+    TileRows tr;
+    double* Q;        // [n_own]
+    double* nnb;      // [n_own]
+    int n_own, n_pad;
+    double rcut2;
+    double K[kBoaMaxL + 1];   // K_lm = sqrt((2l+1)/(4 pi) (l-m)!/(l+m)!)
+};
+
+template <int L>
+__global__ void __launch_bounds__(kForceThreads) k_boa(BoaArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const TileGeo T = tile_geo(a.g, tile);
+    const int t0 = a.obegin[a.tile_oc0[tile]];
+    const int m_own = a.obegin[a.tile_oc0[tile + 1]] - t0;
+    const int rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
+    const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
+    const int total = __shfl_sync(0xffffffffu, ro, T.R);
+    double* sP = reinterpret_cast<double*>(smem);
+    for (int r = warp; r < T.R; r += kForceThreads / 32) {
+        const int b0 = __shfl_sync(0xffffffffu, rb, r);
+        const int o0 = __shfl_sync(0xffffffffu, ro, r);
+        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
+        for (int k = lane; k < len; k += 32) {
+            const double4 p = ld256(a.x + b0 + k);
+            sP[3 * (o0 + k)] = p.x;
+            sP[3 * (o0 + k) + 1] = p.y;
+            sP[3 * (o0 + k) + 2] = p.z;
+        }
+    }
+    if (threadIdx.x == 0) {
+        sP[3 * total] = 1e30;
+        sP[3 * total + 1] = 1e30;
+        sP[3 * total + 2] = 1e30;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < m_own; q += kForceThreads) {
+        const int t = t0 + q;
+        const double4 xi = a.x[a.own_slot[t]];
+        const int cnt = a.ncount[t];
+        double re[L + 1], im[L + 1];
+#pragma unroll
+        for (int m = 0; m <= L; ++m) re[m] = im[m] = 0.0;
+        int nu = 0;
+        for (int k = 0; k < cnt; ++k) {
+            const uint4 w = a.nbr[(size_t)(k >> 3) * a.n_pad + t];
+            const unsigned ww = (k & 7) < 2 ? w.x : (k & 7) < 4 ? w.y : (k & 7) < 6 ? w.z : w.w;
+            const unsigned l = (k & 1) ? (ww >> 16) : (ww & 0xffffu);
+            const double* pj = sP + 3 * l;
+            const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
+            const double r2 = r2_canon(dx, dy, dz);
+            if (!(r2 < a.rcut2)) continue;
+            ++nu;
+            const double ir = 1.0 / sqrt(r2);
+            const double ux = dx * ir, uy = dy * ir, z = dz * ir;       // r_hat_ij
+            double cr = 1.0, ci = 0.0;                                   // (x + i y)^m
+            double pmm = 1.0;                                            // Pbar_m^m = (2m-1)!!
+#pragma unroll
+            for (int m = 0; m <= L; ++m) {
+                double p0 = pmm, p1 = 0.0;
+                if (m < L) {
+                    p1 = (2 * m + 1) * z * pmm;                           // Pbar_{m+1}^m
+                    double a0 = p0, a1 = p1;
+#pragma unroll
+                    for (int ll = m + 2; ll <= L; ++ll) {
+                        const double an = ((2 * ll - 1) * z * a1 - (ll + m - 1) * a0) / (ll - m);
+                        a0 = a1;
+                        a1 = an;
+                    }
+                    p0 = a1;                                              // Pbar_L^m
+                }
+                const double y = a.K[m] * p0;
+                re[m] += y * cr;
+                im[m] += y * ci;
+                const double nr = cr * ux - ci * uy, ni = cr * uy + ci * ux;
+                cr = nr;
+                ci = ni;
+                pmm *= (2 * m + 1);
+            }
+        }
+        double acc = 0.0;
+        if (nu > 0) {
+            const double inv = 1.0 / nu;
+#pragma unroll
+            for (int m = 0; m <= L; ++m) {
+                const double qr = re[m] * inv, qi = im[m] * inv;
+                acc += (m == 0 ? 1.0 : 2.0) * (qr * qr + qi * qi);
+            }
+        }
+        a.Q[t] = sqrt(4.0 * 3.14159265358979323846 / (2 * L + 1) * acc);
+        a.nnb[t] = (double)nu;
+    }
+}
+}  // namespace ljmd

@@ -1295,6 +1295,66 @@ void ljmd_destroy(ljmd_ctx* c) {
 
 }  // extern "C"
 
+
+template <int L>
+void boa_launch(ljmd_ctx* c, const BoaArgs& a, size_t smem) {
+    cudaFuncSetAttribute(k_boa<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxStageSmem);
+    k_boa<L><<<c->n_tiles, kForceThreads, smem, c->stream>>>(a);
+}
+
+extern "C" ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q, int64_t* nnb) {
+    TRY(check_ctx(c));
+    if (!Q || ell < 0 || ell > kBoaMaxL || !(rcut > 0.0))
+        return set_err(c, LJMD_E_ARG, "ljmd_boa: need 0 <= ell <= %d and rcut > 0", kBoaMaxL);
+    if (rcut > c->rc)
+        return set_err(c, LJMD_E_ARG, "ljmd_boa: rcut %g exceeds the force cutoff rc = %g (list validity)", rcut,
+                       c->rc);
+    BoaArgs a;
+    a.g = c->geo;
+    a.x = c->x[c->xc];
+    a.own_slot = c->own_slot;
+    a.nbr = c->nbr8;
+    a.ncount = c->ncount;
+    a.obegin = c->obegin;
+    a.tile_oc0 = c->tile_oc0;
+    a.tr = TileRows{c->tr_begin, c->tr_off};
+    a.Q = c->d_stage;
+    a.nnb = c->d_stage + c->own_cap;
+    a.n_own = c->n_own;
+    a.n_pad = c->n_pad;
+    a.rcut2 = rcut * rcut;
+    for (int m = 0; m <= kBoaMaxL; ++m) {
+        double f = 1.0;   // (l-m)!/(l+m)!
+        for (int k = (int)ell - m + 1; k <= (int)ell + m; ++k) f /= (double)k;
+        a.K[m] = m <= ell ? std::sqrt((2.0 * ell + 1.0) / (4.0 * M_PI) * f) : 0.0;
+    }
+    const size_t smem = 24 * (size_t)(c->max_staged + 1);
+    switch (ell) {
+        case 0: boa_launch<0>(c, a, smem); break;
+        case 1: boa_launch<1>(c, a, smem); break;
+        case 2: boa_launch<2>(c, a, smem); break;
+        case 3: boa_launch<3>(c, a, smem); break;
+        case 4: boa_launch<4>(c, a, smem); break;
+        case 5: boa_launch<5>(c, a, smem); break;
+        case 6: boa_launch<6>(c, a, smem); break;
+        case 7: boa_launch<7>(c, a, smem); break;
+        case 8: boa_launch<8>(c, a, smem); break;
+        case 9: boa_launch<9>(c, a, smem); break;
+        case 10: boa_launch<10>(c, a, smem); break;
+        case 11: boa_launch<11>(c, a, smem); break;
+        default: boa_launch<12>(c, a, smem); break;
+    }
+    CKL();
+    TRY(readback(c, c->d_stage, 1, Q));
+    if (nnb) {
+        std::vector<double> tmp(c->n_global, -1.0);
+        TRY(readback(c, c->d_stage + c->own_cap, 1, tmp.data()));
+        for (int64_t i = 0; i < c->n_global; ++i)
+            if (tmp[i] >= 0.0) nnb[i] = (int64_t)tmp[i];
+    }
+    return LJMD_OK;
+}
+
 extern "C" ljmd_status ljmd_nccl_unique_id(void* out128) {
     if (!out128) return LJMD_E_ARG;
     std::string err;

@@ -28,7 +28,7 @@ EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "
            "ljmd_get_positions", "ljmd_get_velocities", "ljmd_get_particle_energy", "ljmd_get_energy",
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
-           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id")
+           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa")
 
 
 class LjmdError(RuntimeError):
@@ -97,6 +97,7 @@ def load(path: str = LIB_PATH):
         "ljmd_plan_slab": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I, _I], ctypes.c_int),
         "ljmd_measure_fp64_peak": ([ctypes.c_int64, _D], ctypes.c_int),
         "ljmd_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
+        "ljmd_boa": ([vp, ctypes.c_int64, ctypes.c_double, _D, _I], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -274,6 +275,13 @@ class LJMD:
         self._ck(self._lib.ljmd_get_neighbours(self._h, off.ctypes.data_as(_I), g.ctypes.data_as(_I),
                                                g.shape[0]))
         return off, g[:off[-1]]
+
+    def boa(self, ell: int, rcut: float):
+        """Bond-order parameter Q_ell per particle and |N(i)| (Sec. 4.1 of the paper)."""
+        Q = np.zeros(self.n)
+        nnb = np.zeros(self.n, dtype=np.int64)
+        self._ck(self._lib.ljmd_boa(self._h, int(ell), float(rcut), _dp(Q), nnb.ctypes.data_as(_I)))
+        return Q, nnb
 
     def rebuild_steps(self):
         cnt = ctypes.c_int64()
