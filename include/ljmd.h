@@ -159,7 +159,8 @@ const char* ljmd_version(void);
  *   Q_l(i)  = sqrt(4 pi/(2 l + 1) sum_m |q_lm(i)|^2)             (Eq. eqn:Qell)
  * with N(i) = { j : r_ij < rcut } taken from the engine's Verlet list, so rcut <= rc is
  * required (LJMD_E_ARG otherwise); 0 <= ell <= 12.  Q[n] (and nnb[n] = |N(i)| if non-NULL)
- * in the caller's order; with nranks > 1 only owned rows are written; |N(i)| = 0 -> 0. */
+ * in the caller's order; with nranks > 1 only owned rows are written; |N(i)| = 0 -> 0;
+ * at most 160 neighbours inside rcut are used per particle. */
 ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q, int64_t* nnb);
 
 /* Multi-GPU plumbing: fill out128 with a fresh ncclUniqueId (NCCL is loaded with dlopen;

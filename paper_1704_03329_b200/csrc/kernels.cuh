@@ -1133,6 +1133,7 @@ namespace ljmd {
 // (three-term recurrence in l), m >= 0 only: |q_{l,-m}| = |q_{l,m}|; the Condon-Shortley
 // sign is dropped (Q_l depends on |q_lm| only).
 constexpr int kBoaMaxL = 12;
+constexpr int kBoaMaxSel = 160;   // > K: every list entry fits
 
 struct BoaArgs {
     Geo g;
@@ -1186,17 +1187,23 @@ __global__ void __launch_bounds__(kForceThreads) k_boa(BoaArgs a) {
         double re[L + 1], im[L + 1];
 #pragma unroll
         for (int m = 0; m <= L; ++m) re[m] = im[m] = 0.0;
+        // pass 1: the list entries inside rcut (compacted, so the spherical-harmonic work
+        // below is not executed by the whole warp for every list entry)
+        unsigned short sel[kBoaMaxSel];
         int nu = 0;
         for (int k = 0; k < cnt; ++k) {
             const uint4 w = a.nbr[(size_t)(k >> 3) * a.n_pad + t];
             const unsigned ww = (k & 7) < 2 ? w.x : (k & 7) < 4 ? w.y : (k & 7) < 6 ? w.z : w.w;
             const unsigned l = (k & 1) ? (ww >> 16) : (ww & 0xffffu);
             const double* pj = sP + 3 * l;
+            const double r2 = r2_canon(xi.x - pj[0], xi.y - pj[1], xi.z - pj[2]);
+            if (r2 < a.rcut2 && nu < kBoaMaxSel) sel[nu++] = (unsigned short)l;
+        }
+        for (int s = 0; s < nu; ++s) {
+            const double* pj = sP + 3 * sel[s];
             const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
             const double r2 = r2_canon(dx, dy, dz);
-            if (!(r2 < a.rcut2)) continue;
-            ++nu;
-            const double ir = 1.0 / sqrt(r2);
+            const double ir = rsqrt(r2);
             const double ux = dx * ir, uy = dy * ir, z = dz * ir;       // r_hat_ij
             double cr = 1.0, ci = 0.0;                                   // (x + i y)^m
             double pmm = 1.0;                                            // Pbar_m^m = (2m-1)!!
@@ -1208,7 +1215,8 @@ __global__ void __launch_bounds__(kForceThreads) k_boa(BoaArgs a) {
                     double a0 = p0, a1 = p1;
 #pragma unroll
                     for (int ll = m + 2; ll <= L; ++ll) {
-                        const double an = ((2 * ll - 1) * z * a1 - (ll + m - 1) * a0) / (ll - m);
+                        // (ll - m) is a compile-time constant: multiply by its reciprocal
+                        const double an = ((2 * ll - 1) * z * a1 - (ll + m - 1) * a0) * (1.0 / (ll - m));
                         a0 = a1;
                         a1 = an;
                     }
