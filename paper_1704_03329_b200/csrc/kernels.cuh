@@ -718,8 +718,10 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
     bool overflow = false;
     int novf = 0;
     unsigned short pad = 0;
+    uint4 vn = nb > 0 ? in[t] : make_uint4(0u, 0u, 0u, 0u);
     for (int b = 0; b < nb; ++b) {
-        const uint4 v = in[(size_t)b * stride + t];
+        const uint4 v = vn;
+        if (b + 1 < nb) vn = in[(size_t)(b + 1) * stride + t];   // next block in flight
         const unsigned w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
