@@ -163,6 +163,17 @@ const char* ljmd_version(void);
  * at most 160 neighbours inside rcut are used per particle. */
 ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q, int64_t* nnb);
 
+/* Common-neighbour analysis (Sec. 4.2, Algs. alg:cna_I-III, alg:max_cluster_size,
+ * PAPER.md:522-653, 1151-1174) at the current positions, single rank:
+ * bonds = pairs with r < rcut (rcut <= rc: taken from the Verlet list).  For every bond
+ * (i, j): n_nb = |common neighbours|, n_b = bonds among them, n_lcb = bonds in their
+ * largest connected cluster.  cls[n]: 1 fcc (12 x (4,2,1)), 2 hcp (6 x (4,2,1) +
+ * 6 x (4,2,2)), 3 bcc (14 bonds: 8 x (6,6,6) + 6 x (4,4,4)), 0 other.  Optional
+ * trip[n][24]: triplet of the k-th bond of i in ascending neighbour gid, packed
+ * n_nb | n_b << 8 | n_lcb << 16 (0 past the last bond); nnb[n]: bonds per particle.
+ * LJMD_E_CAPACITY if a particle has more than 24 bonds. */
+ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t* trip, int64_t* nnb);
+
 /* Multi-GPU plumbing: fill out128 with a fresh ncclUniqueId (NCCL is loaded with dlopen;
  * the copy torch already mapped is reused).  Rank 0 calls it and broadcasts the 128
  * bytes (e.g. with torch.distributed) into ljmd_options.nccl_id on every rank.  An id

@@ -25,7 +25,7 @@ struct DevFlags {
     int overlap_gid_j;
     int max_staged;              // largest tile staging count at the last build
     int migrate_gid;             // a particle that moved further than one cell plane (INT_MAX: none)
-    int pad1;
+    int overflow;     // analysis capacity exceeded (ljmd_cna)
     unsigned long long maxdisp2; // bits of max |x - x_build|^2 (non-negative double)
     unsigned long long total_nbr;
 };
@@ -1245,5 +1245,147 @@ __global__ void __launch_bounds__(kForceThreads) k_boa(BoaArgs a) {
         a.Q[t] = sqrt(4.0 * 3.14159265358979323846 / (2 * L + 1) * acc);
         a.nnb[t] = (double)nu;
     }
+}
+}  // namespace ljmd
+
+namespace ljmd {
+// ----------------------------------------------------------------------------- common neighbours
+// Common-neighbour analysis (Sec. 4.2, Algs. alg:cna_I-III and alg:max_cluster_size,
+// PAPER.md:522-653, 1151-1174) on the engine's lists, single rank.  Pass 1 (alg:cna_I):
+// the bonded neighbours of every particle (canonical r^2 < rcut^2) as a gid-sorted table.
+// Pass 2 (alg:cna_II/III): for each bond (i, j) the common neighbours C = N(i) & N(j), the
+// bonds among them (the indirect bonds of alg:cna_II restricted to C), and the edges of the
+// largest connected component (alg:max_cluster_size) via bitmask adjacency.
+constexpr int kCnaMax = 24;   // bonded neighbours per particle (12 fcc/hcp, 14 bcc)
+
+struct CnaArgs {
+    Geo g;
+    const double4* x;
+    const int* own_slot;
+    const uint4* nbr;
+    const int* ncount;
+    const int* ocell_of;
+    const int* slot_gid;
+    const int* gid;      // owned t -> gid
+    TileRows tr;
+    int* tab;            // [n_own][kCnaMax] sorted neighbour gids
+    int* tcnt;           // [n_own]
+    const int* tmap;     // gid -> owned t
+    int* trip;           // [n_own][kCnaMax] packed n_nb | n_b << 8 | n_lcb << 16
+    int* cls;            // [n_own] 0 other, 1 fcc, 2 hcp, 3 bcc
+    DevFlags* fl;
+    int n_own, n_pad;
+    double rcut2;
+};
+
+__global__ void k_cna_bonds(CnaArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.n_own) return;
+    int cx, cy, cz;
+    lex_xyz(a.g, a.g.lex_of_oc[a.ocell_of[t]], cx, cy, cz);
+    const int tile = tile_of_cell(a.g, cx, cy, cz);
+    const int* rbeg = a.tr.begin + tile * kRowsMax;
+    const int* roff = a.tr.off + tile * (kRowsMax + 1);
+    const double4 xi = a.x[a.own_slot[t]];
+    int nb[kCnaMax];
+    int n = 0;
+    const int cnt = a.ncount[t];
+    const unsigned short* lst = reinterpret_cast<const unsigned short*>(a.nbr);
+    for (int k = 0; k < cnt; ++k) {
+        const int l = lst[((size_t)(k >> 3) * a.n_pad + t) * 8 + (k & 7)];
+        int r = 0;
+        while (l >= roff[r + 1]) ++r;
+        const int s = rbeg[r] + (l - roff[r]);
+        const double4 xj = a.x[s];
+        if (!(r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z) < a.rcut2)) continue;   // alg:cna_I
+        const int gj = a.slot_gid[s];
+        if (n == kCnaMax) {
+            a.fl->overflow = 1;
+            break;
+        }
+        int p = n++;
+        while (p > 0 && nb[p - 1] > gj) {   // insertion: ascending gid
+            nb[p] = nb[p - 1];
+            --p;
+        }
+        nb[p] = gj;
+    }
+    for (int k = 0; k < n; ++k) a.tab[(size_t)t * kCnaMax + k] = nb[k];
+    a.tcnt[t] = n;
+}
+
+__device__ __forceinline__ bool cna_has(const int* row, int n, int g) {
+    for (int k = 0; k < n; ++k)
+        if (row[k] == g) return true;
+    return false;
+}
+
+__global__ void k_cna_triplets(CnaArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.n_own) return;
+    const int* Ni = a.tab + (size_t)t * kCnaMax;
+    const int ni = a.tcnt[t];
+    int c421 = 0, c422 = 0, c666 = 0, c444 = 0;
+    for (int k = 0; k < ni; ++k) {
+        const int tj = a.tmap[Ni[k]];
+        const int* Nj = a.tab + (size_t)tj * kCnaMax;
+        const int nj = a.tcnt[tj];
+        // common neighbours (both rows ascending): two-pointer intersection
+        int C[kCnaMax];
+        int nc = 0;
+        for (int p = 0, q = 0; p < ni && q < nj;) {
+            if (Ni[p] < Nj[q]) ++p;
+            else if (Ni[p] > Nj[q]) ++q;
+            else { C[nc++] = Ni[p]; ++p; ++q; }
+        }
+        // bonds among the common neighbours (alg:cna_II / III), adjacency as bitmasks
+        unsigned adj[kCnaMax];
+        int nb = 0;
+        for (int u = 0; u < nc; ++u) adj[u] = 0u;
+        for (int u = 0; u < nc; ++u) {
+            const int tu = a.tmap[C[u]];
+            const int* Nu = a.tab + (size_t)tu * kCnaMax;
+            const int nu = a.tcnt[tu];
+            for (int w = u + 1; w < nc; ++w)
+                if (cna_has(Nu, nu, C[w])) {
+                    adj[u] |= 1u << w;
+                    adj[w] |= 1u << u;
+                    ++nb;
+                }
+        }
+        // largest cluster, counted in edges (alg:max_cluster_size)
+        unsigned left = nc >= 32 ? 0xffffffffu : ((1u << nc) - 1u);
+        int lcb = 0;
+        while (left) {
+            const int v = __ffs(left) - 1;
+            unsigned comp = 1u << v, frontier = comp;
+            while (frontier) {
+                const int u = __ffs(frontier) - 1;
+                frontier &= frontier - 1;
+                const unsigned nw = adj[u] & ~comp;
+                comp |= nw;
+                frontier |= nw;
+            }
+            int e = 0;
+            for (unsigned m = comp; m; m &= m - 1) e += __popc(adj[__ffs(m) - 1] & comp);
+            lcb = max(lcb, e / 2);
+            left &= ~comp;
+        }
+        a.trip[(size_t)t * kCnaMax + k] = nc | (nb << 8) | (lcb << 16);
+        c421 += (nc == 4 && nb == 2 && lcb == 1);
+        c422 += (nc == 4 && nb == 2 && lcb == 2);
+        c666 += (nc == 6 && nb == 6 && lcb == 6);
+        c444 += (nc == 4 && nb == 4 && lcb == 4);
+    }
+    int cl = 0;
+    if (ni == 12 && c421 == 12) cl = 1;
+    else if (ni == 12 && c421 == 6 && c422 == 6) cl = 2;
+    else if (ni == 14 && c666 == 8 && c444 == 6) cl = 3;
+    a.cls[t] = cl;
+}
+
+__global__ void k_cna_tmap(int n_own, const int* __restrict__ gid, int* __restrict__ tmap) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_own) tmap[gid[t]] = t;
 }
 }  // namespace ljmd

@@ -1355,6 +1355,70 @@ extern "C" ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q
     return LJMD_OK;
 }
 
+
+extern "C" ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t* trip, int64_t* nnb) {
+    TRY(check_ctx(c));
+    if (!cls || !(rcut > 0.0)) return set_err(c, LJMD_E_ARG, "ljmd_cna: cls and rcut > 0 required");
+    if (rcut > c->rc)
+        return set_err(c, LJMD_E_ARG, "ljmd_cna: rcut %g exceeds the force cutoff rc = %g (list validity)", rcut,
+                       c->rc);
+    if (c->nranks > 1 || c->split) return set_err(c, LJMD_E_ARG, "ljmd_cna: single rank only");
+    const int n = c->n_own;
+    int *tab = nullptr, *tcnt = nullptr, *tmap = nullptr, *dtrip = nullptr, *dcls = nullptr;
+    TRY(dalloc(c, &tab, (size_t)n * kCnaMax));
+    TRY(dalloc(c, &tcnt, n));
+    TRY(dalloc(c, &tmap, (size_t)c->n_global));
+    TRY(dalloc(c, &dtrip, (size_t)n * kCnaMax));
+    TRY(dalloc(c, &dcls, n));
+    TRY(reset_flags(c));
+    CnaArgs a;
+    a.g = c->geo;
+    a.x = c->x[c->xc];
+    a.own_slot = c->own_slot;
+    a.nbr = c->nbr8;
+    a.ncount = c->ncount;
+    a.ocell_of = c->ocell_of;
+    a.slot_gid = c->slot_gid;
+    a.gid = c->gid[c->oc_cur];
+    a.tr = TileRows{c->tr_begin, c->tr_off};
+    a.tab = tab;
+    a.tcnt = tcnt;
+    a.tmap = tmap;
+    a.trip = dtrip;
+    a.cls = dcls;
+    a.fl = c->d_fl;
+    a.n_own = n;
+    a.n_pad = c->n_pad;
+    a.rcut2 = rcut * rcut;
+    k_cna_tmap<<<nblk(n, 256), 256, 0, c->stream>>>(n, a.gid, tmap);
+    CKL();
+    k_cna_bonds<<<nblk(n, 128), 128, 0, c->stream>>>(a);
+    CKL();
+    k_cna_triplets<<<nblk(n, 128), 128, 0, c->stream>>>(a);
+    CKL();
+    TRY(sync_flags(c));
+    ljmd_status st = LJMD_OK;
+    if (c->h_fl->overflow)
+        st = set_err(c, LJMD_E_CAPACITY, "ljmd_cna: more than %d bonded neighbours inside rcut", kCnaMax);
+    if (st == LJMD_OK) {
+        std::vector<int> hc(n), hcnt(n), ht(trip ? (size_t)n * kCnaMax : 0), g(n);
+        cudaMemcpyAsync(hc.data(), dcls, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(hcnt.data(), tcnt, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream);
+        if (trip) cudaMemcpyAsync(ht.data(), dtrip, sizeof(int) * ht.size(), cudaMemcpyDeviceToHost, c->stream);
+        cudaMemcpyAsync(g.data(), c->gid[c->oc_cur], sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream);
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) st = set_err(c, LJMD_E_CUDA, "ljmd_cna readback");
+        for (int t = 0; st == LJMD_OK && t < n; ++t) {
+            cls[g[t]] = hc[t];
+            if (nnb) nnb[g[t]] = hcnt[t];
+            if (trip)
+                for (int k = 0; k < kCnaMax; ++k)
+                    trip[(size_t)g[t] * kCnaMax + k] = k < hcnt[t] ? ht[(size_t)t * kCnaMax + k] : 0;
+        }
+    }
+    for (void* p : {(void*)tab, (void*)tcnt, (void*)tmap, (void*)dtrip, (void*)dcls}) cudaFree(p);
+    return st;
+}
+
 extern "C" ljmd_status ljmd_nccl_unique_id(void* out128) {
     if (!out128) return LJMD_E_ARG;
     std::string err;

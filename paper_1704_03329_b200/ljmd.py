@@ -28,7 +28,7 @@ EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "
            "ljmd_get_positions", "ljmd_get_velocities", "ljmd_get_particle_energy", "ljmd_get_energy",
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
-           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa")
+           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna")
 
 
 class LjmdError(RuntimeError):
@@ -98,6 +98,8 @@ def load(path: str = LIB_PATH):
         "ljmd_measure_fp64_peak": ([ctypes.c_int64, _D], ctypes.c_int),
         "ljmd_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
         "ljmd_boa": ([vp, ctypes.c_int64, ctypes.c_double, _D, _I], ctypes.c_int),
+        "ljmd_cna": ([vp, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), _I],
+                     ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -282,6 +284,22 @@ class LJMD:
         nnb = np.zeros(self.n, dtype=np.int64)
         self._ck(self._lib.ljmd_boa(self._h, int(ell), float(rcut), _dp(Q), nnb.ctypes.data_as(_I)))
         return Q, nnb
+
+    def cna(self, rcut: float, triplets: bool = False):
+        """Common-neighbour analysis (Sec. 4.2): class per particle (0 other, 1 fcc, 2 hcp,
+        3 bcc), bonds per particle, and optionally the (n_nb, n_b, n_lcb) triplets
+        [n, 24, 3] of each bond in ascending neighbour gid."""
+        P32 = ctypes.POINTER(ctypes.c_int32)
+        cls = np.zeros(self.n, dtype=np.int32)
+        nnb = np.zeros(self.n, dtype=np.int64)
+        tr = np.zeros((self.n, 24), dtype=np.int32) if triplets else None
+        self._ck(self._lib.ljmd_cna(self._h, float(rcut), cls.ctypes.data_as(P32),
+                                    tr.ctypes.data_as(P32) if tr is not None else None,
+                                    nnb.ctypes.data_as(_I)))
+        if tr is None:
+            return cls, nnb
+        t3 = np.stack([tr & 0xff, (tr >> 8) & 0xff, (tr >> 16) & 0xff], axis=-1)
+        return cls, nnb, t3
 
     def rebuild_steps(self):
         cnt = ctypes.c_int64()
