@@ -44,7 +44,8 @@ class _LJ(ctypes.Structure):
 class _Params(ctypes.Structure):
     _fields_ = [("lj", _LJ), ("dt", ctypes.c_double), ("mass", ctypes.c_double),
                 ("delta", ctypes.c_double), ("ns", ctypes.c_int64), ("check", ctypes.c_int64),
-                ("mode", ctypes.c_int64), ("energy_every", ctypes.c_int64)]
+                ("mode", ctypes.c_int64), ("energy_every", ctypes.c_int64),
+                ("nu_dt", ctypes.c_double), ("temp", ctypes.c_double), ("seed", ctypes.c_uint64)]
 
 
 def _load():
@@ -76,6 +77,12 @@ def _load():
         lib.orc_run.restype = ctypes.c_int64
         lib.orc_run.argtypes = [ctypes.c_int64, _D, _D, _D, ctypes.POINTER(_Params), ctypes.c_int64,
                                 _D, _D, _D, _I, ctypes.c_int64]
+        U32 = ctypes.POINTER(ctypes.c_uint32)
+        lib.orc_philox4x32.restype = None
+        lib.orc_philox4x32.argtypes = [U32, U32, U32]
+        lib.orc_andersen.restype = ctypes.c_int64
+        lib.orc_andersen.argtypes = [ctypes.c_int64, _D, ctypes.c_uint64, ctypes.c_int64, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double]
         _lib = lib
     return _lib
 
@@ -200,6 +207,23 @@ def forces_rows(pos, box, rows, lj: LJ = LJ()):
     return Forces(F, e, S, A, float(e.sum()))
 
 
+def philox4x32(ctr, key):
+    """O8: Philox4x32-10 block (4 x uint32 counter, 2 x uint32 key) -> 4 x uint32."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    o = np.zeros(4, dtype=np.uint32)
+    U32 = ctypes.POINTER(ctypes.c_uint32)
+    _load().orc_philox4x32(c.ctypes.data_as(U32), k.ctypes.data_as(U32), o.ctypes.data_as(U32))
+    return o
+
+
+def andersen(vel, seed, step, nu_dt, temp, mass=1.0):
+    """O8: one Andersen pass (reading R19) on a copy of vel; returns (vel', n_resampled)."""
+    v = _f64(vel, (-1, 3)).copy()
+    k = _load().orc_andersen(v.shape[0], _dp(v), seed, step, nu_dt, temp, mass)
+    return v, int(k)
+
+
 def neumaier_sum(x):
     x = _f64(x).ravel()
     return _load().orc_sum(_dp(x), x.shape[0])
@@ -221,8 +245,9 @@ class Run:
 
 
 def run(pos, vel, box, nsteps, lj: LJ = LJ(), dt=0.005, mass=1.0, delta=0.25, ns=20,
-        check=0, mode="list", energy_every=10):
-    """O6/O7: velocity-Verlet trajectory with the paper's rebuild schedule."""
+        check=0, mode="list", energy_every=10, thermostat=None):
+    """O6/O7: velocity-Verlet trajectory with the paper's rebuild schedule.
+    thermostat = (nu, T, seed): O8 Andersen collisions after every step."""
     p = _f64(pos, (-1, 3)).copy()
     v = _f64(vel, (-1, 3)).copy()
     b = _f64(box)
@@ -233,7 +258,11 @@ def run(pos, vel, box, nsteps, lj: LJ = LJ(), dt=0.005, mass=1.0, delta=0.25, ns
     ke = np.zeros(ns_samp)
     cap = nsteps + 1
     rs = np.zeros(cap, dtype=np.int64)
-    prm = _Params(lj.c(), dt, mass, delta, ns, check, 1 if mode == "list" else 0, energy_every)
+    nu, temp, seed = thermostat if thermostat is not None else (0.0, 0.0, 0)
+    if nu * dt > 1.0 or nu < 0.0 or temp < 0.0:
+        raise ValueError("Andersen thermostat needs 0 <= nu*dt <= 1 and T >= 0")
+    prm = _Params(lj.c(), dt, mass, delta, ns, check, 1 if mode == "list" else 0, energy_every,
+                  nu * dt, temp, seed)
     nreb = _load().orc_run(n, _dp(p), _dp(v), _dp(b), ctypes.byref(prm), nsteps,
                            _dp(F), _dp(pe), _dp(ke), _ip(rs), cap)
     if nreb < 0:

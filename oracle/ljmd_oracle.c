@@ -23,6 +23,12 @@
  *                          (P:659-675), Tab. access_descriptors
  *   O7 rebuild schedule  : IntegratorRange, every Ns = 20 steps
  *                          (P:728); optional displacement check (R7)
+ *   O8 Andersen thermostat (reading R19): after line 8 of every step each
+ *                          particle, with probability nu*dt, draws a new velocity
+ *                          from N(0, T/m) per component.  Random numbers from the
+ *                          counter-based Philox4x32-10 (Salmon et al. 2011), keyed by
+ *                          (seed, gid, step), written out here independently of the
+ *                          GPU's copy and pinned by its published known-answer vectors.
  *
  * Every function is pinned by a -m "not gpu" test (tests/test_oracle_*.py)
  * against closed forms, golden fixtures or brute force; see DESIGN.md §Oracle.
@@ -336,6 +342,77 @@ void orc_forces_rows(int64_t n, const double *pos, const double box[3], const or
 }
 
 /* ------------------------------------------------------------- O6 / O7 -- */
+/* ------------------------------------------------------------------ O8 -- */
+/* Philox4x32-10: 10 rounds of two 32x32->64 multiplies and a Weyl key schedule. */
+void orc_philox4x32(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* 53-bit uniform in [0, 1) from two words (a supplies 27 bits, b 26). */
+static double u53(uint32_t a, uint32_t b)
+{
+    return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
+}
+
+/* Reading R19: draws of particle gid at step `step` (1-based, the step being completed).
+ * Block k = 0: (w0, w1) -> decision uniform, (w2, w3) -> U1; k = 1: U2, U3; k = 2: U4.
+ * Selected iff decision < nu*dt; then, Box-Muller,
+ *   v = sqrt(T/m) (R1 cos(2 pi U2), R1 sin(2 pi U2), R2 cos(2 pi U4)),
+ *   R1 = sqrt(-2 ln(1 - U1)), R2 = sqrt(-2 ln(1 - U3)).  Returns 1 if selected. */
+int orc_andersen_draw(uint64_t seed, int64_t gid, int64_t step, double nu_dt, double sd, double v[3])
+{
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {(uint32_t)gid, (uint32_t)step, (uint32_t)((uint64_t)step >> 32), 0u};
+    uint32_t w[4], w1[4], w2[4];
+    orc_philox4x32(ctr, key, w);
+    if (!(u53(w[0], w[1]) < nu_dt)) return 0;
+    ctr[3] = 1u;
+    orc_philox4x32(ctr, key, w1);
+    ctr[3] = 2u;
+    orc_philox4x32(ctr, key, w2);
+    double U1 = u53(w[2], w[3]), U2 = u53(w1[0], w1[1]), U3 = u53(w1[2], w1[3]), U4 = u53(w2[0], w2[1]);
+    const double two_pi = 6.283185307179586;
+    double R1 = sqrt(-2.0 * log(1.0 - U1)), R2 = sqrt(-2.0 * log(1.0 - U3));
+    v[0] = sd * (R1 * cos(two_pi * U2));
+    v[1] = sd * (R1 * sin(two_pi * U2));
+    v[2] = sd * (R2 * cos(two_pi * U4));
+    return 1;
+}
+
+/* One thermostat pass over all particles (gid = row); returns the number resampled. */
+int64_t orc_andersen(int64_t n, double *vel, uint64_t seed, int64_t step, double nu_dt, double temp,
+                     double mass)
+{
+    double sd = sqrt(temp / mass);
+    int64_t k = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double v[3];
+        if (orc_andersen_draw(seed, i, step, nu_dt, sd, v)) {
+            vel[3 * i] = v[0];
+            vel[3 * i + 1] = v[1];
+            vel[3 * i + 2] = v[2];
+            ++k;
+        }
+    }
+    return k;
+}
+
 typedef struct {
     orc_lj lj;
     double dt;            /* delta t                                           */
@@ -345,6 +422,9 @@ typedef struct {
     int64_t check;        /* 1: also rebuild when 2 max|x - x_build| > delta   */
     int64_t mode;         /* 0: brute-force forces, 1: cell + neighbour list   */
     int64_t energy_every; /* sample PE/KE every k steps (10)            */
+    double nu_dt;         /* Andersen collision probability per step (0: NVE)  */
+    double temp;          /* Andersen target temperature T (k_B = 1)           */
+    uint64_t seed;        /* Philox key                                        */
 } orc_params;
 
 typedef struct {
@@ -425,6 +505,7 @@ int64_t orc_run(int64_t n, double *pos, double *vel, const double box[3], const 
         }
         pe = orc_forces(n, pos, box, &p->lj, p->mode == 1 ? L.off : NULL, L.nbr, F, NULL, NULL, NULL);
         for (int64_t i = 0; i < 3 * n; ++i) vel[i] = vel[i] + h * F[i];
+        if (p->nu_dt > 0.0) orc_andersen(n, vel, p->seed, step, p->nu_dt, p->temp, p->mass);
         if (p->energy_every > 0 && step % p->energy_every == 0) {
             if (pe_hist) pe_hist[ks] = pe;
             if (ke_hist) ke_hist[ks] = orc_kinetic(n, vel, p->mass);
