@@ -163,6 +163,15 @@ const char* ljmd_version(void);
  * at most 160 neighbours inside rcut are used per particle. */
 ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q, int64_t* nnb);
 
+/* Andersen thermostat ("coupled the system to an Andersen thermostat"; SPEC
+ * S:346-354; reading R19).  From the next ljmd_step on, at the end of every step (after
+ * line 8 of Alg. alg:VelocityVerlet, before the energy sample) each particle is, with
+ * probability nu*dt, given a new velocity drawn from N(0, T/m) per component.  The draws
+ * are Philox4x32-10 keyed by (seed, gid, step index since init/set_state), so they do not
+ * depend on the number of ranks.  nu = 0 switches it off (NVE, the default).
+ * LJMD_E_ARG if nu < 0, T < 0 or nu*dt > 1. */
+ljmd_status ljmd_set_thermostat(ljmd_ctx* c, double nu, double temperature, uint64_t seed);
+
 /* Common-neighbour analysis (Sec. 4.2, Algs. alg:cna_I-III, alg:max_cluster_size,
  * PAPER.md:522-653, 1151-1174) at the current positions, single rank:
  * bonds = pairs with r < rcut (rcut <= rc: taken from the Verlet list).  For every bond

@@ -783,7 +783,9 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
 //   kKick  : v += h F (line 8), F stored          -- last step of ljmd_step
 //   kKKD   : v += h F (line 8) ; [KE sample] ; v += h F ; x' = x + dt v (line 6 of the
 //            next step) written to the other position buffer
-enum { kStore = 0, kKick = 1, kKKD = 2 };
+//   | kThermo : Andersen collisions after line 8, a separate instantiation so the
+//            default kernels keep their register allocation
+enum { kStore = 0, kKick = 1, kKKD = 2, kThermo = 4 };
 
 struct ForceArgs {
     Geo g;
@@ -805,7 +807,53 @@ struct ForceArgs {
     int n_own, n_pad;
     double rc2, c12, nc6, a12, na6, a0;   // nc6 = -c6, na6 = -a6 (fold into DFMA operands)
     double h, dt, half_m;
+    // Andersen thermostat (reading R19): nu_dt = 0 disables
+    const int* gid;
+    double nu_dt, sd;                     // collision probability per step, sqrt(T/m)
+    unsigned long long seed;
+    long long step;                       // 1-based index of the step this launch completes
 };
+
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, so the draws of (gid, step) do not
+// depend on the decomposition or the launch order.
+__device__ __forceinline__ uint4 philox4x32(uint4 c, unsigned k0, unsigned k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const unsigned lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const unsigned lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ double uniform53(unsigned a, unsigned b) {
+    return __dmul_rn(__dadd_rn(__dmul_rn((double)(a >> 5), 67108864.0), (double)(b >> 6)),
+                     1.0 / 9007199254740992.0);
+}
+
+// Andersen collision of one particle at the end of step a.step: with probability nu_dt the
+// velocity is replaced by a Maxwell-Boltzmann draw (Box-Muller on Philox uniforms).
+__device__ __forceinline__ void andersen(unsigned long long seed, long long step, double nu_dt, double sd, int g,
+                                         double& vx, double& vy, double& vz) {
+    const unsigned k0 = (unsigned)seed, k1 = (unsigned)(seed >> 32);
+    uint4 c = make_uint4((unsigned)g, (unsigned)step, (unsigned)((unsigned long long)step >> 32), 0u);
+    const uint4 w = philox4x32(c, k0, k1);
+    if (!(uniform53(w.x, w.y) < nu_dt)) return;
+    c.w = 1u;
+    const uint4 w1 = philox4x32(c, k0, k1);
+    c.w = 2u;
+    const uint4 w2 = philox4x32(c, k0, k1);
+    const double U1 = uniform53(w.z, w.w), U2 = uniform53(w1.x, w1.y);
+    const double U3 = uniform53(w1.z, w1.w), U4 = uniform53(w2.x, w2.y);
+    const double two_pi = 6.283185307179586;
+    const double R1 = sqrt(__dmul_rn(-2.0, log(__dadd_rn(1.0, -U1))));
+    const double R2 = sqrt(__dmul_rn(-2.0, log(__dadd_rn(1.0, -U3))));
+    vx = __dmul_rn(sd, __dmul_rn(R1, cos(__dmul_rn(two_pi, U2))));
+    vy = __dmul_rn(sd, __dmul_rn(R1, sin(__dmul_rn(two_pi, U2))));
+    vz = __dmul_rn(sd, __dmul_rn(R2, cos(__dmul_rn(two_pi, U4))));
+}
 
 constexpr int kForceThreads = 320;   // ~16 cells x 18.5 particles per tile at rho = 0.8442
 
@@ -903,7 +951,7 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
         }
         cur = nxt;
     }
-    if (MODE == kStore) {
+    if ((MODE & 3) == kStore) {
         a.fx[t] = fx; a.fy[t] = fy; a.fz[t] = fz;
         if (ENERGY) {
             const double vx = a.vx[t], vy = a.vy[t], vz = a.vz[t];
@@ -915,9 +963,10 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
         vx = __dadd_rn(vx, __dmul_rn(a.h, fx));
         vy = __dadd_rn(vy, __dmul_rn(a.h, fy));
         vz = __dadd_rn(vz, __dmul_rn(a.h, fz));
+        if (MODE & kThermo) andersen(a.seed, a.step, a.nu_dt, a.sd, a.gid[t], vx, vy, vz);
         if (ENERGY)
             ke += a.half_m * __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
-        if (MODE == kKick) {
+        if ((MODE & 3) == kKick) {
             a.fx[t] = fx; a.fy[t] = fy; a.fz[t] = fz;
         } else {
             // line 6 of the next step: v += dt/(2m) F ; r += dt v (Listing lst:position_update)

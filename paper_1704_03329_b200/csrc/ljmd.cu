@@ -55,6 +55,8 @@ struct ljmd_ctx {
     // ---- slot space
     double4* x[2] = {nullptr, nullptr};
     int xc = 0;                       // current position buffer
+    double nu_dt = 0.0, thermo_sd = 0.0;   // Andersen thermostat (ljmd_set_thermostat)
+    unsigned long long thermo_seed = 0;
     float4* xf = nullptr;
     int* slot_gid = nullptr;
     // ---- owned space (double-buffered across rebuilds)
@@ -497,6 +499,11 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.h = 0.5 * c->dt / c->opt.mass;
     a.dt = c->dt;
     a.half_m = 0.5 * c->opt.mass;
+    a.gid = c->gid[c->oc_cur];
+    a.nu_dt = c->nu_dt;
+    a.sd = c->thermo_sd;
+    a.seed = c->thermo_seed;
+    a.step = c->steps_done;
     return a;
 }
 
@@ -517,10 +524,14 @@ ljmd_status set_force_attrs(ljmd_ctx* c) {
     cudaError_t e = cudaFuncSetAttribute(k_build_nlist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStageSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_list_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRrSmem);
+    constexpr int KT = kKick | kThermo, DT = kKKD | kThermo;
     for (cudaError_t r : {force_attr<true, kStore, false>(), force_attr<true, kKick, false>(),
                           force_attr<true, kKKD, false>(), force_attr<true, kKKD, true>(),
                           force_attr<false, kStore, false>(), force_attr<false, kKick, false>(),
-                          force_attr<false, kKKD, false>(), force_attr<false, kKKD, true>()})
+                          force_attr<false, kKKD, false>(), force_attr<false, kKKD, true>(),
+                          force_attr<true, KT, false>(), force_attr<true, DT, false>(), force_attr<true, DT, true>(),
+                          force_attr<false, KT, false>(), force_attr<false, DT, false>(),
+                          force_attr<false, DT, true>()})
         if (r != cudaSuccess) e = r;
     if (e != cudaSuccess) return set_err(c, LJMD_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return LJMD_OK;
@@ -540,16 +551,18 @@ ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check) {
         e1 = c->ev[k + 1];
         CK(cudaEventRecord(e0, c->stream));
     }
+    constexpr int KT = kKick | kThermo, DT = kKKD | kThermo;
+    const bool th = c->nu_dt > 0.0 && mode != kStore;
     if (energy) {
         if (mode == kStore) force_launch<true, kStore, false>(c, a);
-        else if (mode == kKick) force_launch<true, kKick, false>(c, a);
-        else if (check) force_launch<true, kKKD, true>(c, a);
-        else force_launch<true, kKKD, false>(c, a);
+        else if (mode == kKick) th ? force_launch<true, KT, false>(c, a) : force_launch<true, kKick, false>(c, a);
+        else if (check) th ? force_launch<true, DT, true>(c, a) : force_launch<true, kKKD, true>(c, a);
+        else th ? force_launch<true, DT, false>(c, a) : force_launch<true, kKKD, false>(c, a);
     } else {
         if (mode == kStore) force_launch<false, kStore, false>(c, a);
-        else if (mode == kKick) force_launch<false, kKick, false>(c, a);
-        else if (check) force_launch<false, kKKD, true>(c, a);
-        else force_launch<false, kKKD, false>(c, a);
+        else if (mode == kKick) th ? force_launch<false, KT, false>(c, a) : force_launch<false, kKick, false>(c, a);
+        else if (check) th ? force_launch<false, DT, true>(c, a) : force_launch<false, kKKD, true>(c, a);
+        else th ? force_launch<false, DT, false>(c, a) : force_launch<false, kKKD, false>(c, a);
     }
     CKL();
     if (c->opt.profile) {
@@ -1355,6 +1368,17 @@ extern "C" ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q
     return LJMD_OK;
 }
 
+
+extern "C" ljmd_status ljmd_set_thermostat(ljmd_ctx* c, double nu, double temperature, uint64_t seed) {
+    TRY(check_ctx(c));
+    if (!(nu >= 0.0) || !(temperature >= 0.0) || !(nu * c->dt <= 1.0))
+        return set_err(c, LJMD_E_ARG, "ljmd_set_thermostat: need nu >= 0, T >= 0 and nu*dt <= 1 (nu*dt = %g)",
+                       nu * c->dt);
+    c->nu_dt = nu * c->dt;
+    c->thermo_sd = std::sqrt(temperature / c->opt.mass);
+    c->thermo_seed = seed;
+    return LJMD_OK;
+}
 
 extern "C" ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t* trip, int64_t* nnb) {
     TRY(check_ctx(c));

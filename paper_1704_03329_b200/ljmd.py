@@ -28,7 +28,7 @@ EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "
            "ljmd_get_positions", "ljmd_get_velocities", "ljmd_get_particle_energy", "ljmd_get_energy",
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
-           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna")
+           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna", "ljmd_set_thermostat")
 
 
 class LjmdError(RuntimeError):
@@ -98,6 +98,7 @@ def load(path: str = LIB_PATH):
         "ljmd_measure_fp64_peak": ([ctypes.c_int64, _D], ctypes.c_int),
         "ljmd_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
         "ljmd_boa": ([vp, ctypes.c_int64, ctypes.c_double, _D, _I], ctypes.c_int),
+        "ljmd_set_thermostat": ([vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64], ctypes.c_int),
         "ljmd_cna": ([vp, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), _I],
                      ctypes.c_int),
     }
@@ -284,6 +285,11 @@ class LJMD:
         nnb = np.zeros(self.n, dtype=np.int64)
         self._ck(self._lib.ljmd_boa(self._h, int(ell), float(rcut), _dp(Q), nnb.ctypes.data_as(_I)))
         return Q, nnb
+
+    def set_thermostat(self, nu: float, temperature: float, seed: int = 0):
+        """Andersen thermostat: collision frequency nu (probability nu*dt per step),
+        target temperature T, Philox seed; nu = 0 restores NVE."""
+        self._ck(self._lib.ljmd_set_thermostat(self._h, float(nu), float(temperature), int(seed)))
 
     def cna(self, rcut: float, triplets: bool = False):
         """Common-neighbour analysis (Sec. 4.2): class per particle (0 other, 1 fcc, 2 hcp,

@@ -18,7 +18,7 @@ import ljinputs as li
 pytestmark = pytest.mark.gpu
 
 
-def run_ranks(nranks, pos, vel, box, nsteps, **kw):
+def run_ranks(nranks, pos, vel, box, nsteps, thermostat=None, **kw):
     from paper_1704_03329_b200 import ljmd
     gid = ljmd.local_group_id(uuid.uuid4().hex)
     out = [None] * nranks
@@ -27,6 +27,8 @@ def run_ranks(nranks, pos, vel, box, nsteps, **kw):
     def work(r):
         try:
             with ljmd.LJMD(pos, vel, box, rank=r, nranks=nranks, nccl_id=gid, **kw) as ctx:
+                if thermostat is not None:
+                    ctx.set_thermostat(*thermostat)
                 ctx.step(nsteps)
                 F = np.full((len(pos), 3), np.nan)
                 X = np.full((len(pos), 3), np.nan)
@@ -61,9 +63,11 @@ def run_ranks(nranks, pos, vel, box, nsteps, **kw):
     return merged, out
 
 
-def single(pos, vel, box, nsteps, **kw):
+def single(pos, vel, box, nsteps, thermostat=None, **kw):
     from paper_1704_03329_b200 import ljmd
     with ljmd.LJMD(pos, vel, box, **kw) as ctx:
+        if thermostat is not None:
+            ctx.set_thermostat(*thermostat)
         ctx.step(nsteps)
         return dict(F=ctx.forces(), X=ctx.positions(), V=ctx.velocities(), e=ctx.energy(),
                     hist=ctx.energy_history(), rs=ctx.rebuild_steps())
