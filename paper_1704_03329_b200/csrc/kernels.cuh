@@ -568,7 +568,7 @@ struct NlistArgs {
 // blocks of 8 entries written with 16-byte stores from registers.
 constexpr int kBuildThreads = 320;
 
-__global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
+__global__ void __launch_bounds__(kBuildThreads, 5) k_build_nlist(NlistArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -591,6 +591,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     const size_t stride = (size_t)a.n_pad;
+    const float thr_lo = a.thr_lo, thr_hi = a.thr_hi;
+    const int K = a.K;
     unsigned long long kk = 0ull;
     for (int q = threadIdx.x; q < m; q += kBuildThreads) {
         const int t = t0 + q;
@@ -602,9 +604,11 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
         const int r0 = (cz + 1 - T.z0) * (T.ty + 2) + (cy + 1 - T.y0);
         const int li = a.tr.off[tile * (kRowsMax + 1) + r0] + si - a.tr.begin[tile * kRowsMax + r0];
         const float4 fi = sF[li];
-        // entry k of particle t lives at ((k >> 3) * n_pad + t) * 8 + (k & 7) (blocked layout)
-        unsigned short* out = reinterpret_cast<unsigned short*>(a.nbr8) + (size_t)t * 8;
-        const size_t bstride = stride * 8;
+        // entry k of particle t lives at ((k >> 3) * n_pad + t) * 8 + (k & 7) (blocked layout):
+        // the pending block is shifted in from the top of four registers (one funnel shift
+        // each) and leaves as one 16-byte store when it is full (K is a multiple of 8)
+        uint4* outb = a.nbr8 + t;
+        unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
         int k = 0;
         for (int dz = -1; dz <= 1; ++dz) {
             const float ddz = dz < 0 ? fi.z - a.zlo_f[cz] : (dz > 0 ? a.zlo_f[cz + 1] - fi.z : 0.f);
@@ -641,8 +645,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
                     const float4 fj = sF[jl];
                     const float fx = fi.x - fj.x, fy = fi.y - fj.y, fz = fi.z - fj.z;
                     const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-                    if (r2f >= a.thr_hi || jl == li) continue;
-                    bool take = r2f < a.thr_lo;
+                    if (r2f >= thr_hi || jl == li) continue;
+                    bool take = r2f < thr_lo;
                     if (!take || r2f < 1e-6f) {          // rare: decide in fp64 (the oracle's test)
                         const int j = rbeg + (jl - roff);
                         const double4 xj = a.x[j];
@@ -654,15 +658,28 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_nlist(NlistArgs a) {
                         }
                     }
                     if (take) {
-                        if (k < a.K) out[(size_t)(k >> 3) * bstride + (k & 7)] = (unsigned short)jl;
+                        w0 = __funnelshift_r(w0, w1, 16);
+                        w1 = __funnelshift_r(w1, w2, 16);
+                        w2 = __funnelshift_r(w2, w3, 16);
+                        w3 = __funnelshift_r(w3, (unsigned)jl, 16);
+                        if ((k & 7) == 7) {
+                            if (k < K) *outb = make_uint4(w0, w1, w2, w3);
+                            outb += stride;
+                        }
                         ++k;
                     }
                 }
             }
         }
-        if ((k & 7) && k < a.K) {   // pad the last block with the tile's sentinel index
-            const unsigned short sen = (unsigned short)a.tr.off[tile * (kRowsMax + 1) + T.R];
-            for (int e = k & 7; e < 8; ++e) out[(size_t)(k >> 3) * bstride + e] = sen;
+        if ((k & 7) && k < K) {   // pad the last block with the tile's sentinel index
+            const unsigned sen = (unsigned)a.tr.off[tile * (kRowsMax + 1) + T.R];
+            for (int e = k & 7; e < 8; ++e) {
+                w0 = __funnelshift_r(w0, w1, 16);
+                w1 = __funnelshift_r(w1, w2, 16);
+                w2 = __funnelshift_r(w2, w3, 16);
+                w3 = __funnelshift_r(w3, sen, 16);
+            }
+            *outb = make_uint4(w0, w1, w2, w3);
         }
         a.ncount[t] = k;
         atomicMax(&a.fl->max_nbr, k);
