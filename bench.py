@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-boa", action="store_true")
+    ap.add_argument("--newton3", action="store_true",
+                    help="NEXT-1 half-list force with reaction reductions (single GPU; slower)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -224,7 +226,8 @@ def main():
     stream = torch.cuda.current_stream()
     check = 1 if (args.check or cfg.rebuild_check) else 0
     opts = ljmd.default_options(device=local, stream=stream.cuda_stream, profile=1,
-                                rebuild_check=check, rank=rank, nranks=world)
+                                rebuild_check=check, rank=rank, nranks=world,
+                                newton3=1 if args.newton3 else 0)
     if id_buf is not None:
         import ctypes
         opts.nccl_id = ctypes.cast(id_buf, ctypes.c_void_p)
@@ -256,13 +259,14 @@ def main():
     f_ms = (st1["force_ms"] - st0["force_ms"]) / max(launches, 1)
     cand = st1["total_neighbours"]
     e_frac = 1.0 / 10.0
-    flops = cand * (FLOPS_PER_CAND * (1 - e_frac) + FLOPS_PER_CAND_E * e_frac)
+    # the half list holds each pair once: half the candidates per launch
+    flops = (cand / 2 if args.newton3 else cand) * (FLOPS_PER_CAND * (1 - e_frac) + FLOPS_PER_CAND_E * e_frac)
     achieved = flops / (f_ms * 1e-3) / 1e12
     # DRAM bytes per force launch from the committed ncu --set full capture of this config
     traffic, traffic_src = None, None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "force_traffic.json")))
-        if tj.get("workload") == cfg.name:
+        if tj.get("workload") == cfg.name and not args.newton3:
             traffic = tj["dram_bytes_per_launch"]
             traffic_src = tj["source"]
     except (OSError, ValueError, KeyError):
@@ -336,11 +340,14 @@ def main():
                    "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "energy_every": 10, "dt": li.DT,
                    "t0": cfg.t0, "rebuild_policy": "safe" if check else "paper-fixed-20",
                    "parallelism": f"z-slab x{world}",
+                   "force_path": "newton3 half list + reductions (NEXT-1)" if args.newton3 else
+                   "full list, fused velocity Verlet",
                    "l2": "working set > L2 (list %.0f MB + positions %.0f MB)" % (
                        4 * cand / 1e6, 32 * (n + st1["n_ghost"]) / 1e6)},
         "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
         "transport": "nccl" if world > 1 else "none",
-        "roofline": {"bound": "alu", "kernel": "k_force (fp64 LJ pair loop)", "achieved": achieved,
+        "roofline": {"bound": "alu",
+                     "kernel": "k_force_half (fp64 LJ pair loop)" if args.newton3 else "k_force (fp64 LJ pair loop)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": traffic_src,
                      "flops_per_launch": flops, "avg_launch_ms": f_ms, "peak_source": peak_src,

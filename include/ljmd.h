@@ -76,6 +76,11 @@ typedef struct {
                                of slabs (bitwise), at ~15 % more force-kernel time          */
     int64_t split_self;     /* 1: with nranks = 1, still run the slab-exchange path (halo
                                planes sent to itself through the transport; testing)        */
+    int64_t newton3;        /* 1: Newton-3 half list: each pair
+                               evaluated once, reactions added with fp64 global reductions,
+                               velocity Verlet in a separate pass; nranks = 1 only.  Slower
+                               than the default on B200; sums not bitwise
+                               reproducible (reduction order)                                */
 } ljmd_options;
 
 typedef struct {

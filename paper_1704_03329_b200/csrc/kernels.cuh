@@ -1455,3 +1455,232 @@ __global__ void k_cna_tmap(int n_own, const int* __restrict__ gid, int* __restri
     if (t < n_own) tmap[gid[t]] = t;
 }
 }  // namespace ljmd
+
+namespace ljmd {
+// ----------------------------------------------------------------------------- Newton-3 half list
+// SURVEY §8(f) NEXT-1 ("a factor of two" from Newton's third law, which the paper
+// does not use).  Each unordered pair is kept once, at the particle with the smaller gid (a
+// periodic image carries its source's gid, so the pair with an image is also kept once); the
+// force kernel adds f_ij to i in registers and the reaction -f_ij to j's owner with fp64
+// global reductions (RED.ADD.F64 in L2), then a separate velocity-Verlet kernel runs on the
+// completed F.  Single rank only (a reverse halo for the ghosts of other ranks is not built).
+
+// slot -> owned index of its particle (ghost slots: the source particle), single rank
+__global__ void k_slot_owner(int n_slots, const int* __restrict__ slot_gid, const int* __restrict__ tmap,
+                             int* __restrict__ slot_t) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n_slots) slot_t[s] = tmap[slot_gid[s]];
+}
+
+// half list: the entries of the full build-order list whose gid is larger than the particle's
+__global__ void k_list_half(int n_own, int n_pad, Geo g, const uint4* __restrict__ in, const int* __restrict__ ncount,
+                            const int* __restrict__ ocell_of, TileRows tr, const int* __restrict__ slot_gid,
+                            const int* __restrict__ gid, uint4* __restrict__ out, int* __restrict__ ncount_h) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_own) return;
+    int cx, cy, cz;
+    lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
+    const int tile = tile_of_cell(g, cx, cy, cz);
+    const int* rbeg = tr.begin + tile * kRowsMax;
+    const int* roff = tr.off + tile * (kRowsMax + 1);
+    const int gi = gid[t];
+    const int n = ncount[t];
+    const unsigned short* lst = reinterpret_cast<const unsigned short*>(in);
+    uint4* outb = out + t;
+    unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
+    int k = 0;
+    for (int e = 0; e < n; ++e) {
+        const int l = lst[((size_t)(e >> 3) * n_pad + t) * 8 + (e & 7)];
+        int r = 0;
+        while (l >= roff[r + 1]) ++r;
+        if (slot_gid[rbeg[r] + (l - roff[r])] <= gi) continue;
+        w0 = __funnelshift_r(w0, w1, 16);
+        w1 = __funnelshift_r(w1, w2, 16);
+        w2 = __funnelshift_r(w2, w3, 16);
+        w3 = __funnelshift_r(w3, (unsigned)l, 16);
+        if ((k & 7) == 7) {
+            *outb = make_uint4(w0, w1, w2, w3);
+            outb += n_pad;
+        }
+        ++k;
+    }
+    if (k & 7) {
+        const unsigned sen = (unsigned)roff[tile_geo(g, tile).R];
+        for (int e = k & 7; e < 8; ++e) {
+            w0 = __funnelshift_r(w0, w1, 16);
+            w1 = __funnelshift_r(w1, w2, 16);
+            w2 = __funnelshift_r(w2, w3, 16);
+            w3 = __funnelshift_r(w3, sen, 16);
+        }
+        *outb = make_uint4(w0, w1, w2, w3);
+    }
+    ncount_h[t] = k;
+}
+
+struct HalfArgs {
+    Geo g;
+    const double4* x;
+    const int* own_slot;
+    const uint4* nbr;       // half list, blocked like the full one
+    const int* ncount;
+    const int* obegin;
+    const int* tile_oc0;
+    const int* slot_t;
+    TileRows tr;
+    double* fx; double* fy; double* fz;
+    double* e;
+    double* pe_part;
+    int n_own, n_pad;
+    double rc2, c12, nc6, a12, na6, a0;
+};
+
+// F and e must be zero before the launch (they are accumulated from both ends of a pair).
+template <bool ENERGY>
+__global__ void __launch_bounds__(kForceThreads, 3) k_force_half(HalfArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double sh[kForceThreads / 32];
+    const int tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const TileGeo T = tile_geo(a.g, tile);
+    const int t0 = a.obegin[a.tile_oc0[tile]];
+    const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
+    const int rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
+    const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
+    const int total = __shfl_sync(0xffffffffu, ro, T.R);
+    double* sP = reinterpret_cast<double*>(smem);                 // packed {x, y, z}
+    int* sO = reinterpret_cast<int*>(sP + 3 * (total + 1));         // owner of each staged particle
+    for (int r = warp; r < T.R; r += kForceThreads / 32) {
+        const int b0 = __shfl_sync(0xffffffffu, rb, r);
+        const int o0 = __shfl_sync(0xffffffffu, ro, r);
+        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
+        for (int k = lane; k < len; k += 32) {
+            const double4 p = a.x[b0 + k];
+            sP[3 * (o0 + k)] = p.x;
+            sP[3 * (o0 + k) + 1] = p.y;
+            sP[3 * (o0 + k) + 2] = p.z;
+            sO[o0 + k] = a.slot_t[b0 + k];
+        }
+    }
+    if (threadIdx.x == 0) {
+        sP[3 * total] = 1e30;
+        sP[3 * total + 1] = 1e30;
+        sP[3 * total + 2] = 1e30;
+        sO[total] = -1;
+    }
+    __syncthreads();
+    double epart = 0.0;
+    for (int q = threadIdx.x; q < m; q += kForceThreads) {
+        const int t = t0 + q;
+        const double4 xi = a.x[a.own_slot[t]];
+        const int cnt = a.ncount[t];
+        double fx = 0.0, fy = 0.0, fz = 0.0, u = 0.0;
+        for (int b = 0; b < ((cnt + 7) >> 3); ++b) {
+            const uint4 blk = a.nbr[(size_t)b * a.n_pad + t];
+            const unsigned w4[4] = {blk.x, blk.y, blk.z, blk.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const unsigned l = (e & 1) ? (w4[e >> 1] >> 16) : (w4[e >> 1] & 0xffffu);
+                const double* pj = sP + 3 * l;
+                const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
+                const double r2 = r2_canon(dx, dy, dz);
+                if (r2 < a.rc2) {
+                    const double ir2 = rcp64(r2);
+                    const double ir4 = ir2 * ir2;
+                    const double ir6 = ir4 * ir2;
+                    const double ir8 = ir4 * ir4;
+                    const double gg = ir8 * fma(a.c12, ir6, a.nc6);
+                    const double gx = gg * dx, gy = gg * dy, gz = gg * dz;
+                    fx += gx; fy += gy; fz += gz;
+                    const int tj = sO[l];
+                    atomicAdd(a.fx + tj, -gx);
+                    atomicAdd(a.fy + tj, -gy);
+                    atomicAdd(a.fz + tj, -gz);
+                    if (ENERGY) {
+                        const double v = fma(fma(a.a12, ir6, a.na6), ir6, a.a0);
+                        u += v;
+                        atomicAdd(a.e + tj, 0.5 * v);
+                    }
+                }
+            }
+        }
+        atomicAdd(a.fx + t, fx);
+        atomicAdd(a.fy + t, fy);
+        atomicAdd(a.fz + t, fz);
+        if (ENERGY) {
+            atomicAdd(a.e + t, 0.5 * u);
+            epart += u;
+        }
+    }
+    if (ENERGY) {
+        const double pe = block_sum<kForceThreads>(epart, sh);
+        if (threadIdx.x == 0) a.pe_part[blockIdx.x] = pe;
+    }
+}
+
+// velocity Verlet on the completed F (Newton-3 path): [line 8: v += h F] [Andersen]
+// [KE sample] [line 6 of the next step: v += h F; x' = x + dt v, displacement check].
+// Grid = n_tiles blocks (grid-stride) so the KE partials line up with the PE partials.
+struct VvArgs {
+    int n_own;
+    const double4* x;
+    double4* x_next;
+    const int* own_slot;
+    double* vx; double* vy; double* vz;
+    const double* fx; const double* fy; const double* fz;
+    double* ke_part;
+    const double4* xbuild;
+    DevFlags* fl;
+    const int* gid;
+    double h, dt, half_m, nu_dt, sd;
+    unsigned long long seed;
+    long long step;
+};
+
+template <bool KICK2, bool ENERGY, bool KD, bool CHECK, bool THERMO>
+__global__ void __launch_bounds__(256) k_vv(VvArgs a) {
+    __shared__ double sh[8];
+    double ke = 0.0;
+    unsigned long long dbits = 0ull;
+    for (int t = blockIdx.x * 256 + threadIdx.x; t < a.n_own; t += gridDim.x * 256) {
+        double vx = a.vx[t], vy = a.vy[t], vz = a.vz[t];
+        const double fx = a.fx[t], fy = a.fy[t], fz = a.fz[t];
+        if (KICK2) {
+            vx = __dadd_rn(vx, __dmul_rn(a.h, fx));
+            vy = __dadd_rn(vy, __dmul_rn(a.h, fy));
+            vz = __dadd_rn(vz, __dmul_rn(a.h, fz));
+            if (THERMO) andersen(a.seed, a.step, a.nu_dt, a.sd, a.gid[t], vx, vy, vz);
+        }
+        if (ENERGY) ke += a.half_m * __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+        if (KD) {
+            vx = __dadd_rn(vx, __dmul_rn(a.h, fx));
+            vy = __dadd_rn(vy, __dmul_rn(a.h, fy));
+            vz = __dadd_rn(vz, __dmul_rn(a.h, fz));
+            const int si = a.own_slot[t];
+            const double4 xi = a.x[si];
+            const double4 xn = make_double4(__dadd_rn(xi.x, __dmul_rn(a.dt, vx)), __dadd_rn(xi.y, __dmul_rn(a.dt, vy)),
+                                            __dadd_rn(xi.z, __dmul_rn(a.dt, vz)), 0.0);
+            a.x_next[si] = xn;
+            if (CHECK) {
+                const double4 bb = a.xbuild[t];
+                const unsigned long long d2 =
+                    __double_as_longlong(r2_canon(xn.x - bb.x, xn.y - bb.y, xn.z - bb.z));
+                dbits = d2 > dbits ? d2 : dbits;
+            }
+        }
+        if (KICK2 || KD) {
+            a.vx[t] = vx; a.vy[t] = vy; a.vz[t] = vz;
+        }
+    }
+    if (CHECK) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_down_sync(0xffffffffu, dbits, o);
+            dbits = ob > dbits ? ob : dbits;
+        }
+        if ((threadIdx.x & 31) == 0 && dbits) atomicMax(&a.fl->maxdisp2, dbits);
+    }
+    if (ENERGY) {
+        const double k2 = block_sum<256>(ke, sh);
+        if (threadIdx.x == 0) a.ke_part[blockIdx.x] = k2;
+    }
+}
+}  // namespace ljmd

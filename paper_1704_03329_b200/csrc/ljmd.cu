@@ -94,6 +94,11 @@ struct ljmd_ctx {
     uint4* nbr8 = nullptr;            // 16-bit tile-local indices in blocks of 8: [K/8][n_pad]
     uint4* nbr8b = nullptr;           // the same, bank-aware order (what k_force reads)
     int bank_order = 1;               // 0: the force kernel walks the build order
+    bool newton3 = false;             // half list + reaction reductions (NEXT-1)
+    uint4* nbr8h = nullptr;           // half list (newton3), blocked like nbr8
+    int* ncount_h = nullptr;
+    int* slot_t = nullptr;            // slot -> owned index (newton3)
+    int* tmap = nullptr;              // gid -> owned index (newton3)
     int* ncount = nullptr;
     // ---- energies
     double* pe_part = nullptr;
@@ -384,6 +389,10 @@ ljmd_status alloc_owned(ljmd_ctx* c, int cap) {
     c->n_fblocks = c->n_tiles;   // one force CTA per tile
     TRY(dalloc(c, &c->pe_part, c->n_fblocks));
     TRY(dalloc(c, &c->ke_part, c->n_fblocks));
+    if (c->newton3) {
+        TRY(dalloc(c, &c->ncount_h, cap));
+        TRY(dalloc(c, &c->tmap, (size_t)c->n_global));
+    }
     return LJMD_OK;
 }
 
@@ -407,6 +416,7 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     }
     TRY(dalloc(c, &c->xf, cap));
     TRY(dalloc(c, &c->slot_gid, cap));
+    if (c->newton3) TRY(dalloc(c, &c->slot_t, cap));
     c->slot_cap = cap;
     return LJMD_OK;
 }
@@ -415,6 +425,7 @@ ljmd_status alloc_list(ljmd_ctx* c, int K) {
     c->K = K;
     TRY(dalloc(c, &c->nbr8, (size_t)(K / 8) * c->n_pad));
     TRY(dalloc(c, &c->nbr8b, (size_t)(K / 8) * c->n_pad));
+    if (c->newton3) TRY(dalloc(c, &c->nbr8h, (size_t)(K / 8) * c->n_pad));
     return LJMD_OK;
 }
 
@@ -533,11 +544,113 @@ ljmd_status set_force_attrs(ljmd_ctx* c) {
                           force_attr<false, KT, false>(), force_attr<false, DT, false>(),
                           force_attr<false, DT, true>()})
         if (r != cudaSuccess) e = r;
+    for (cudaError_t r : {cudaFuncSetAttribute(k_force_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kMaxStageSmem),
+                          cudaFuncSetAttribute(k_force_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               kMaxStageSmem)})
+        if (r != cudaSuccess) e = r;
     if (e != cudaSuccess) return set_err(c, LJMD_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return LJMD_OK;
 }
 
+template <bool K2, bool E, bool KD, bool C, bool TH>
+void vv_launch(ljmd_ctx* c, const VvArgs& v) {
+    k_vv<K2, E, KD, C, TH><<<c->n_tiles, 256, 0, c->stream>>>(v);
+}
+
+// Newton-3 path (NEXT-1): zero F (and e), half-list force with reaction reductions, then
+// the velocity-Verlet updates of `mode` on the completed F.
+ljmd_status launch_half(ljmd_ctx* c, bool energy, int mode, bool check, cudaEvent_t e0, cudaEvent_t e1) {
+    const size_t oc = c->own_cap;
+    if (e0) CK(cudaEventRecord(e0, c->stream));
+    CK(cudaMemsetAsync(c->F, 0, sizeof(double) * 3 * oc, c->stream));
+    if (energy) CK(cudaMemsetAsync(c->e, 0, sizeof(double) * oc, c->stream));
+    const double s2 = c->sigma * c->sigma, s6 = s2 * s2 * s2, s12 = s6 * s6;
+    HalfArgs h;
+    h.g = c->geo;
+    h.x = c->x[c->xc];
+    h.own_slot = c->own_slot;
+    h.nbr = c->nbr8h;
+    h.ncount = c->ncount_h;
+    h.obegin = c->obegin;
+    h.tile_oc0 = c->tile_oc0;
+    h.slot_t = c->slot_t;
+    h.tr = TileRows{c->tr_begin, c->tr_off};
+    h.fx = c->F;
+    h.fy = c->F + oc;
+    h.fz = c->F + 2 * oc;
+    h.e = c->e;
+    h.pe_part = c->pe_part;
+    h.n_own = c->n_own;
+    h.n_pad = c->n_pad;
+    h.rc2 = c->rc * c->rc;
+    h.c12 = 48.0 * c->eps * s12;
+    h.nc6 = -24.0 * c->eps * s6;
+    h.a12 = 4.0 * c->eps * s12;
+    h.na6 = -4.0 * c->eps * s6;
+    h.a0 = 4.0 * c->eps * c->opt.energy_shift;
+    const size_t smem = (kStageBytes + sizeof(int)) * (size_t)(c->max_staged + 1) + 8;
+    if (energy) k_force_half<true><<<c->n_tiles, kForceThreads, smem, c->stream>>>(h);
+    else k_force_half<false><<<c->n_tiles, kForceThreads, smem, c->stream>>>(h);
+    CKL();
+    if (e1) CK(cudaEventRecord(e1, c->stream));
+    double* v = c->v[c->oc_cur];
+    VvArgs a;
+    a.n_own = c->n_own;
+    a.x = c->x[c->xc];
+    a.x_next = c->x[c->xc ^ 1];
+    a.own_slot = c->own_slot;
+    a.vx = v;
+    a.vy = v + oc;
+    a.vz = v + 2 * oc;
+    a.fx = c->F;
+    a.fy = c->F + oc;
+    a.fz = c->F + 2 * oc;
+    a.ke_part = c->ke_part;
+    a.xbuild = c->xbuild;
+    a.fl = c->d_fl;
+    a.gid = c->gid[c->oc_cur];
+    a.h = 0.5 * c->dt / c->opt.mass;
+    a.dt = c->dt;
+    a.half_m = 0.5 * c->opt.mass;
+    a.nu_dt = c->nu_dt;
+    a.sd = c->thermo_sd;
+    a.seed = c->thermo_seed;
+    a.step = c->steps_done;
+    const bool th = c->nu_dt > 0.0;
+    if (mode == kStore) {
+        if (!energy) return LJMD_OK;
+        vv_launch<false, true, false, false, false>(c, a);
+    } else if (mode == kKick) {
+        if (energy) th ? vv_launch<true, true, false, false, true>(c, a) : vv_launch<true, true, false, false, false>(c, a);
+        else th ? vv_launch<true, false, false, false, true>(c, a) : vv_launch<true, false, false, false, false>(c, a);
+    } else if (check) {
+        if (energy) th ? vv_launch<true, true, true, true, true>(c, a) : vv_launch<true, true, true, true, false>(c, a);
+        else th ? vv_launch<true, false, true, true, true>(c, a) : vv_launch<true, false, true, true, false>(c, a);
+    } else {
+        if (energy) th ? vv_launch<true, true, true, false, true>(c, a) : vv_launch<true, true, true, false, false>(c, a);
+        else th ? vv_launch<true, false, true, false, true>(c, a) : vv_launch<true, false, true, false, false>(c, a);
+    }
+    CKL();
+    return LJMD_OK;
+}
+
 ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check) {
+    if (c->newton3) {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (c->opt.profile) {
+            size_t k = (size_t)c->force_launches * 2;
+            while (c->ev.size() < k + 2) {
+                cudaEvent_t ev;
+                CK(cudaEventCreate(&ev));
+                c->ev.push_back(ev);
+            }
+            e0 = c->ev[k];
+            e1 = c->ev[k + 1];
+            ++c->force_launches;
+        }
+        return launch_half(c, energy, mode, check, e0, e1);
+    }
     ForceArgs a = force_args(c);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->opt.profile) {
@@ -791,7 +904,17 @@ ljmd_status rebuild(ljmd_ctx* c) {
     }
     c->max_nbr = c->h_fl->max_nbr;
     c->total_nbr = c->h_fl->total_nbr;
-    if (c->bank_order) {
+    if (c->newton3) {
+        const int* g = c->gid[c->oc_cur];
+        k_cna_tmap<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, g, c->tmap);
+        CKL();
+        k_slot_owner<<<nblk(c->n_slots, 256), 256, 0, c->stream>>>(c->n_slots, c->slot_gid, c->tmap, c->slot_t);
+        CKL();
+        k_list_half<<<nblk(c->n_own, 128), 128, 0, c->stream>>>(c->n_own, c->n_pad, c->geo, c->nbr8, c->ncount,
+                                                                 c->ocell_of, TileRows{c->tr_begin, c->tr_off},
+                                                                 c->slot_gid, g, c->nbr8h, c->ncount_h);
+        CKL();
+    } else if (c->bank_order) {
         k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
             c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b);
         CKL();
@@ -938,6 +1061,7 @@ ljmd_status ljmd_default_options(ljmd_options* o) {
     o->profile = 0;
     o->list_order = 1;
     o->split_self = 0;
+    o->newton3 = 0;
     return LJMD_OK;
 }
 
@@ -992,6 +1116,11 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     c->dt = dt;
     c->rn = rc + o.delta;
     c->bank_order = o.list_order != 0;
+    c->newton3 = o.newton3 != 0;
+    if (c->newton3 && (o.nranks > 1 || o.split_self)) {
+        delete c;
+        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: newton3 needs nranks = 1 (no reverse halo)");
+    }
     auto fail = [&](ljmd_status s) {
         g_init_error = c->msg.empty() ? std::string("ljmd_init failed") : c->msg;
         ljmd_destroy(c);

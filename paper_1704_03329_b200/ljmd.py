@@ -45,7 +45,7 @@ class Options(ctypes.Structure):
                 ("rank", ctypes.c_int64), ("nranks", ctypes.c_int64),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int64), ("list_order", ctypes.c_int64),
-                ("split_self", ctypes.c_int64)]
+                ("split_self", ctypes.c_int64), ("newton3", ctypes.c_int64)]
 
 
 class Stats(ctypes.Structure):
