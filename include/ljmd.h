@@ -188,6 +188,49 @@ ljmd_status ljmd_set_thermostat(ljmd_ctx* c, double nu, double temperature, uint
  * LJMD_E_CAPACITY if a particle has more than 24 bonds. */
 ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t* trip, int64_t* nnb);
 
+/* ---------------------------------------------------------------------------------------
+ * PairLoop / ParticleLoop front end (the paper's DSL, Sec. 2.2-2.4; Tabs.
+ * tab:DSL_data, tab:DSL_looping, tab:DSL_access).  Single rank.
+ *
+ * Particle data ("ParticleDat"): ncomp components of dtype (0 double, 1 int32,
+ * 2 int64) per particle, zero-initialised, owned by the context, kept in the engine's
+ * particle order on the device (permuted at every rebuild); ljmd_dat_set/get copy
+ * [n][ncomp] host arrays in the caller's particle order.  global = 1 makes a ScalarArray
+ * (P:166): one row of ncomp values, shared by all particles.
+ * Engine data usable in loops (handles < 0): positions (the PositionDat, READ), velocities
+ * (any access), forces, global ids (int32), per-particle energies (READ).
+ *
+ * Loops (ljmd_loop_create): kind 0 = ParticleLoop, 1 = PairLoop.  `code` is the user's C
+ * kernel (Listing lst:simple-kernel style): for every argument k, labels[k] is visible as a
+ * struct with member i (pointer to particle i's components) and, in pair loops for READ /
+ * RW / WRITE data, member j (particle j's; reading R20); a ScalarArray is used as label[k]
+ * (and label += x for INC).  access[k]: LJMD_READ .. LJMD_INC_ZERO (Tab. tab:DSL_access;
+ * INC_ZERO zeroes first).  constants: "name=value" lines, substituted as #defines (the
+ * Constant class).  A PairLoop visits the ordered pairs (i, j) of the neighbour list with
+ * canonical r^2 < shell_cutoff^2, 0 < shell_cutoff <= rc (Listing lst:LJ-loop).  flags bit 0:
+ * allow FMA contraction (default: every operation rounded as written, like the oracle).
+ * The kernel is compiled with NVRTC for sm_100a at creation; a compile error returns
+ * LJMD_E_ARG with the compiler log in ljmd_last_error. */
+#define LJMD_DAT_POSITION (-1)
+#define LJMD_DAT_VELOCITY (-2)
+#define LJMD_DAT_FORCE (-3)
+#define LJMD_DAT_GID (-4)
+#define LJMD_DAT_ENERGY (-5)
+enum { LJMD_READ = 0, LJMD_WRITE = 1, LJMD_RW = 2, LJMD_INC = 3, LJMD_INC_ZERO = 4 };
+
+ljmd_status ljmd_dat_create(ljmd_ctx* c, int64_t ncomp, int64_t dtype, int64_t global, int64_t* handle);
+ljmd_status ljmd_dat_set(ljmd_ctx* c, int64_t handle, const void* host);
+ljmd_status ljmd_dat_get(ljmd_ctx* c, int64_t handle, void* host);
+ljmd_status ljmd_dat_free(ljmd_ctx* c, int64_t handle);
+ljmd_status ljmd_loop_create(ljmd_ctx* c, int64_t kind, const char* name, const char* code,
+                             const char* constants, double shell_cutoff, int64_t nargs,
+                             const char* const* labels, const int64_t* handles,
+                             const int64_t* access, int64_t flags, int64_t* loop);
+ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop);
+/* the generated CUDA source (len = its length; copied into out when cap > 0) */
+ljmd_status ljmd_loop_source(ljmd_ctx* c, int64_t loop, char* out, int64_t cap, int64_t* len);
+ljmd_status ljmd_loop_free(ljmd_ctx* c, int64_t loop);
+
 /* Multi-GPU plumbing: fill out128 with a fresh ncclUniqueId (NCCL is loaded with dlopen;
  * the copy torch already mapped is reused).  Rank 0 calls it and broadcasts the 128
  * bytes (e.g. with torch.distributed) into ljmd_options.nccl_id on every rank.  An id

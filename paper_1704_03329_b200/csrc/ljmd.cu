@@ -3,6 +3,7 @@
 // and the velocity-Verlet step loop (Alg. alg:VelocityVerlet).
 #include "../../include/ljmd.h"
 #include "kernels.cuh"
+#include "dsl.h"
 #include "transport.h"
 
 #include <cuda_runtime.h>
@@ -98,7 +99,13 @@ struct ljmd_ctx {
     uint4* nbr8h = nullptr;           // half list (newton3), blocked like nbr8
     int* ncount_h = nullptr;
     int* slot_t = nullptr;            // slot -> owned index (newton3)
-    int* tmap = nullptr;              // gid -> owned index (newton3)
+    int* tmap = nullptr;              // gid -> owned index (newton3, DSL)
+    // ---- DSL front end (dsl.cuh): particle data and compiled loops
+    std::vector<ljmd::DslDat> dats;
+    std::vector<ljmd::DslLoop*> loops;
+    bool dsl_on = false;
+    bool slot_t_valid = false;
+    int* tile_R = nullptr;
     int* ncount = nullptr;
     // ---- energies
     double* pe_part = nullptr;
@@ -145,6 +152,11 @@ struct ljmd_ctx {
     int* iota = nullptr;
     int* h_tot = nullptr;         // pinned: send/recv plane totals
 };
+
+ljmd_status dsl_before_sort(ljmd_ctx* c, const int* gid_old);
+ljmd_status dsl_after_sort(ljmd_ctx* c);
+ljmd_status dsl_to_gid_order(ljmd_ctx* c);
+void dsl_destroy(ljmd_ctx* c);
 
 namespace {
 
@@ -416,7 +428,10 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     }
     TRY(dalloc(c, &c->xf, cap));
     TRY(dalloc(c, &c->slot_gid, cap));
-    if (c->newton3) TRY(dalloc(c, &c->slot_t, cap));
+    if (c->newton3 || c->dsl_on) {
+        TRY(dalloc(c, &c->slot_t, cap));
+        c->slot_t_valid = false;
+    }
     c->slot_cap = cap;
     return LJMD_OK;
 }
@@ -860,6 +875,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     double* vn = c->v[on];
     const size_t oc = c->own_cap;
     double4* xn = c->x[c->xc ^ 1];
+    TRY(dsl_before_sort(c, gid_old));
     k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
         c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, gid_old, c->xw, vo, vo + oc, vo + 2 * oc,
         xn, c->xf, vn, vn + oc, vn + 2 * oc, c->gid[on], c->own_slot, c->ocell_of, c->slot_gid,
@@ -867,6 +883,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     CKL();
     c->oc_cur = on;
     c->xc ^= 1;
+    TRY(dsl_after_sort(c));
     if (c->split) {   // ghost planes: positions + gids of the neighbours' boundary planes
         k_plane_index<<<nblk((int64_t)2 * c->npc * 32, 256), 256, 0, c->stream>>>(c->geo, c->send_cnt,
                                                                                   c->send_off, c->ebegin,
@@ -986,6 +1003,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
         TRY(dalloc(c, &dg, (size_t)n));
         CK(cudaMemcpyAsync(dg, fg.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
     }
+    TRY(dsl_to_gid_order(c));   // particle data keeps its rows across a new state
     TRY(reset_flags(c));
     c->oc_cur = 0;
     c->xc = 0;
@@ -1421,6 +1439,9 @@ void ljmd_destroy(ljmd_ctx* c) {
                     c->tr_off, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    dsl_destroy(c);
+    for (void* p : {(void*)c->nbr8h, (void*)c->ncount_h, (void*)c->slot_t, (void*)c->tmap, (void*)c->tile_R})
+        if (p) cudaFree(p);
     void* ptrs2[] = {c->send_cnt, c->send_off, c->recv_cnt, c->recv_off, c->send_idx, c->send_buf, c->mig_send[0],
                      c->mig_send[1], c->mig_recv[0], c->mig_recv[1], c->mig_cnt, c->xs, c->vs, c->gs, c->iota};
     for (void* p : ptrs2)
@@ -1615,3 +1636,5 @@ extern "C" ljmd_status ljmd_measure_fp64_peak(int64_t device, double* tflops) {
     cudaFree(out);
     return LJMD_OK;
 }
+
+#include "dsl.cuh"

@@ -28,7 +28,9 @@ EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "
            "ljmd_get_positions", "ljmd_get_velocities", "ljmd_get_particle_energy", "ljmd_get_energy",
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
-           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna", "ljmd_set_thermostat")
+           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna", "ljmd_set_thermostat",
+           "ljmd_dat_create", "ljmd_dat_set", "ljmd_dat_get", "ljmd_dat_free", "ljmd_loop_create",
+           "ljmd_loop_execute", "ljmd_loop_source", "ljmd_loop_free")
 
 
 class LjmdError(RuntimeError):
@@ -101,6 +103,16 @@ def load(path: str = LIB_PATH):
         "ljmd_set_thermostat": ([vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64], ctypes.c_int),
         "ljmd_cna": ([vp, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), _I],
                      ctypes.c_int),
+        "ljmd_dat_create": ([vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I], ctypes.c_int),
+        "ljmd_dat_set": ([vp, ctypes.c_int64, ctypes.c_void_p], ctypes.c_int),
+        "ljmd_dat_get": ([vp, ctypes.c_int64, ctypes.c_void_p], ctypes.c_int),
+        "ljmd_dat_free": ([vp, ctypes.c_int64], ctypes.c_int),
+        "ljmd_loop_create": ([vp, ctypes.c_int64, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_double,
+                              ctypes.c_int64, ctypes.POINTER(ctypes.c_char_p), _I, _I, ctypes.c_int64, _I],
+                             ctypes.c_int),
+        "ljmd_loop_execute": ([vp, ctypes.c_int64], ctypes.c_int),
+        "ljmd_loop_source": ([vp, ctypes.c_int64, ctypes.c_char_p, ctypes.c_int64, _I], ctypes.c_int),
+        "ljmd_loop_free": ([vp, ctypes.c_int64], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
