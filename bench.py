@@ -32,6 +32,22 @@ sys.path.insert(0, ROOT)
 import ljinputs as li  # noqa: E402
 
 MD_PER_STEP = li.NS           # one rebuild cycle
+# Listing lst:LJ-kernel, a user kernel for the DSL timing below
+LJ_LISTING = """
+const double dr0 = r.i[0] - r.j[0];
+const double dr1 = r.i[1] - r.j[1];
+const double dr2 = r.i[2] - r.j[2];
+double dr_sq = dr0*dr0+dr1*dr1+dr2*dr2;
+const double r_m2 = sigma2/dr_sq;
+const double r_m4 = r_m2*r_m2;
+const double r_m6 = r_m4*r_m2;
+const double r_m8 = r_m4*r_m4;
+u[0]+= (dr_sq<rc_sq) ? CV*((r_m6-1.0)*r_m6+0.25) : 0.0;
+const double f_tmp=CF*(r_m6-0.5)*r_m8;
+F.i[0]+= (dr_sq<rc_sq)?f_tmp*dr0:0.0;
+F.i[1]+= (dr_sq<rc_sq)?f_tmp*dr1:0.0;
+F.i[2]+= (dr_sq<rc_sq)?f_tmp*dr2:0.0;
+"""
 METRIC = "LJ particle-timesteps/s"
 UNIT = "particle-timesteps/s"
 FLOPS_PER_CAND = 21.0         # Listing lst:LJ-kernel, force only (PAPER.md:983-1003)
@@ -176,6 +192,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-boa", action="store_true")
+    ap.add_argument("--no-dsl", action="store_true")
     ap.add_argument("--newton3", action="store_true",
                     help="NEXT-1 half-list force with reaction reductions (single GPU; slower)")
     args = ap.parse_args()
@@ -223,7 +240,10 @@ def main():
 
     pos, vel, box = cfg.build()
     n = len(pos)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the engine launches on it and every CUDA event below is
+    # recorded on it (torch's default stream has handle 0, which the ABI reads as "create one")
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     check = 1 if (args.check or cfg.rebuild_check) else 0
     opts = ljmd.default_options(device=local, stream=stream.cuda_stream, profile=1,
                                 rebuild_check=check, rank=rank, nranks=world,
@@ -322,6 +342,31 @@ def main():
         boa = {"ell": 6, "rcut": 1.5, "ms_per_call_incl_readback": b0.elapsed_time(b1) / nb,
                "mean_Q6": float(np.mean(Qb))}
 
+    # §8(f) NEXT-3: the paper's LJ kernel (Listing lst:LJ-kernel) as a user PairLoop compiled
+    # at run time (NVRTC), timed on the same state against the hand-written force kernel
+    dsl_info = None
+    if not args.no_dsl and world == 1:
+        from paper_1704_03329_b200 import dsl
+        consts = (dsl.Constant("sigma2", 1.0), dsl.Constant("rc_sq", li.RC * li.RC), dsl.Constant("CV", 4.0),
+                  dsl.Constant("CF", 48.0))
+        Fd, ud = dsl.ParticleDat(ctx, ncomp=3), dsl.ScalarArray(ctx)
+        dsl_info = {"kernel": "Listing lst:LJ-kernel as a PairLoop (shell_cutoff = rc), NVRTC sm_100a",
+                    "handwritten_force_ms": f_ms}
+        for fmad in (False, True):
+            loop = dsl.PairLoop(dsl.Kernel("lj", LJ_LISTING, consts),
+                                {"r": dsl.PositionDat(ctx)(dsl.READ), "F": Fd(dsl.INC_ZERO), "u": ud(dsl.INC_ZERO)},
+                                shell_cutoff=li.RC, fmad=fmad)
+            loop.execute()
+            torch.cuda.synchronize()
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            for _ in range(5):
+                loop.execute()
+            d1.record(stream)
+            torch.cuda.synchronize()
+            dsl_info["ms_per_execute_fmad" if fmad else "ms_per_execute_exact"] = d0.elapsed_time(d1) / 5
+            loop.free()
+
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         cores, model = cpu_info()
@@ -357,6 +402,7 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu,
         "boa": boa,
+        "dsl": dsl_info,
         "clocks": clocks,
     }
     if rank == 0:

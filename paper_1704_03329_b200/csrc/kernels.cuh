@@ -1130,6 +1130,15 @@ __global__ void k_finalize_energy(const double* __restrict__ pe_part, const doub
     }
 }
 
+// readback: owned-order rows of `width` doubles into caller (gid) order
+__global__ void k_rows_to_gid(int n, int width, const int* __restrict__ gid, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+    const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long long)n * width) return;
+    const int t = (int)(idx / width), k = (int)(idx % width);
+    dst[(size_t)gid[t] * width + k] = src[idx];
+}
+
 // readback helpers: compact owned-space copies
 __global__ void k_gather_pos(int n_own, const double4* __restrict__ x, const int* __restrict__ own_slot,
                              double* __restrict__ out) {

@@ -106,6 +106,9 @@ struct ljmd_ctx {
     bool dsl_on = false;
     bool slot_t_valid = false;
     int* tile_R = nullptr;
+    double* ld_pos = nullptr;         // load_state staging
+    double* ld_vel = nullptr;
+    int* ld_gid = nullptr;
     int* ncount = nullptr;
     // ---- energies
     double* pe_part = nullptr;
@@ -992,15 +995,20 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
         pos = fp.data();
         vel = fv.data();
     }
-    double* dpos = nullptr;
-    double* dvel = nullptr;
+    // persistent staging (allocated once: a per-call cudaMalloc/cudaFree would serialise the
+    // device and dominate set_state)
+    if (!c->ld_pos) {
+        TRY(dalloc(c, &c->ld_pos, (size_t)3 * c->n_global));
+        TRY(dalloc(c, &c->ld_vel, (size_t)3 * c->n_global));
+        if (c->split) TRY(dalloc(c, &c->ld_gid, (size_t)c->n_global));
+    }
+    double* dpos = c->ld_pos;
+    double* dvel = c->ld_vel;
     int* dg = nullptr;
-    TRY(dalloc(c, &dpos, (size_t)3 * n));
-    TRY(dalloc(c, &dvel, (size_t)3 * n));
     CK(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dvel, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
     if (c->split) {
-        TRY(dalloc(c, &dg, (size_t)n));
+        dg = c->ld_gid;
         CK(cudaMemcpyAsync(dg, fg.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
     }
     TRY(dsl_to_gid_order(c));   // particle data keeps its rows across a new state
@@ -1013,9 +1021,6 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
                                                     c->gid[0], c->own_slot, dg, c->d_fl);
     CKL();
     TRY(sync_flags(c));
-    cudaFree(dpos);
-    cudaFree(dvel);
-    if (dg) cudaFree(dg);
     if (c->h_fl->nonfinite_gid != INT_MAX)
         return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
                        c->h_fl->nonfinite_gid);
@@ -1044,6 +1049,17 @@ ljmd_status check_ctx(ljmd_ctx* c) {
 
 // host scatter of a compact owned-space [n_own][3] (or [n_own]) array into caller rows
 ljmd_status readback(ljmd_ctx* c, const double* dsrc, int width, double* out) {
+    if (!c->split && c->ld_pos && c->n_own == c->n_global) {
+        // single rank: scatter into caller order on the device, one D2H copy into `out`
+        k_rows_to_gid<<<nblk((int64_t)c->n_own * width, 256), 256, 0, c->stream>>>(c->n_own, width,
+                                                                                    c->gid[c->oc_cur], dsrc,
+                                                                                    c->ld_pos);
+        CKL();
+        CK(cudaMemcpyAsync(out, c->ld_pos, sizeof(double) * width * (size_t)c->n_own, cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return LJMD_OK;
+    }
     std::vector<double> tmp((size_t)width * c->n_own);
     std::vector<int> g(c->n_own);
     CK(cudaMemcpyAsync(tmp.data(), dsrc, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, c->stream));
@@ -1309,6 +1325,7 @@ ljmd_status ljmd_get_positions(ljmd_ctx* c, double* out, int64_t wrapped) {
     if (!out) return LJMD_E_ARG;
     k_gather_pos<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->x[c->xc], c->own_slot, c->d_stage);
     CKL();
+    if (!wrapped) return readback(c, c->d_stage, 3, out);
     std::vector<double> tmp((size_t)3 * c->n_own);
     std::vector<int> g(c->n_own);
     CK(cudaMemcpyAsync(tmp.data(), c->d_stage, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, c->stream));
@@ -1440,7 +1457,8 @@ void ljmd_destroy(ljmd_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     dsl_destroy(c);
-    for (void* p : {(void*)c->nbr8h, (void*)c->ncount_h, (void*)c->slot_t, (void*)c->tmap, (void*)c->tile_R})
+    for (void* p : {(void*)c->nbr8h, (void*)c->ncount_h, (void*)c->slot_t, (void*)c->tmap, (void*)c->tile_R,
+                    (void*)c->ld_pos, (void*)c->ld_vel, (void*)c->ld_gid})
         if (p) cudaFree(p);
     void* ptrs2[] = {c->send_cnt, c->send_off, c->recv_cnt, c->recv_off, c->send_idx, c->send_buf, c->mig_send[0],
                      c->mig_send[1], c->mig_recv[0], c->mig_recv[1], c->mig_cnt, c->xs, c->vs, c->gs, c->iota};
