@@ -68,11 +68,13 @@ class Stats(ctypes.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libljmd.so (raises if it has not been built: no fallback path exists)."""
+def load(path: str = None):
+    """Load libljmd.so (raises if it has not been built: no fallback path exists).
+    LJMD_LIB overrides the path (A/B builds of the same sources)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("LJMD_LIB", LIB_PATH)
     if not os.path.exists(path):
         raise RuntimeError(f"libljmd.so not built at {path}; run __graft_entry__.build()")
     lib = ctypes.CDLL(path)
