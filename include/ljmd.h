@@ -190,7 +190,13 @@ ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t* trip, int6
 
 /* ---------------------------------------------------------------------------------------
  * PairLoop / ParticleLoop front end (the paper's DSL, Sec. 2.2-2.4; Tabs.
- * tab:DSL_data, tab:DSL_looping, tab:DSL_access).  Single rank.
+ * tab:DSL_data, tab:DSL_looping, tab:DSL_access).
+ * With nranks > 1 particle data migrates with its particles at every rebuild, data read on
+ * the j side of a pair loop is exchanged into the halo before the loop (only for READ / RW /
+ * WRITE arguments: the access descriptors decide), and ScalarArray increments
+ * are all-reduced over the ranks.  ljmd_dat_set takes the full [n][ncomp] array on every
+ * rank; ljmd_dat_get writes the rows of this rank's particles; ljmd_set_state on several
+ * ranks zeroes particle data (its rows may now belong to another rank).
  *
  * Particle data ("ParticleDat"): ncomp components of dtype (0 double, 1 int32,
  * 2 int64) per particle, zero-initialised, owned by the context, kept in the engine's

@@ -5,7 +5,8 @@
 // target is sm_100a: the template is the engine's tile-staged neighbour-list loop (one CTA per
 // tile, positions of the tile's halo rows in shared memory, thread per particle over its
 // Verlet list), compiled at run time with NVRTC to a cubin and loaded with
-// cudaLibraryLoadData.  Single rank (the j-side of a dat is read through slot -> owner).
+// cudaLibraryLoadData.  One rank: the j side of a dat is read through slot -> owner; several
+// ranks: data migrates with its particles and j-side data is brought into the halo first.
 #include <dlfcn.h>
 #include <nvrtc.h>
 
@@ -54,6 +55,82 @@ __global__ void k_dsl_fin(const T* __restrict__ part, int nb, int nc, T* __restr
 __global__ void k_tile_R(int n_tiles, Geo g, int* __restrict__ out) {
     const int tile = blockIdx.x * blockDim.x + threadIdx.x;
     if (tile < n_tiles) out[tile] = tile_geo(g, tile).R;
+}
+
+// ---- several ranks: particle data travels with its particle, and the data a
+// pair loop reads on the j side is brought into the halo
+// migration: compact rows of the stayers (in the engine's compaction order), rows of leavers
+__global__ void k_dat_gather_idx(int n, int words, const int* __restrict__ idx, const unsigned* __restrict__ src,
+                                 unsigned* __restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * words) return;
+    const int k = (int)(i / words), w = (int)(i % words);
+    dst[i] = src[(size_t)idx[k] * words + w];
+}
+
+__global__ void k_dat_gather_mig(int n, int words, const MigRec* __restrict__ rec, const unsigned* __restrict__ src,
+                                 unsigned* __restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * words) return;
+    const int k = (int)(i / words), w = (int)(i % words);
+    dst[i] = src[(size_t)rec[k].pad * words + w];
+}
+
+// slot-space copy of argument data: owned rows (any stride) -> their slots
+template <class T>
+__global__ void k_elems_to_slots(int n, int nc, const int* __restrict__ own_slot, const T* __restrict__ src,
+                                 long long st, long long sc, T* __restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * nc) return;
+    const int t = (int)(i / nc), c = (int)(i % nc);
+    dst[(size_t)own_slot[t] * nc + c] = src[(size_t)t * st + (size_t)c * sc];
+}
+
+__global__ void k_slot_pack_words(int n, int words, const int* __restrict__ idx, const unsigned* __restrict__ src,
+                                  unsigned* __restrict__ dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)n * words) return;
+    const int k = (int)(i / words), w = (int)(i % words);
+    dst[i] = src[(size_t)idx[k] * words + w];
+}
+
+// ghost cells of the slot-space copy: rows of the source cell (local) or of the received
+// plane cell, as k_ghost_refresh does for positions (no periodic shift for data)
+__global__ void k_slot_ghosts_words(GhostCells gc, const int* __restrict__ ebegin, const int* __restrict__ ecount,
+                                    const int* __restrict__ recv_cnt, const int* __restrict__ recv_off, int n_slots,
+                                    int words, unsigned* __restrict__ d) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= gc.n) return;
+    const int dst = gc.dst[warp], s = gc.src[warp];
+    const int db = ebegin[dst];
+    int sb, m;
+    if (s >= 0) {
+        sb = ebegin[s];
+        m = ecount[s];
+    } else {
+        sb = n_slots + recv_off[-s - 1];
+        m = recv_cnt[-s - 1];
+    }
+    for (int i = lane; i < m * words; i += 32) d[(size_t)db * words + i] = d[(size_t)sb * words + i];
+}
+
+// ScalarArray INC: this launch's sums as doubles (exact for integers below 2^53), all-reduced
+// over the ranks, then applied
+template <class T>
+__global__ void k_dsl_fin_delta(const T* __restrict__ part, int nb, int nc, double* __restrict__ delta) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    T s = 0;
+    for (int b = 0; b < nb; ++b) s += part[(size_t)b * nc + c];
+    delta[c] = (double)s;
+}
+
+template <class T>
+__global__ void k_dsl_apply(const double* __restrict__ delta, int nc, T* __restrict__ out, int zero) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    out[c] = zero ? (T)delta[c] : (T)(out[c] + (T)delta[c]);
 }
 }  // namespace ljmd
 
@@ -142,27 +219,31 @@ template <typename T> __device__ T dsl_block_sum(T v) {
 // (positions, and the owner index for j-side dat reads), thread per owned particle i over its
 // Verlet list, kernel body run for every entry with canonical r^2 < shell_cutoff^2.
 std::string generate(const DslLoop& L, const std::string& code, const std::string& consts) {
+    // every name the template declares starts with ljmd_ so it cannot shadow a user label
     std::ostringstream s;
     s << kDslPrelude << "\n" << consts << "\n";
     const bool pair = L.kind == 1;
-    s << "extern \"C\" __global__ void __launch_bounds__(" << L.block << ") " << L.name << "(DslParams p) {\n";
+    s << "extern \"C\" __global__ void __launch_bounds__(" << L.block << ") " << L.name << "(DslParams ljmd_p) {\n";
     if (pair) {
-        s << "  extern __shared__ double dsl_smem[];\n"
-             "  const int tile = blockIdx.x;\n"
-             "  const int t0 = p.obegin[p.tile_oc0[tile]];\n"
-             "  const int m = p.obegin[p.tile_oc0[tile + 1]] - t0;\n"
-             "  const int R = p.tile_R[tile];\n"
-             "  const int* rb = p.tr_begin + tile * p.rows_max;\n"
-             "  const int* ro = p.tr_off + tile * (p.rows_max + 1);\n"
-             "  const int total = ro[R];\n"
-             "  double* sP = dsl_smem;\n"
-             "  int* sO = (int*)(sP + 3 * total);\n"
-             "  for (int r = 0; r < R; ++r) {\n"
-             "    const int b0 = rb[r], o0 = ro[r], len = ro[r + 1] - o0;\n"
-             "    for (int k = threadIdx.x; k < len; k += blockDim.x) {\n"
-             "      const double* q = p.x + 4 * (long long)(b0 + k);\n"
-             "      sP[3 * (o0 + k)] = q[0]; sP[3 * (o0 + k) + 1] = q[1]; sP[3 * (o0 + k) + 2] = q[2];\n"
-             "      sO[o0 + k] = p.slot_t[b0 + k];\n"
+        s << "  extern __shared__ double ljmd_smem[];\n"
+             "  const int ljmd_tile = blockIdx.x;\n"
+             "  const int ljmd_t0 = ljmd_p.obegin[ljmd_p.tile_oc0[ljmd_tile]];\n"
+             "  const int ljmd_m = ljmd_p.obegin[ljmd_p.tile_oc0[ljmd_tile + 1]] - ljmd_t0;\n"
+             "  const int ljmd_R = ljmd_p.tile_R[ljmd_tile];\n"
+             "  const int* ljmd_rb = ljmd_p.tr_begin + ljmd_tile * ljmd_p.rows_max;\n"
+             "  const int* ljmd_ro = ljmd_p.tr_off + ljmd_tile * (ljmd_p.rows_max + 1);\n"
+             "  const int ljmd_total = ljmd_ro[ljmd_R];\n"
+             "  double* ljmd_sP = ljmd_smem;\n"
+             "  int* ljmd_sO = (int*)(ljmd_sP + 3 * ljmd_total);\n"
+             "  for (int ljmd_r = 0; ljmd_r < ljmd_R; ++ljmd_r) {\n"
+             "    const int ljmd_b0 = ljmd_rb[ljmd_r], ljmd_o0 = ljmd_ro[ljmd_r];\n"
+             "    const int ljmd_len = ljmd_ro[ljmd_r + 1] - ljmd_o0;\n"
+             "    for (int ljmd_k = threadIdx.x; ljmd_k < ljmd_len; ljmd_k += blockDim.x) {\n"
+             "      const double* ljmd_q = ljmd_p.x + 4 * (long long)(ljmd_b0 + ljmd_k);\n"
+             "      ljmd_sP[3 * (ljmd_o0 + ljmd_k)] = ljmd_q[0];\n"
+             "      ljmd_sP[3 * (ljmd_o0 + ljmd_k) + 1] = ljmd_q[1];\n"
+             "      ljmd_sP[3 * (ljmd_o0 + ljmd_k) + 2] = ljmd_q[2];\n"
+             "      ljmd_sO[ljmd_o0 + ljmd_k] = ljmd_p.slot_t ? ljmd_p.slot_t[ljmd_b0 + ljmd_k] : (ljmd_b0 + ljmd_k);\n"
              "    }\n"
              "  }\n"
              "  __syncthreads();\n";
@@ -174,40 +255,45 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
             s << "  DslAcc<" << ctype_of(a.dtype) << ", " << a.ncomp << "> " << a.label << ";\n";
     }
     if (pair)
-        s << "  for (int q = threadIdx.x; q < m; q += blockDim.x) {\n    const int t = t0 + q;\n";
+        s << "  for (int ljmd_qq = threadIdx.x; ljmd_qq < ljmd_m; ljmd_qq += blockDim.x) {\n"
+             "    const int ljmd_t = ljmd_t0 + ljmd_qq;\n";
     else
-        s << "  {\n    const int t = blockIdx.x * blockDim.x + threadIdx.x;\n    if (t < p.n_own) {\n";
-    s << "    const double* xi_p = p.x + 4 * (long long)p.own_slot[t];\n"
-         "    const double xi[3] = {xi_p[0], xi_p[1], xi_p[2]};\n";
+        s << "  {\n    const int ljmd_t = blockIdx.x * blockDim.x + threadIdx.x;\n    if (ljmd_t < ljmd_p.n_own) {\n";
+    s << "    const double* ljmd_xip = ljmd_p.x + 4 * (long long)ljmd_p.own_slot[ljmd_t];\n"
+         "    const double ljmd_xi[3] = {ljmd_xip[0], ljmd_xip[1], ljmd_xip[2]};\n";
+    const std::string P = "ljmd_p.";
+    auto K = [](size_t k) { return std::to_string(k); };
     // i-side copies
     for (size_t k = 0; k < L.args.size(); ++k) {
         const DslArg& a = L.args[k];
         if (a.handle == LJMD_DAT_POSITION || a.global || !a.local) continue;
         const char* T = ctype_of(a.dtype);
-        s << "    " << T << " " << a.label << "_li[" << a.ncomp << "];\n";
+        s << "    " << T << " ljmd_" << a.label << "_i[" << a.ncomp << "];\n";
         if (a.access == LJMD_INC_ZERO) {
-            s << "    for (int c = 0; c < " << a.ncomp << "; ++c) " << a.label << "_li[c] = (" << T << ")0;\n";
+            s << "    for (int ljmd_c = 0; ljmd_c < " << a.ncomp << "; ++ljmd_c) ljmd_" << a.label << "_i[ljmd_c] = ("
+              << T << ")0;\n";
         } else {
-            s << "    for (int c = 0; c < " << a.ncomp << "; ++c) " << a.label << "_li[c] = ((const " << T
-              << "*)p.ptr[" << k << "])[(long long)t * p.st[" << k << "] + (long long)c * p.sc[" << k << "]];\n";
+            s << "    for (int ljmd_c = 0; ljmd_c < " << a.ncomp << "; ++ljmd_c) ljmd_" << a.label
+              << "_i[ljmd_c] = ((const " << T << "*)" << P << "ptr[" << K(k) << "])[(long long)ljmd_t * " << P
+              << "st[" << K(k) << "] + (long long)ljmd_c * " << P << "sc[" << K(k) << "]];\n";
         }
     }
     std::ostringstream bind;   // the labels seen by the user code
     for (size_t k = 0; k < L.args.size(); ++k) {
         const DslArg& a = L.args[k];
-        const char* T = ctype_of(a.dtype);
+        const std::string T = ctype_of(a.dtype);
         const std::string q = a.access == LJMD_READ ? "const " : "";
         if (a.global) {
             if (a.access == LJMD_READ)
-                bind << "      const " << T << "* " << a.label << " = (const " << T << "*)p.ptr[" << k << "];\n";
+                bind << "      const " << T << "* " << a.label << " = (const " << T << "*)" << P << "ptr[" << K(k)
+                     << "];\n";
             continue;
         }
         const bool jside = pair && (a.access == LJMD_READ || a.access == LJMD_RW || a.access == LJMD_WRITE);
         std::string ival;
-        if (a.handle == LJMD_DAT_POSITION) ival = "xi";
-        else if (a.local) ival = a.label + "_li";
-        else ival = "((" + std::string(T) + "*)p.ptr[" + std::to_string(k) + "]) + (long long)t * p.st[" +
-                    std::to_string(k) + "]";
+        if (a.handle == LJMD_DAT_POSITION) ival = "ljmd_xi";
+        else if (a.local) ival = "ljmd_" + a.label + "_i";
+        else ival = "((" + T + "*)" + P + "ptr[" + K(k) + "]) + (long long)ljmd_t * " + P + "st[" + K(k) + "]";
         if (!jside) {
             bind << "      struct { " << q << T << "* i; } " << a.label << " = { " << ival << " };\n";
             continue;
@@ -215,29 +301,30 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
         std::string jt, jval;
         if (a.handle == LJMD_DAT_POSITION) {
             jt = "const double*";
-            jval = "sP + 3 * l";
+            jval = "ljmd_sP + 3 * ljmd_l";
         } else if (a.ncomp == 1 || a.handle >= 0) {   // AoS rows (user dats) or one component
-            jt = "const " + std::string(T) + "*";
-            jval = "((const " + std::string(T) + "*)p.ptr[" + std::to_string(k) + "]) + (long long)tj * p.st[" +
-                   std::to_string(k) + "]";
+            jt = "const " + T + "*";
+            jval = "((const " + T + "*)" + P + "jptr[" + K(k) + "]) + (long long)ljmd_tj * " + P + "jst[" + K(k) + "]";
         } else {                                      // engine SoA (velocities, forces)
-            jt = "DslStrided<" + std::string(T) + ">";
-            jval = "DslStrided<" + std::string(T) + ">{((const " + std::string(T) + "*)p.ptr[" + std::to_string(k) +
-                   "]) + tj, p.sc[" + std::to_string(k) + "]}";
+            jt = "DslStrided<" + T + ">";
+            jval = "DslStrided<" + T + ">{((const " + T + "*)" + P + "jptr[" + K(k) + "]) + ljmd_tj * " + P + "jst[" +
+                   K(k) + "], " + P + "jsc[" + K(k) + "]}";
         }
         bind << "      struct { " << q << T << "* i; " << jt << " j; } " << a.label << " = { " << ival << ", " << jval
              << " };\n";
     }
     if (pair) {
-        s << "    const int cnt = p.ncount[t];\n"
-             "    for (int kk = 0; kk < cnt; ++kk) {\n"
-             "      const int l = p.nbr[((long long)(kk >> 3) * p.n_pad + t) * 8 + (kk & 7)];\n"
-             "      const double* xj = sP + 3 * l;\n"
-             "      const double dx = xi[0] - xj[0], dy = xi[1] - xj[1], dz = xi[2] - xj[2];\n"
-             "      const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));\n"
-             "      if (!(r2 < p.cut2)) continue;\n"
-             "      const int tj = sO[l];\n"
-             "      (void)tj;\n"
+        s << "    const int ljmd_cnt = ljmd_p.ncount[ljmd_t];\n"
+             "    for (int ljmd_kk = 0; ljmd_kk < ljmd_cnt; ++ljmd_kk) {\n"
+             "      const int ljmd_l = ljmd_p.nbr[((long long)(ljmd_kk >> 3) * ljmd_p.n_pad + ljmd_t) * 8 + (ljmd_kk & 7)];\n"
+             "      const double* ljmd_xj = ljmd_sP + 3 * ljmd_l;\n"
+             "      const double ljmd_dx = ljmd_xi[0] - ljmd_xj[0], ljmd_dy = ljmd_xi[1] - ljmd_xj[1];\n"
+             "      const double ljmd_dz = ljmd_xi[2] - ljmd_xj[2];\n"
+             "      const double ljmd_r2 = __dadd_rn(__dadd_rn(__dmul_rn(ljmd_dx, ljmd_dx), __dmul_rn(ljmd_dy, ljmd_dy)),\n"
+             "                                       __dmul_rn(ljmd_dz, ljmd_dz));\n"
+             "      if (!(ljmd_r2 < ljmd_p.cut2)) continue;\n"
+             "      const int ljmd_tj = ljmd_sO[ljmd_l];\n"
+             "      (void)ljmd_tj;\n"
           << bind.str() << "      {\n" << code << "\n      }\n    }\n";
     } else {
         s << "    {\n" << bind.str() << "      {\n" << code << "\n      }\n    }\n";
@@ -246,8 +333,9 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
     for (size_t k = 0; k < L.args.size(); ++k) {
         const DslArg& a = L.args[k];
         if (a.handle == LJMD_DAT_POSITION || a.global || !a.local || a.access == LJMD_READ) continue;
-        s << "    for (int c = 0; c < " << a.ncomp << "; ++c) ((" << ctype_of(a.dtype) << "*)p.ptr[" << k
-          << "])[(long long)t * p.st[" << k << "] + (long long)c * p.sc[" << k << "]] = " << a.label << "_li[c];\n";
+        s << "    for (int ljmd_c = 0; ljmd_c < " << a.ncomp << "; ++ljmd_c) ((" << ctype_of(a.dtype) << "*)" << P
+          << "ptr[" << K(k) << "])[(long long)ljmd_t * " << P << "st[" << K(k) << "] + (long long)ljmd_c * " << P
+          << "sc[" << K(k) << "]] = ljmd_" << a.label << "_i[ljmd_c];\n";
     }
     s << (pair ? "  }\n" : "    }\n  }\n");
     // ScalarArray INC: deterministic block sums into per-block partials
@@ -255,10 +343,10 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
         const DslArg& a = L.args[k];
         if (!a.global || a.access == LJMD_READ) continue;
         const char* T = ctype_of(a.dtype);
-        s << "  for (int c = 0; c < " << a.ncomp << "; ++c) {\n"
-          << "    const " << T << " v = dsl_block_sum<" << T << ">(" << a.label << ".v[c]);\n"
-          << "    if (threadIdx.x == 0) ((" << T << "*)p.part[" << k << "])[(long long)blockIdx.x * " << a.ncomp
-          << " + c] = v;\n  }\n";
+        s << "  for (int ljmd_c = 0; ljmd_c < " << a.ncomp << "; ++ljmd_c) {\n"
+          << "    const " << T << " ljmd_v = dsl_block_sum<" << T << ">(" << a.label << ".v[ljmd_c]);\n"
+          << "    if (threadIdx.x == 0) ((" << T << "*)" << P << "part[" << K(k) << "])[(long long)blockIdx.x * "
+          << a.ncomp << " + ljmd_c] = ljmd_v;\n  }\n";
     }
     s << "}\n";
     return s.str();
@@ -266,8 +354,7 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
 
 ljmd_status dsl_enable(ljmd_ctx* c) {
     if (c->dsl_on) return LJMD_OK;
-    if (c->split) return set_err(c, LJMD_E_ARG, "the DSL front end runs on a single rank (nranks = 1)");
-    if (!c->slot_t) TRY(dalloc(c, &c->slot_t, (size_t)c->slot_cap));
+    if (!c->split && !c->slot_t) TRY(dalloc(c, &c->slot_t, (size_t)c->slot_cap));
     if (!c->tmap) TRY(dalloc(c, &c->tmap, (size_t)c->n_global));
     TRY(dalloc(c, &c->tile_R, (size_t)c->n_tiles));
     k_tile_R<<<nblk(c->n_tiles, 256), 256, 0, c->stream>>>(c->n_tiles, c->geo, c->tile_R);
@@ -278,7 +365,7 @@ ljmd_status dsl_enable(ljmd_ctx* c) {
 }
 
 ljmd_status dsl_slot_owner(ljmd_ctx* c) {
-    if (c->slot_t_valid) return LJMD_OK;
+    if (c->slot_t_valid || c->split) return LJMD_OK;
     k_cna_tmap<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->gid[c->oc_cur], c->tmap);
     CKL();
     k_slot_owner<<<nblk(c->n_slots, 256), 256, 0, c->stream>>>(c->n_slots, c->slot_gid, c->tmap, c->slot_t);
@@ -317,10 +404,46 @@ ljmd_status dsl_to_gid_order(ljmd_ctx* c) {
     if (!c->dsl_on || c->n_own == 0) return LJMD_OK;
     for (DslDat& d : c->dats) {
         if (!d.alive || d.global) continue;
+        if (c->split) {   // a new state may give this slab particles whose rows live elsewhere
+            CK(cudaMemsetAsync(d.d, 0, (size_t)c->own_cap * d.ncomp * d.esize, c->stream));
+            continue;
+        }
         const int words = d.ncomp * d.esize / 4;
         k_dat_to_gid<<<nblk((int64_t)c->n_own * words, 256), 256, 0, c->stream>>>(
             c->n_own, words, c->gid[c->oc_cur], (const unsigned*)d.d, (unsigned*)d.tmp);
         CKL();
+        std::swap(d.d, d.tmp);
+    }
+    return LJMD_OK;
+}
+
+// migration ("the State object will automatically move all data owned by the
+// particle to the receiving processor"): rows follow the engine's compaction of (x, v, gid)
+ljmd_status dsl_migrate(ljmd_ctx* c, int stay, int out_lo, int out_hi, int in_lo, int in_hi) {
+    if (!c->dsl_on) return LJMD_OK;
+    for (DslDat& d : c->dats) {
+        if (!d.alive || d.global) continue;
+        const size_t row = (size_t)d.ncomp * d.esize;
+        const int words = (int)(row / 4);
+        if ((size_t)c->mig_cap > d.msend_cap) {
+            for (int b = 0; b < 2; ++b) TRY(dalloc(c, (char**)&d.msend[b], row * (size_t)c->mig_cap));
+            d.msend_cap = (size_t)c->mig_cap;
+        }
+        if (stay) {
+            k_dat_gather_idx<<<nblk((int64_t)stay * words, 256), 256, 0, c->stream>>>(
+                stay, words, c->stay_t, (const unsigned*)d.d, (unsigned*)d.tmp);
+            CKL();
+        }
+        const int outs[2] = {out_lo, out_hi};
+        for (int b = 0; b < 2; ++b) {
+            if (!outs[b]) continue;
+            k_dat_gather_mig<<<nblk((int64_t)outs[b] * words, 256), 256, 0, c->stream>>>(
+                outs[b], words, c->mig_send[b], (const unsigned*)d.d, (unsigned*)d.msend[b]);
+            CKL();
+        }
+        char* dst = (char*)d.tmp;
+        TRY(exchange(c, d.msend[1], row * out_hi, d.msend[0], row * out_lo, dst + row * stay, row * in_lo,
+                     dst + row * (stay + in_lo), row * in_hi));
         std::swap(d.d, d.tmp);
     }
     return LJMD_OK;
@@ -391,8 +514,19 @@ extern "C" ljmd_status ljmd_dat_get(ljmd_ctx* c, int64_t h, void* host) {
     k_dat_to_gid<<<nblk((int64_t)c->n_own * words, 256), 256, 0, c->stream>>>(
         c->n_own, words, c->gid[c->oc_cur], (const unsigned*)d->d, (unsigned*)d->tmp);
     CKL();
-    CK(cudaMemcpyAsync(host, d->tmp, row * (size_t)c->n_global, cudaMemcpyDeviceToHost, c->stream));
+    if (!c->split) {
+        CK(cudaMemcpyAsync(host, d->tmp, row * (size_t)c->n_global, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return LJMD_OK;
+    }
+    // several ranks: only the rows of this rank's particles are written
+    std::vector<char> all(row * (size_t)c->n_global);
+    std::vector<int> g(c->n_own);
+    CK(cudaMemcpyAsync(all.data(), d->tmp, all.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g.data(), c->gid[c->oc_cur], sizeof(int) * g.size(), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    for (int t = 0; t < c->n_own; ++t)
+        std::memcpy((char*)host + row * (size_t)g[t], all.data() + row * (size_t)g[t], row);
     return LJMD_OK;
 }
 
@@ -401,8 +535,8 @@ extern "C" ljmd_status ljmd_dat_free(ljmd_ctx* c, int64_t h) {
     DslDat* d;
     TRY(dat_lookup(c, h, &d));
     CK(cudaStreamSynchronize(c->stream));
-    cudaFree(d->d);
-    cudaFree(d->tmp);
+    for (void* q : {d->d, d->tmp, d->msend[0], d->msend[1]})
+        if (q) cudaFree(q);
     *d = DslDat{};
     return LJMD_OK;
 }
@@ -509,11 +643,67 @@ extern "C" ljmd_status ljmd_loop_create(ljmd_ctx* c, int64_t kind, const char* n
                                            (int)kMaxStageSmem, c->device));
     L.part.assign(L.args.size(), nullptr);
     L.part_cap.assign(L.args.size(), 0);
+    L.jbuf.assign(L.args.size(), nullptr);
+    L.jbuf_cap.assign(L.args.size(), 0);
+    L.jsend.assign(L.args.size(), nullptr);
+    L.jsend_cap.assign(L.args.size(), 0);
     L.alive = true;
     c->loops.push_back(new DslLoop(L));
     *loop = (int64_t)c->loops.size() - 1;
     return LJMD_OK;
 }
+
+namespace {
+// Halo update of one argument the pair loop reads on the j side ("before the
+// execution of the loop halo regions have to be updated for all variables which have a
+// READ access descriptor"): owned rows to their slots, boundary-plane rows exchanged with
+// the z neighbours exactly like the positions, then the ghost cells filled.
+ljmd_status dsl_halo(ljmd_ctx* c, DslLoop& L, size_t k, DslParams& p) {
+    const DslArg& a = L.args[k];
+    const int es = a.dtype == kDslI32 ? 4 : 8;
+    const size_t row = (size_t)a.ncomp * es;
+    const int words = (int)(row / 4);
+    if ((size_t)c->slot_cap > L.jbuf_cap[k]) {
+        TRY(dalloc(c, (char**)&L.jbuf[k], row * (size_t)c->slot_cap));
+        L.jbuf_cap[k] = (size_t)c->slot_cap;
+    }
+    const int ns = c->n_send[0] + c->n_send[1];
+    if ((size_t)std::max(ns, 1) > L.jsend_cap[k]) {
+        TRY(dalloc(c, (char**)&L.jsend[k], row * (size_t)std::max(ns, 1)));
+        L.jsend_cap[k] = (size_t)std::max(ns, 1);
+    }
+    const int n = c->n_own, g = nblk((int64_t)n * a.ncomp, 256);
+    if (a.dtype == kDslF64)
+        k_elems_to_slots<double><<<g, 256, 0, c->stream>>>(n, a.ncomp, c->own_slot, (const double*)p.ptr[k],
+                                                           p.st[k], p.sc[k], (double*)L.jbuf[k]);
+    else if (a.dtype == kDslI64)
+        k_elems_to_slots<long long><<<g, 256, 0, c->stream>>>(n, a.ncomp, c->own_slot, (const long long*)p.ptr[k],
+                                                              p.st[k], p.sc[k], (long long*)L.jbuf[k]);
+    else
+        k_elems_to_slots<int><<<g, 256, 0, c->stream>>>(n, a.ncomp, c->own_slot, (const int*)p.ptr[k], p.st[k],
+                                                        p.sc[k], (int*)L.jbuf[k]);
+    CKL();
+    if (ns) {
+        k_slot_pack_words<<<nblk((int64_t)ns * words, 256), 256, 0, c->stream>>>(
+            ns, words, c->send_idx, (const unsigned*)L.jbuf[k], (unsigned*)L.jsend[k]);
+        CKL();
+    }
+    char* sb = (char*)L.jsend[k];
+    char* rb = (char*)L.jbuf[k] + row * (size_t)c->n_slots;
+    TRY(exchange(c, sb + row * c->n_send[0], row * c->n_send[1], sb, row * c->n_send[0], rb, row * c->n_recv[0],
+                 rb + row * c->n_recv[0], row * c->n_recv[1]));
+    if (c->n_gcell) {
+        GhostCells gc{c->gc_dst, c->gc_src, c->gc_shift, c->n_gcell};
+        k_slot_ghosts_words<<<nblk((int64_t)c->n_gcell * 32, 256), 256, 0, c->stream>>>(
+            gc, c->ebegin, c->ecount, c->recv_cnt, c->recv_off, c->n_slots, words, (unsigned*)L.jbuf[k]);
+        CKL();
+    }
+    p.jptr[k] = L.jbuf[k];
+    p.jst[k] = a.ncomp;
+    p.jsc[k] = 1;
+    return LJMD_OK;
+}
+}  // namespace
 
 extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
     TRY(check_ctx(c));
@@ -537,6 +727,7 @@ extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
     p.n_pad = c->n_pad;
     p.rows_max = kRowsMax;
     p.cut2 = L.cut2;
+    p.slot_t = c->split ? nullptr : c->slot_t;
     const int nblocks = L.kind == 1 ? c->n_tiles : std::max(1, nblk(c->n_own, L.block));
     const size_t oc = c->own_cap;
     for (size_t k = 0; k < L.args.size(); ++k) {
@@ -569,24 +760,51 @@ extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
             }
         }
     }
+    for (size_t k = 0; k < L.args.size(); ++k) {   // j-side data (pair loops)
+        p.jptr[k] = p.ptr[k];
+        p.jst[k] = p.st[k];
+        p.jsc[k] = p.sc[k];
+        const DslArg& a = L.args[k];
+        const bool jside = L.kind == 1 && !a.global && a.handle != LJMD_DAT_POSITION &&
+                           (a.access == LJMD_READ || a.access == LJMD_RW || a.access == LJMD_WRITE);
+        if (!jside || !c->split) continue;
+        if (a.handle == LJMD_DAT_GID) {   // slot-space gids exist for every slot already
+            p.jptr[k] = c->slot_gid;
+            p.jst[k] = 1;
+            p.jsc[k] = 1;
+            continue;
+        }
+        TRY(dsl_halo(c, L, k, p));
+    }
     void* args[] = {&p};
     const size_t smem = L.kind == 1 ? (3 * sizeof(double) + sizeof(int)) * (size_t)(c->max_staged + 1) : 0;
     CK(cudaLaunchKernel((const void*)L.kernel, dim3(nblocks), dim3(L.block), args, smem, c->stream));
     CKL();
-    for (size_t k = 0; k < L.args.size(); ++k) {
+    for (size_t k = 0; k < L.args.size(); ++k) {   // ScalarArray INC: sum, all-reduce, apply
         const DslArg& a = L.args[k];
         if (!a.global || a.access == LJMD_READ) continue;
         DslDat* d = &c->dats[a.handle];
         const int zero = a.access == LJMD_INC_ZERO;
+        if ((size_t)a.ncomp > L.delta_cap) {
+            TRY(dalloc(c, &L.delta, (size_t)a.ncomp));
+            L.delta_cap = (size_t)a.ncomp;
+        }
+        const int g = nblk(a.ncomp, 128);
         if (a.dtype == kDslF64)
-            k_dsl_fin<double><<<nblk(a.ncomp, 128), 128, 0, c->stream>>>((const double*)L.part[k], nblocks, a.ncomp,
-                                                                         (double*)d->d, zero);
+            k_dsl_fin_delta<double><<<g, 128, 0, c->stream>>>((const double*)L.part[k], nblocks, a.ncomp, L.delta);
         else if (a.dtype == kDslI64)
-            k_dsl_fin<long long><<<nblk(a.ncomp, 128), 128, 0, c->stream>>>(
-                (const long long*)L.part[k], nblocks, a.ncomp, (long long*)d->d, zero);
+            k_dsl_fin_delta<long long><<<g, 128, 0, c->stream>>>((const long long*)L.part[k], nblocks, a.ncomp,
+                                                                  L.delta);
         else
-            k_dsl_fin<int><<<nblk(a.ncomp, 128), 128, 0, c->stream>>>((const int*)L.part[k], nblocks, a.ncomp,
-                                                                      (int*)d->d, zero);
+            k_dsl_fin_delta<int><<<g, 128, 0, c->stream>>>((const int*)L.part[k], nblocks, a.ncomp, L.delta);
+        CKL();
+        if (c->split) TRY(allreduce(c, L.delta, a.ncomp, false));
+        if (a.dtype == kDslF64)
+            k_dsl_apply<double><<<g, 128, 0, c->stream>>>(L.delta, a.ncomp, (double*)d->d, zero);
+        else if (a.dtype == kDslI64)
+            k_dsl_apply<long long><<<g, 128, 0, c->stream>>>(L.delta, a.ncomp, (long long*)d->d, zero);
+        else
+            k_dsl_apply<int><<<g, 128, 0, c->stream>>>(L.delta, a.ncomp, (int*)d->d, zero);
         CKL();
     }
     return LJMD_OK;
@@ -612,8 +830,10 @@ extern "C" ljmd_status ljmd_loop_free(ljmd_ctx* c, int64_t loop) {
         return set_err(c, LJMD_E_ARG, "bad loop handle %lld", (long long)loop);
     CK(cudaStreamSynchronize(c->stream));
     DslLoop* L = c->loops[loop];
-    for (void* q : L->part)
-        if (q) cudaFree(q);
+    for (auto* v : {&L->part, &L->jbuf, &L->jsend})
+        for (void* q : *v)
+            if (q) cudaFree(q);
+    if (L->delta) cudaFree(L->delta);
     if (L->lib) cudaLibraryUnload(L->lib);
     delete L;
     c->loops[loop] = nullptr;
@@ -621,15 +841,16 @@ extern "C" ljmd_status ljmd_loop_free(ljmd_ctx* c, int64_t loop) {
 }
 
 void dsl_destroy(ljmd_ctx* c) {
-    for (DslDat& d : c->dats) {
-        if (d.d) cudaFree(d.d);
-        if (d.tmp) cudaFree(d.tmp);
-    }
+    for (DslDat& d : c->dats)
+        for (void* q : {d.d, d.tmp, d.msend[0], d.msend[1]})
+            if (q) cudaFree(q);
     c->dats.clear();
     for (DslLoop* L : c->loops) {
         if (!L) continue;
-        for (void* q : L->part)
-            if (q) cudaFree(q);
+        for (auto* v : {&L->part, &L->jbuf, &L->jsend})
+            for (void* q : *v)
+                if (q) cudaFree(q);
+        if (L->delta) cudaFree(L->delta);
         if (L->lib) cudaLibraryUnload(L->lib);
         delete L;
     }

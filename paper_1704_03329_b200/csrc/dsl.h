@@ -22,10 +22,13 @@ namespace ljmd {
     const int* tr_begin;                                                                      \
     const int* tr_off;                                                                        \
     const int* tile_R;                                                                        \
-    const int* slot_t;           /* slot -> owned index of its particle               */     \
+    const int* slot_t;           /* slot -> owned index (one rank); null: j by slot    */     \
     void* ptr[24];               /* argument k: data base pointer                     */     \
     long long st[24];            /* element (t, c) at ptr[k][t * st[k] + c * sc[k]]   */     \
     long long sc[24];                                                                         \
+    void* jptr[24];              /* j-side data: owned arrays (one rank) or the        */     \
+    long long jst[24];           /* slot-space halo copy (several ranks), indexed by   */     \
+    long long jsc[24];           /* the staged sO[l]                                   */     \
     void* part[24];              /* argument k (ScalarArray INC): per-block partials  */     \
     int n_own;                                                                                \
     int n_pad;                                                                                \
@@ -53,6 +56,8 @@ struct DslDat {
     int esize = 8;
     void* d = nullptr;     // owned order [own_cap][ncomp] (global: [ncomp])
     void* tmp = nullptr;   // permutation / host-order staging, same size
+    void* msend[2] = {nullptr, nullptr};   // migration send rows (nranks > 1)
+    size_t msend_cap = 0;
 };
 
 struct DslArg {
@@ -76,6 +81,12 @@ struct DslLoop {
     std::vector<DslArg> args;
     std::vector<void*> part;      // per-argument partial buffers (ScalarArray INC)
     std::vector<size_t> part_cap;
+    std::vector<void*> jbuf;      // per-argument slot-space halo copy (nranks > 1)
+    std::vector<size_t> jbuf_cap;
+    std::vector<void*> jsend;     // per-argument boundary-plane send rows
+    std::vector<size_t> jsend_cap;
+    double* delta = nullptr;      // ScalarArray INC: this launch's sums (all-reduced)
+    size_t delta_cap = 0;
 };
 
 }  // namespace ljmd

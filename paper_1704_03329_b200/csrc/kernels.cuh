@@ -380,7 +380,7 @@ __global__ void k_migrate_mark(int n_own, const double4* __restrict__ x, const i
                                double4* __restrict__ xs, double* __restrict__ vxs, double* __restrict__ vys,
                                double* __restrict__ vzs, int* __restrict__ gids, MigRec* __restrict__ lo,
                                MigRec* __restrict__ hi, int cap_mig, int* __restrict__ counters,
-                               DevFlags* fl) {
+                               DevFlags* fl, int* __restrict__ stay_t) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_own) return;
     double4 p = x[own_slot[t]];
@@ -411,6 +411,7 @@ __global__ void k_migrate_mark(int n_own, const double4* __restrict__ x, const i
         vys[k] = vy[t];
         vzs[k] = vz[t];
         gids[k] = gid[t];
+        stay_t[k] = t;   // the compaction order, for particle data that travels along (DSL)
     } else {
         const int k = atomicAdd(&counters[dir < 0 ? 1 : 2], 1);
         if (k < cap_mig) {
@@ -418,7 +419,7 @@ __global__ void k_migrate_mark(int n_own, const double4* __restrict__ x, const i
             r.x = p.x; r.y = p.y; r.z = p.z;
             r.vx = vx[t]; r.vy = vy[t]; r.vz = vz[t];
             r.gid = gid[t];
-            r.pad = 0;
+            r.pad = t;       // source row of the particle's other data (DSL)
             (dir < 0 ? lo : hi)[k] = r;
         }
     }

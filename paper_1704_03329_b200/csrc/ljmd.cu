@@ -153,12 +153,14 @@ struct ljmd_ctx {
     double* vs = nullptr;
     int* gs = nullptr;
     int* iota = nullptr;
+    int* stay_t = nullptr;        // compaction order of the stayers (migrate)
     int* h_tot = nullptr;         // pinned: send/recv plane totals
 };
 
 ljmd_status dsl_before_sort(ljmd_ctx* c, const int* gid_old);
 ljmd_status dsl_after_sort(ljmd_ctx* c);
 ljmd_status dsl_to_gid_order(ljmd_ctx* c);
+ljmd_status dsl_migrate(ljmd_ctx* c, int stay, int out_lo, int out_hi, int in_lo, int in_hi);
 void dsl_destroy(ljmd_ctx* c);
 
 namespace {
@@ -772,7 +774,7 @@ ljmd_status migrate(ljmd_ctx* c) {
     k_migrate_mark<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc,
                                                        c->gid[c->oc_cur], c->geo, c->xs, c->vs, c->vs + oc,
                                                        c->vs + 2 * oc, c->gs, c->mig_send[0], c->mig_send[1],
-                                                       c->mig_cap, c->mig_cnt, c->d_fl);
+                                                       c->mig_cap, c->mig_cnt, c->d_fl, c->stay_t);
     CKL();
     TRY(exchange(c, c->mig_cnt + 2, sizeof(int), c->mig_cnt + 1, sizeof(int), c->mig_cnt + 3, sizeof(int),
                  c->mig_cnt + 4, sizeof(int)));
@@ -803,6 +805,7 @@ ljmd_status migrate(ljmd_ctx* c) {
         CKL();
     }
     c->n_own = stay + in_lo + in_hi;
+    TRY(dsl_migrate(c, stay, out_lo, out_hi, in_lo, in_hi));
     return LJMD_OK;
 }
 
@@ -1210,7 +1213,7 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         }
         if ((s = dalloc(c, &c->mig_cnt, 8)) != LJMD_OK || (s = dalloc(c, &c->xs, cap)) != LJMD_OK ||
             (s = dalloc(c, &c->vs, (size_t)3 * cap)) != LJMD_OK || (s = dalloc(c, &c->gs, cap)) != LJMD_OK ||
-            (s = dalloc(c, &c->iota, cap)) != LJMD_OK)
+            (s = dalloc(c, &c->iota, cap)) != LJMD_OK || (s = dalloc(c, &c->stay_t, cap)) != LJMD_OK)
             return fail(s);
         if (cudaMallocHost(&c->h_mig, sizeof(int) * 8) != cudaSuccess ||
             cudaMallocHost(&c->h_tot, sizeof(int) * 4) != cudaSuccess) {
@@ -1458,7 +1461,7 @@ void ljmd_destroy(ljmd_ctx* c) {
         if (p) cudaFree(p);
     dsl_destroy(c);
     for (void* p : {(void*)c->nbr8h, (void*)c->ncount_h, (void*)c->slot_t, (void*)c->tmap, (void*)c->tile_R,
-                    (void*)c->ld_pos, (void*)c->ld_vel, (void*)c->ld_gid})
+                    (void*)c->ld_pos, (void*)c->ld_vel, (void*)c->ld_gid, (void*)c->stay_t})
         if (p) cudaFree(p);
     void* ptrs2[] = {c->send_cnt, c->send_off, c->recv_cnt, c->recv_off, c->send_idx, c->send_buf, c->mig_send[0],
                      c->mig_send[1], c->mig_recv[0], c->mig_recv[1], c->mig_cnt, c->xs, c->vs, c->gs, c->iota};
