@@ -177,6 +177,12 @@ ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q, int64_t* 
  * LJMD_E_ARG if nu < 0, T < 0 or nu*dt > 1. */
 ljmd_status ljmd_set_thermostat(ljmd_ctx* c, double nu, double temperature, uint64_t seed);
 
+/* Switch the per-launch force timing (ljmd_options.profile) on (1) or off (0) between
+ * ljmd_step calls: the CUDA events around every force launch cost a few microseconds per
+ * step, so a benchmark times its headline region without them.  LJMD_E_ARG if profile is
+ * not 0 or 1. */
+ljmd_status ljmd_set_profile(ljmd_ctx* c, int64_t profile);
+
 /* Common-neighbour analysis (Sec. 4.2, Algs. alg:cna_I-III, alg:max_cluster_size,
  * PAPER.md:522-653, 1151-1174) at the current positions, single rank:
  * bonds = pairs with r < rcut (rcut <= rc: taken from the Verlet list).  For every bond

@@ -26,6 +26,7 @@ struct DevFlags {
     int max_staged;              // largest tile staging count at the last build
     int migrate_gid;             // a particle that moved further than one cell plane (INT_MAX: none)
     int overflow;     // analysis capacity exceeded (ljmd_cna)
+    int n_gflat;                 // ghost slots listed by the build-time refresh
     unsigned long long maxdisp2; // bits of max |x - x_build|^2 (non-negative double)
     unsigned long long total_nbr;
 };
@@ -330,12 +331,14 @@ struct GhostCells {
 
 // Sources: gc.src >= 0 -> extended cell (local owned slots); gc.src < 0 -> received plane
 // cell -(src+1), stored after the slot range at n_slots + recv_off[cell] (nranks > 1).
+// at_build also lists every ghost slot as {dst slot, src slot, shift code} (gflat, order
+// immaterial) for the per-step refresh k_ghost_flat.
 template <bool AT_BUILD>
 __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
                                 const int* __restrict__ ecount, Geo g, double4* __restrict__ x,
                                 float4* __restrict__ xf, int* __restrict__ slot_gid,
                                 const int* __restrict__ recv_cnt, const int* __restrict__ recv_off,
-                                int n_slots) {
+                                int n_slots, int4* __restrict__ gflat, DevFlags* fl) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= gc.n) return;
@@ -352,6 +355,11 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
     double sx = (double)((code & 3) - 1), sy = (double)(((code >> 2) & 3) - 1),
            sz = (double)(((code >> 4) & 3) - 1);
     double Lx = sx * g.L[0], Ly = sy * g.L[1], Lz = sz * g.L[2];   // exact
+    int base = 0;
+    if (AT_BUILD) {
+        if (lane == 0) base = atomicAdd(&fl->n_gflat, m);
+        base = __shfl_sync(0xffffffffu, base, 0);
+    }
     for (int k = lane; k < m; k += 32) {
         double4 p = ld256(x + sb + k);
         double4 q = make_double4(__dadd_rn(p.x, Lx), __dadd_rn(p.y, Ly), __dadd_rn(p.z, Lz), 0.0);
@@ -359,8 +367,23 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
         if (AT_BUILD) {
             xf[db + k] = make_float4((float)q.x, (float)q.y, (float)q.z, 0.f);
             slot_gid[db + k] = slot_gid[sb + k];
+            gflat[base + k] = make_int4(db + k, sb + k, code, 0);
         }
     }
+}
+
+// Per-step ghost refresh: thread per ghost slot from the build-time list (one 16-byte
+// descriptor, one 32-byte read, one 32-byte write; every lane busy).
+__global__ void __launch_bounds__(256) k_ghost_flat(int n, const int4* __restrict__ gflat, Geo g,
+                                                    double4* __restrict__ x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 e = gflat[i];
+    const double sx = (double)((e.z & 3) - 1), sy = (double)(((e.z >> 2) & 3) - 1),
+                 sz = (double)(((e.z >> 4) & 3) - 1);
+    const double4 p = ld256(x + e.y);
+    st256(x + e.x, make_double4(__dadd_rn(p.x, sx * g.L[0]), __dadd_rn(p.y, sy * g.L[1]),
+                                __dadd_rn(p.z, sz * g.L[2]), 0.0));
 }
 
 // --------------------------------------------------------------------------- z-slab decomposition
@@ -569,7 +592,10 @@ struct NlistArgs {
 // blocks of 8 entries written with 16-byte stores from registers.
 constexpr int kBuildThreads = 320;
 
-__global__ void __launch_bounds__(kBuildThreads, 5) k_build_nlist(NlistArgs a) {
+#ifndef LJMD_BUILD_MINB
+#define LJMD_BUILD_MINB 5
+#endif
+__global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(NlistArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -698,14 +724,18 @@ __global__ void __launch_bounds__(kBuildThreads, 5) k_build_nlist(NlistArgs a) {
 // up) spreads the 16 lanes of a phase over distinct banks most of the time; measured on C2
 // the force kernel drops from ~199 to ~170 us.  Only the order of a particle's sum
 // changes, not its terms.  Thread per particle; buckets of kRrCap entries per residue in
-// bank-padded shared memory (stride 65 words per thread); a particle with a fuller residue
-// keeps the build order.
+// bank-padded shared memory (288 B, stride 73 words per thread); the per-residue fill and
+// remaining counts live in registers as 16 nibbles each, so the output walk reads a bucket
+// entry at (filled - remaining) (245 us per C2 rebuild against 300 us with count and head
+// arrays in shared memory: occupancy 36 % instead of 24 %).  A particle with a fuller
+// residue keeps the build order.
 constexpr int kRrThreads = 128;
 constexpr int kRrCap = 8;                        // per-residue capacity (mean ~4.6)
 constexpr int kRrOvf = 16;                       // entries beyond a full bucket, emitted last
 constexpr int kRrStrideW = (16 * kRrCap + kRrOvf) / 2 + 1;   // words per thread (odd: no bank aliasing)
-constexpr int kRrCntW = 17;                      // words per thread of the count / head areas
-constexpr size_t kRrSmem = sizeof(unsigned) * (size_t)kRrThreads * (kRrStrideW + 2 * kRrCntW);
+constexpr size_t kRrSmem = sizeof(unsigned) * (size_t)kRrThreads * kRrStrideW;
+
+__device__ __forceinline__ unsigned nib(unsigned long long w, int r) { return (unsigned)(w >> (4 * r)) & 15u; }
 
 __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, int K, Geo g,
                                                        const uint4* __restrict__ in,
@@ -718,8 +748,6 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
     const int tid = threadIdx.x;
     const int t = blockIdx.x * kRrThreads + tid;
     unsigned short* bkt = reinterpret_cast<unsigned short*>(rr_smem + (size_t)tid * kRrStrideW);
-    int* cnt = reinterpret_cast<int*>(rr_smem + (size_t)kRrThreads * kRrStrideW) + tid * kRrCntW;
-    int* head = reinterpret_cast<int*>(rr_smem + (size_t)kRrThreads * (kRrStrideW + kRrCntW)) + tid * kRrCntW;
     if (t >= n_own) return;
     const int n = min(ncount[t], K);
     const int nb = (n + 7) >> 3;
@@ -728,11 +756,7 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
     lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
     const int tile = tile_of_cell(g, cx, cy, cz);
     const int off = (t - obegin[tile_oc0[tile]]) & 15;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-        cnt[r] = 0;
-        head[r] = 0;
-    }
+    unsigned long long cnt = 0ull;   // entries filed per residue (nibbles)
     bool overflow = false;
     int novf = 0;
     unsigned short pad = 0;
@@ -746,10 +770,10 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
             const unsigned short l = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
             if (b * 8 + e < n) {
                 const int r = l & 15;
-                const int c = cnt[r];
-                if (c < kRrCap) {
+                const unsigned c = nib(cnt, r);
+                if (c < (unsigned)kRrCap) {
                     bkt[r * kRrCap + c] = l;
-                    cnt[r] = c + 1;
+                    cnt += 1ull << (4 * r);
                 } else if (novf < kRrOvf) {
                     bkt[16 * kRrCap + novf++] = l;
                 } else {
@@ -767,26 +791,32 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
     unsigned avail = 0u;
 #pragma unroll
     for (int r = 0; r < 16; ++r)
-        if (cnt[r]) avail |= 1u << r;
-    unsigned long long lo64 = 0ull, hi64 = 0ull;   // 8 pending entries, shifted in from the top
+        if (nib(cnt, r)) avail |= 1u << r;
+    unsigned long long rem = cnt;   // entries not yet emitted per residue
+    const int nin = n - novf;
+    unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;   // 8 pending entries, shifted in from the top
+    uint4* o = out + t;
     for (int k = 0; k < nb * 8; ++k) {
-        unsigned short l = pad;
-        if (k >= n - novf && k < n) {
-            l = bkt[16 * kRrCap + (k - (n - novf))];
-        } else if (k < n) {
+        unsigned l = pad;
+        if (k < nin) {
             const int tgt = (off + k) & 15;
             const unsigned rot = ((avail >> tgt) | (avail << (16 - tgt))) & 0xffffu;
             const int rr = (tgt + __ffs(rot) - 1) & 15;
-            const int h = head[rr];
-            l = bkt[rr * kRrCap + h];
-            head[rr] = h + 1;
-            if (h + 1 == cnt[rr]) avail &= ~(1u << rr);
+            const unsigned m = nib(rem, rr);
+            l = bkt[rr * kRrCap + (nib(cnt, rr) - m)];
+            rem -= 1ull << (4 * rr);
+            if (m == 1u) avail &= ~(1u << rr);
+        } else if (k < n) {
+            l = bkt[16 * kRrCap + (k - nin)];
         }
-        lo64 = (lo64 >> 16) | (hi64 << 48);
-        hi64 = (hi64 >> 16) | ((unsigned long long)l << 48);
-        if ((k & 7) == 7)
-            out[(size_t)(k >> 3) * stride + t] =
-                make_uint4((unsigned)lo64, (unsigned)(lo64 >> 32), (unsigned)hi64, (unsigned)(hi64 >> 32));
+        w0 = __funnelshift_r(w0, w1, 16);
+        w1 = __funnelshift_r(w1, w2, 16);
+        w2 = __funnelshift_r(w2, w3, 16);
+        w3 = __funnelshift_r(w3, l, 16);
+        if ((k & 7) == 7) {
+            *o = make_uint4(w0, w1, w2, w3);
+            o += stride;
+        }
     }
 }
 
@@ -873,7 +903,14 @@ __device__ __forceinline__ void andersen(unsigned long long seed, long long step
     vz = __dmul_rn(sd, __dmul_rn(R2, cos(__dmul_rn(two_pi, U4))));
 }
 
-constexpr int kForceThreads = 320;   // ~16 cells x 18.5 particles per tile at rho = 0.8442
+constexpr int kForceThreads = 320;
+// 3 CTAs of 320 threads per SM with up to 64 registers: measured on C2 160 us per launch
+// against 167 us at 4 CTAs / 48 registers and 170 us at 2 CTAs (more in-flight neighbours
+// per warp beats more warps)
+#ifndef LJMD_FORCE_MINB
+#define LJMD_FORCE_MINB 3
+#endif
+   // ~16 cells x 18.5 particles per tile at rho = 0.8442
 
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -1019,7 +1056,7 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
 // LDS.64 from one address (bank group = 3 l mod 16, spread across a half-warp by the
 // bank-aware list order) instead of a scattered 32 B global gather.
 template <bool ENERGY, int MODE, bool CHECK>
-__global__ void __launch_bounds__(kForceThreads, 4) k_force(ForceArgs a) {
+__global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double sh[kForceThreads / 32];
     const int tile = blockIdx.x;

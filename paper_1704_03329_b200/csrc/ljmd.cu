@@ -79,6 +79,8 @@ struct ljmd_ctx {
     int* ecount = nullptr;
     int* ebegin = nullptr;   // n_ecell + 1
     int* ecell_src = nullptr;
+    int4* gflat = nullptr;            // ghost slots {dst, src, shift code} (k_ghost_flat)
+    int n_gflat = 0;
     int* gc_dst = nullptr;
     int* gc_src = nullptr;
     int* gc_shift = nullptr;
@@ -433,6 +435,7 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     }
     TRY(dalloc(c, &c->xf, cap));
     TRY(dalloc(c, &c->slot_gid, cap));
+    TRY(dalloc(c, &c->gflat, cap));
     if (c->newton3 || c->dsl_on) {
         TRY(dalloc(c, &c->slot_t, cap));
         c->slot_t_valid = false;
@@ -755,11 +758,9 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
     if (at_build)
         k_ghost_refresh<true><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo, c->x[c->xc],
                                                              c->xf, c->slot_gid, c->recv_cnt, c->recv_off,
-                                                             c->n_slots);
-    else
-        k_ghost_refresh<false><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo,
-                                                              c->x[c->xc], c->xf, c->slot_gid, c->recv_cnt,
-                                                              c->recv_off, c->n_slots);
+                                                             c->n_slots, c->gflat, c->d_fl);
+    else if (c->n_gflat > 0)
+        k_ghost_flat<<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->geo, c->x[c->xc]);
     CKL();
     return LJMD_OK;
 }
@@ -908,6 +909,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     CKL();
     TRY(sync_flags(c));
     c->max_staged = c->h_fl->max_staged;
+    c->n_gflat = c->h_fl->n_gflat;
     if (16 * (size_t)(c->max_staged + 1) > kMaxStageSmem || c->max_staged > 65535)
         return set_err(c, LJMD_E_CAPACITY,
                        "a force tile needs %d staged particles (> %zu B of shared memory): density too high",
@@ -1548,6 +1550,13 @@ extern "C" ljmd_status ljmd_set_thermostat(ljmd_ctx* c, double nu, double temper
     c->nu_dt = nu * c->dt;
     c->thermo_sd = std::sqrt(temperature / c->opt.mass);
     c->thermo_seed = seed;
+    return LJMD_OK;
+}
+
+extern "C" ljmd_status ljmd_set_profile(ljmd_ctx* c, int64_t profile) {
+    TRY(check_ctx(c));
+    if (profile != 0 && profile != 1) return set_err(c, LJMD_E_ARG, "ljmd_set_profile: profile must be 0 or 1");
+    c->opt.profile = profile;
     return LJMD_OK;
 }
 

@@ -28,7 +28,7 @@ EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "
            "ljmd_get_positions", "ljmd_get_velocities", "ljmd_get_particle_energy", "ljmd_get_energy",
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
-           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna", "ljmd_set_thermostat",
+           "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna", "ljmd_set_thermostat", "ljmd_set_profile",
            "ljmd_dat_create", "ljmd_dat_set", "ljmd_dat_get", "ljmd_dat_free", "ljmd_loop_create",
            "ljmd_loop_execute", "ljmd_loop_source", "ljmd_loop_free")
 
@@ -103,6 +103,7 @@ def load(path: str = None):
         "ljmd_nccl_unique_id": ([ctypes.c_void_p], ctypes.c_int),
         "ljmd_boa": ([vp, ctypes.c_int64, ctypes.c_double, _D, _I], ctypes.c_int),
         "ljmd_set_thermostat": ([vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64], ctypes.c_int),
+        "ljmd_set_profile": ([vp, ctypes.c_int64], ctypes.c_int),
         "ljmd_cna": ([vp, ctypes.c_double, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), _I],
                      ctypes.c_int),
         "ljmd_dat_create": ([vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I], ctypes.c_int),
@@ -304,6 +305,10 @@ class LJMD:
         """Andersen thermostat: collision frequency nu (probability nu*dt per step),
         target temperature T, Philox seed; nu = 0 restores NVE."""
         self._ck(self._lib.ljmd_set_thermostat(self._h, float(nu), float(temperature), int(seed)))
+
+    def set_profile(self, on: bool):
+        """Per-launch CUDA-event timing of the force kernel on/off (ljmd_get_stats force_ms)."""
+        self._ck(self._lib.ljmd_set_profile(self._h, 1 if on else 0))
 
     def cna(self, rcut: float, triplets: bool = False):
         """Common-neighbour analysis (Sec. 4.2): class per particle (0 other, 1 fcc, 2 hcp,
