@@ -118,8 +118,26 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
                       const ljmd_options* opt);
 
 /* Replace positions and velocities (same n, box and parameters as init) and
- * redo the init sequence (wrap, bin, list, F(r0), step-0 energies). */
+ * redo the init sequence (wrap, bin, list, F(r0), step-0 energies).
+ * pos = vel = NULL: take the state most recently queued by ljmd_stage_state (single
+ * rank; LJMD_E_ARG if none is queued). */
 ljmd_status ljmd_set_state(ljmd_ctx* c, const double* pos, const double* vel);
+
+/* Overlapped host transfers for a stream of states (single rank, nranks = 1 without
+ * split_self; LJMD_E_ARG otherwise).  The context owns a copy stream and two device
+ * staging buffers per direction, so a transfer runs while the previous state computes.
+ *
+ * ljmd_stage_state: queue the host->device copy of pos and vel ([n][3] fp64, caller
+ *   order; page-locked memory for a truly asynchronous copy) and return.  The host arrays
+ *   must stay valid and unchanged until the ljmd_set_state(c, NULL, NULL) that consumes
+ *   them has returned.  At most two states may be queued ahead of their consumption.
+ * ljmd_get_positions_async: queue the device->host copy of the current positions
+ *   ([n][3], caller order, unwrapped as ljmd_get_positions) into out and return; out is
+ *   complete after ljmd_wait_transfers.
+ * ljmd_wait_transfers: block until every queued copy has completed. */
+ljmd_status ljmd_stage_state(ljmd_ctx* c, const double* pos, const double* vel);
+ljmd_status ljmd_get_positions_async(ljmd_ctx* c, double* out);
+ljmd_status ljmd_wait_transfers(ljmd_ctx* c);
 
 /* Advance nsteps velocity-Verlet steps (Alg. alg:VelocityVerlet lines 5-9):
  * v += dt/(2m) F; r += dt v; [rebuild every Ns steps, after the drift, R8];

@@ -32,6 +32,22 @@ struct DevFlags {
 };
 
 // --------------------------------------------------------------------------- helpers
+// Small device->host results (flags, counts, energies) are written by a kernel into mapped
+// page-locked memory instead of a copy-engine transfer, so they never queue behind a bulk
+// host transfer of the copy stream (ljmd_get_positions_async / ljmd_stage_state).
+__global__ void k_copy_words(const unsigned* __restrict__ src, unsigned* dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void k_reset_flags(DevFlags* fl) {
+    DevFlags f;
+    memset(&f, 0, sizeof f);
+    f.migrate_gid = INT_MAX;
+    f.nonfinite_gid = INT_MAX;
+    f.overlap_gid = INT_MAX;
+    f.overlap_gid_j = -1;
+    *fl = f;
+}
 __device__ __forceinline__ double4 ld256(const double4* p) {
     double4 r;
     asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"

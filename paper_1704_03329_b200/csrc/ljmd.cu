@@ -117,6 +117,8 @@ struct ljmd_ctx {
     double* ke_part = nullptr;
     int n_fblocks = 0;
     double* hist = nullptr;   // [hist_cap][2]
+    double* h_histm = nullptr;   // mapped page-locked readback of hist
+    int64_t h_histm_cap = 0;
     int64_t hist_cap = 0, hist_count = 0;
     std::vector<double> h_hist;
     // ---- flags / staging
@@ -124,6 +126,14 @@ struct ljmd_ctx {
     DevFlags* h_fl = nullptr;      // pinned
     int* h_slots = nullptr;        // pinned
     double* d_stage = nullptr;     // [3][own_cap] readback staging
+    // overlapped host transfers (ljmd_stage_state / ljmd_get_positions_async)
+    cudaStream_t copy_stream = nullptr;
+    double* stg[2] = {nullptr, nullptr};      // [pos 3n | vel 3n] staged states
+    cudaEvent_t stg_ev[2] = {nullptr, nullptr}, stg_used[2] = {nullptr, nullptr};
+    int stg_next = 0, stg_queued = 0;         // next buffer to fill, states queued
+    double* rb[2] = {nullptr, nullptr};       // [3n] positions in caller order
+    cudaEvent_t rb_ev[2] = {nullptr, nullptr}, rb_done[2] = {nullptr, nullptr};
+    int rb_next = 0;
     // ---- policy / stats
     int64_t since = 0, steps_done = 0, n_rebuilds = 0, regrows = 0;
     std::vector<int64_t> rebuild_steps;
@@ -239,24 +249,23 @@ ljmd_status scan(ljmd_ctx* c, const int* in, int n, int* out) {
     return LJMD_OK;
 }
 
+// device -> mapped host memory by a kernel (no copy engine); complete after a stream sync
+ljmd_status to_host(ljmd_ctx* c, void* hmapped, const void* dsrc, size_t bytes) {
+    k_copy_words<<<1, 256, 0, c->stream>>>(static_cast<const unsigned*>(dsrc), static_cast<unsigned*>(hmapped),
+                                          (int)(bytes / 4));
+    CKL();
+    return LJMD_OK;
+}
+
 ljmd_status sync_flags(ljmd_ctx* c) {
-    CK(cudaMemcpyAsync(c->h_fl, c->d_fl, sizeof(DevFlags), cudaMemcpyDeviceToHost, c->stream));
+    TRY(to_host(c, c->h_fl, c->d_fl, sizeof(DevFlags)));
     CK(cudaStreamSynchronize(c->stream));
     return LJMD_OK;
 }
 
 ljmd_status reset_flags(ljmd_ctx* c) {
-    DevFlags f{};
-    f.max_nbr = 0;
-    f.max_staged = 0;
-    f.migrate_gid = INT_MAX;
-    f.nonfinite_gid = INT_MAX;
-    f.overlap_gid = INT_MAX;
-    f.overlap_gid_j = -1;
-    f.maxdisp2 = 0ull;
-    f.total_nbr = 0ull;
-    *c->h_fl = f;
-    CK(cudaMemcpyAsync(c->d_fl, c->h_fl, sizeof(DevFlags), cudaMemcpyHostToDevice, c->stream));
+    k_reset_flags<<<1, 1, 0, c->stream>>>(c->d_fl);
+    CKL();
     return LJMD_OK;
 }
 
@@ -851,7 +860,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
                                                               c->recv_cnt, c->ecount);
     CKL();
     TRY(scan(c, c->ecount, c->n_ecell, c->ebegin));
-    CK(cudaMemcpyAsync(c->h_slots, c->ebegin + c->n_ecell, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TRY(to_host(c, c->h_slots, c->ebegin + c->n_ecell, sizeof(int)));
     TRY(sync_flags(c));
     if (c->h_fl->nonfinite_gid != INT_MAX)
         return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
@@ -964,15 +973,23 @@ ljmd_status finalize_energy(ljmd_ctx* c, double* dst) {
 
 ljmd_status pull_hist(ljmd_ctx* c, int64_t count) {
     if (count <= 0) return LJMD_OK;
-    std::vector<double> tmp((size_t)2 * count);
-    CK(cudaMemcpyAsync(tmp.data(), c->hist, sizeof(double) * 2 * count, cudaMemcpyDeviceToHost, c->stream));
+    if (count > c->h_histm_cap) {
+        if (c->h_histm) cudaFreeHost(c->h_histm);
+        c->h_histm = nullptr;
+        c->h_histm_cap = 0;
+        CK(cudaHostAlloc(&c->h_histm, sizeof(double) * 2 * (size_t)count, cudaHostAllocMapped));
+        c->h_histm_cap = count;
+    }
+    TRY(to_host(c, c->h_histm, c->hist, sizeof(double) * 2 * (size_t)count));
     CK(cudaStreamSynchronize(c->stream));
-    c->h_hist.insert(c->h_hist.end(), tmp.begin(), tmp.end());
+    c->h_hist.insert(c->h_hist.end(), c->h_histm, c->h_histm + 2 * count);
     return LJMD_OK;
 }
 
-// init sequence shared by ljmd_init and ljmd_set_state
-ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
+// init sequence shared by ljmd_init and ljmd_set_state; dpos/dvel != null: the state is
+// already on the device (a staged state, single rank)
+ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const double* dpos_in = nullptr,
+                       const double* dvel_in = nullptr) {
     int64_t n = c->n_global;
     std::vector<double> fp, fv;
     std::vector<int> fg;
@@ -1007,11 +1024,16 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
         TRY(dalloc(c, &c->ld_vel, (size_t)3 * c->n_global));
         if (c->split) TRY(dalloc(c, &c->ld_gid, (size_t)c->n_global));
     }
-    double* dpos = c->ld_pos;
-    double* dvel = c->ld_vel;
+    const double* dpos = c->ld_pos;
+    const double* dvel = c->ld_vel;
     int* dg = nullptr;
-    CK(cudaMemcpyAsync(dpos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(dvel, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    if (dpos_in) {
+        dpos = dpos_in;
+        dvel = dvel_in;
+    } else {
+        CK(cudaMemcpyAsync(c->ld_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->ld_vel, vel, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c->stream));
+    }
     if (c->split) {
         dg = c->ld_gid;
         CK(cudaMemcpyAsync(dg, fg.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
@@ -1025,6 +1047,10 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel) {
     k_load_rows<<<nblk(n, 256), 256, 0, c->stream>>>((int)n, dpos, dvel, c->x[0], v, v + oc, v + 2 * oc,
                                                     c->gid[0], c->own_slot, dg, c->d_fl);
     CKL();
+    if (dpos_in) {   // the staged buffer may be refilled once this kernel has read it
+        const int b = dpos_in == c->stg[0] ? 0 : 1;
+        CK(cudaEventRecord(c->stg_used[b], c->stream));
+    }
     TRY(sync_flags(c));
     if (c->h_fl->nonfinite_gid != INT_MAX)
         return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
@@ -1198,8 +1224,8 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     if ((s = plan_geometry(c, box)) != LJMD_OK) return fail(s);
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
-        cudaMallocHost(&c->h_fl, sizeof(DevFlags)) != cudaSuccess ||
-        cudaMallocHost(&c->h_slots, sizeof(int)) != cudaSuccess) {
+        cudaHostAlloc(&c->h_fl, sizeof(DevFlags), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostAlloc(&c->h_slots, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
         set_err(c, LJMD_E_CUDA, "flag allocation failed");
         return fail(LJMD_E_CUDA);
     }
@@ -1238,8 +1264,77 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
 
 ljmd_status ljmd_set_state(ljmd_ctx* c, const double* pos, const double* vel) {
     TRY(check_ctx(c));
+    if (!pos && !vel) {
+        if (c->stg_queued == 0) return set_err(c, LJMD_E_ARG, "ljmd_set_state(NULL, NULL): no staged state queued");
+        const int b = (c->stg_next + 2 - c->stg_queued) & 1;   // oldest queued buffer
+        --c->stg_queued;
+        CK(cudaStreamWaitEvent(c->stream, c->stg_ev[b], 0));
+        const size_t n3 = (size_t)3 * c->n_global;
+        return load_state(c, nullptr, nullptr, c->stg[b], c->stg[b] + n3);
+    }
     if (!pos || !vel) return LJMD_E_ARG;
     return load_state(c, pos, vel);
+}
+
+static ljmd_status transfers_init(ljmd_ctx* c) {
+    if (c->split || c->n_own != c->n_global)
+        return set_err(c, LJMD_E_ARG, "overlapped transfers need a single rank (nranks = 1, no split_self)");
+    if (c->copy_stream) return LJMD_OK;
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    const size_t n3 = (size_t)3 * c->n_global;
+    for (int b = 0; b < 2; ++b) {
+        TRY(dalloc(c, &c->stg[b], 2 * n3));
+        TRY(dalloc(c, &c->rb[b], n3));
+        CK(cudaEventCreateWithFlags(&c->stg_ev[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->stg_used[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->rb_ev[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->rb_done[b], cudaEventDisableTiming));
+        CK(cudaEventRecord(c->stg_used[b], c->stream));
+        CK(cudaEventRecord(c->rb_done[b], c->copy_stream));
+    }
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_stage_state(ljmd_ctx* c, const double* pos, const double* vel) {
+    TRY(check_ctx(c));
+    if (!pos || !vel) return LJMD_E_ARG;
+    TRY(transfers_init(c));
+    if (c->stg_queued >= 2) return set_err(c, LJMD_E_ARG, "ljmd_stage_state: two states already queued");
+    const int b = c->stg_next;
+    const size_t n3 = (size_t)3 * c->n_global;
+    CK(cudaStreamWaitEvent(c->copy_stream, c->stg_used[b], 0));   // its last consumer has read it
+    CK(cudaMemcpyAsync(c->stg[b], pos, sizeof(double) * n3, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaMemcpyAsync(c->stg[b] + n3, vel, sizeof(double) * n3, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaEventRecord(c->stg_ev[b], c->copy_stream));
+    c->stg_next = b ^ 1;
+    ++c->stg_queued;
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_positions_async(ljmd_ctx* c, double* out) {
+    TRY(check_ctx(c));
+    if (!out) return LJMD_E_ARG;
+    TRY(transfers_init(c));
+    const int b = c->rb_next;
+    c->rb_next = b ^ 1;
+    CK(cudaStreamWaitEvent(c->stream, c->rb_done[b], 0));   // its previous copy-out has finished
+    k_gather_pos<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->x[c->xc], c->own_slot, c->d_stage);
+    CKL();
+    k_rows_to_gid<<<nblk((int64_t)c->n_own * 3, 256), 256, 0, c->stream>>>(c->n_own, 3, c->gid[c->oc_cur],
+                                                                          c->d_stage, c->rb[b]);
+    CKL();
+    CK(cudaEventRecord(c->rb_ev[b], c->stream));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->rb_ev[b], 0));
+    CK(cudaMemcpyAsync(out, c->rb[b], sizeof(double) * 3 * (size_t)c->n_own, cudaMemcpyDeviceToHost,
+                       c->copy_stream));
+    CK(cudaEventRecord(c->rb_done[b], c->copy_stream));
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_wait_transfers(ljmd_ctx* c) {
+    TRY(check_ctx(c));
+    if (c->copy_stream) CK(cudaStreamSynchronize(c->copy_stream));
+    return LJMD_OK;
 }
 
 ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
@@ -1364,11 +1459,14 @@ ljmd_status ljmd_get_energy(ljmd_ctx* c, double* pe, double* ke) {
     double* tmp = c->hist + 2 * (c->hist_cap - 1);
     TRY(finalize_energy(c, tmp));
     TRY(allreduce(c, tmp, 2, false));
-    double h[2];
-    CK(cudaMemcpyAsync(h, tmp, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    if (c->h_histm_cap < 1) {
+        CK(cudaHostAlloc(&c->h_histm, sizeof(double) * 2, cudaHostAllocMapped));
+        c->h_histm_cap = 1;
+    }
+    TRY(to_host(c, c->h_histm, tmp, sizeof(double) * 2));
     CK(cudaStreamSynchronize(c->stream));
-    if (pe) *pe = h[0];
-    if (ke) *ke = h[1];
+    if (pe) *pe = c->h_histm[0];
+    if (ke) *ke = c->h_histm[1];
     return LJMD_OK;
 }
 
@@ -1473,8 +1571,19 @@ void ljmd_destroy(ljmd_ctx* c) {
     if (c->h_tot) cudaFreeHost(c->h_tot);
     delete c->tr;
     if (c->h_fl) cudaFreeHost(c->h_fl);
+    if (c->h_histm) cudaFreeHost(c->h_histm);
     if (c->h_slots) cudaFreeHost(c->h_slots);
     for (auto e : c->ev) cudaEventDestroy(e);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(c->stg[b]);
+            cudaFree(c->rb[b]);
+            for (cudaEvent_t e : {c->stg_ev[b], c->stg_used[b], c->rb_ev[b], c->rb_done[b]})
+                if (e) cudaEventDestroy(e);
+        }
+        cudaStreamDestroy(c->copy_stream);
+    }
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -29,6 +29,7 @@ EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
            "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna", "ljmd_set_thermostat", "ljmd_set_profile",
+           "ljmd_stage_state", "ljmd_get_positions_async", "ljmd_wait_transfers",
            "ljmd_dat_create", "ljmd_dat_set", "ljmd_dat_get", "ljmd_dat_free", "ljmd_loop_create",
            "ljmd_loop_execute", "ljmd_loop_source", "ljmd_loop_free")
 
@@ -84,6 +85,9 @@ def load(path: str = None):
         "ljmd_init": ([ctypes.POINTER(vp), ctypes.c_int64, _D, _D, _D, ctypes.c_double, ctypes.c_double,
                        ctypes.c_double, ctypes.c_double, ctypes.POINTER(Options)], ctypes.c_int),
         "ljmd_set_state": ([vp, _D, _D], ctypes.c_int),
+        "ljmd_stage_state": ([vp, _D, _D], ctypes.c_int),
+        "ljmd_get_positions_async": ([vp, _D], ctypes.c_int),
+        "ljmd_wait_transfers": ([vp], ctypes.c_int),
         "ljmd_step": ([vp, ctypes.c_int64], ctypes.c_int),
         "ljmd_get_forces": ([vp, _D], ctypes.c_int),
         "ljmd_get_positions": ([vp, _D, ctypes.c_int64], ctypes.c_int),
@@ -247,6 +251,23 @@ class LJMD:
     def set_state_ptr(self, pos_ptr: int, vel_ptr: int):
         """Same as set_state, from raw host pointers (e.g. pinned torch tensors)."""
         self._ck(self._lib.ljmd_set_state(self._h, ctypes.cast(pos_ptr, _D), ctypes.cast(vel_ptr, _D)))
+
+    def stage_state_ptr(self, pos_ptr: int, vel_ptr: int):
+        """Queue an overlapped host->device copy of the next state (page-locked host arrays,
+        [n][3] fp64); consumed by set_staged_state.  The arrays must stay unchanged until then."""
+        self._ck(self._lib.ljmd_stage_state(self._h, ctypes.cast(pos_ptr, _D), ctypes.cast(vel_ptr, _D)))
+
+    def set_staged_state(self):
+        """ljmd_set_state(NULL, NULL): load the oldest state queued by stage_state_ptr."""
+        self._ck(self._lib.ljmd_set_state(self._h, None, None))
+
+    def positions_async_ptr(self, ptr: int):
+        """Queue an overlapped device->host copy of the positions (caller order) into a
+        page-locked [n][3] fp64 buffer; complete after wait_transfers()."""
+        self._ck(self._lib.ljmd_get_positions_async(self._h, ctypes.cast(ptr, _D)))
+
+    def wait_transfers(self):
+        self._ck(self._lib.ljmd_wait_transfers(self._h))
 
     def step(self, nsteps: int):
         self._ck(self._lib.ljmd_step(self._h, int(nsteps)))
