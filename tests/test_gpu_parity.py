@@ -262,14 +262,16 @@ def test_errors(eng):
 
 # ------------------------------------------------------------------------------ full size
 
-@pytest.mark.parametrize("cfg", ["C2"])
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
 def test_full_size_sampled(eng, orc, cfg):
-    """BASELINE configs[1] (N = 1,048,576) in the bench's launch configuration: the
-    neighbour lists and forces of 64 sampled particles (incl. box corners, seams) equal the
-    oracle's brute force computed row by row; invariants at any size: sum F ~ 0."""
+    """BASELINE configs at full size on one GPU -- C2 (N = 1,048,576, the bench's launch
+    configuration), C3 (8,388,608), C4 (2,097,152, non-cubic box) and C5 (2,048,000 perturbed
+    at T = 1.5 under the displacement-checked rebuild policy): the neighbour lists and forces
+    of 64 sampled particles (incl. box corners, seams) equal the oracle's brute force computed
+    row by row; invariants at any size: sum F ~ 0."""
     c = li.CONFIGS[cfg]
     pos, vel, box = c.build()
-    with eng.LJMD(pos, vel, box) as ctx:
+    with eng.LJMD(pos, vel, box, rebuild_check=c.rebuild_check) as ctx:
         ctx.step(21)
         x = ctx.positions()
         n = len(x)
