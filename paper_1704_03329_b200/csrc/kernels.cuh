@@ -27,6 +27,7 @@ struct DevFlags {
     int migrate_gid;             // a particle that moved further than one cell plane (INT_MAX: none)
     int overflow;     // analysis capacity exceeded (ljmd_cna)
     int n_gflat;                 // ghost slots listed by the build-time refresh
+    int n_grecv;                 // of those, images of received halo planes (nranks > 1)
     unsigned long long maxdisp2; // bits of max |x - x_build|^2 (non-negative double)
     unsigned long long total_nbr;
 };
@@ -400,6 +401,51 @@ __global__ void __launch_bounds__(256) k_ghost_flat(int n, const int4* __restric
     const double4 p = ld256(x + e.y);
     st256(x + e.x, make_double4(__dadd_rn(p.x, sx * g.L[0]), __dadd_rn(p.y, sy * g.L[1]),
                                 __dadd_rn(p.z, sz * g.L[2]), 0.0));
+}
+
+// Ghost images per owned particle (CSR, built at the rebuild from the ghost list): the
+// kernels that move a particle -- the fused force epilogue and the opening kick-drift --
+// also write its periodic images x + s L (one rounding, as k_ghost_refresh), so the ghost
+// slots never need a separate per-step refresh.  Images of received halo planes
+// (nranks > 1) are listed apart (grecv) and refreshed after each exchange.
+struct Images {
+    const int* off;    // [n_own + 1]; null: the kernel writes no images
+    const int2* e;     // {dst slot, shift code}
+};
+
+__device__ __forceinline__ void write_images(const Images& im, int t, const Geo& g, double4* __restrict__ x,
+                                             double4 p) {
+    if (!im.off) return;
+    const int b = im.off[t], e = im.off[t + 1];
+    for (int i = b; i < e; ++i) {
+        const int2 d = im.e[i];
+        st256(x + d.x, make_double4(__dadd_rn(p.x, (double)((d.y & 3) - 1) * g.L[0]),
+                                    __dadd_rn(p.y, (double)(((d.y >> 2) & 3) - 1) * g.L[1]),
+                                    __dadd_rn(p.z, (double)(((d.y >> 4) & 3) - 1) * g.L[2]), 0.0));
+    }
+}
+
+__global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __restrict__ slot2t) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n_own) slot2t[own_slot[t]] = t;
+}
+
+// FILL = false: count the images of each owned source (and move received-plane images to
+// grecv); FILL = true: place them (the counts return to zero)
+template <bool FILL>
+__global__ void k_img_build(int n, const int4* __restrict__ gflat, int n_slots, const int* __restrict__ slot2t,
+                            int* __restrict__ cnt, const int* __restrict__ off, int2* __restrict__ img,
+                            int4* __restrict__ grecv, DevFlags* fl) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 e = gflat[i];
+    if (e.y < n_slots) {
+        const int t = slot2t[e.y];
+        if (FILL) img[off[t] + atomicSub(&cnt[t], 1) - 1] = make_int2(e.x, e.z);
+        else atomicAdd(&cnt[t], 1);
+    } else if (!FILL) {
+        grecv[atomicAdd(&fl->n_grecv, 1)] = e;
+    }
 }
 
 // --------------------------------------------------------------------------- z-slab decomposition
@@ -867,6 +913,7 @@ struct ForceArgs {
     double* pe_part;         // per-block partial sums (ENERGY)
     double* ke_part;
     const double4* xbuild;   // displacement check (may be null)
+    Images im;               // ghost images written with x(n+1) (kKKD)
     DevFlags* fl;
     int n_own, n_pad;
     double rc2, c12, nc6, a12, na6, a0;   // nc6 = -c6, na6 = -a6 (fold into DFMA operands)
@@ -1048,6 +1095,7 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
                                             __dadd_rn(xi.y, __dmul_rn(a.dt, vy)),
                                             __dadd_rn(xi.z, __dmul_rn(a.dt, vz)), 0.0);
             st256(a.x_next + P.si, xn);
+            write_images(a.im, t, a.g, a.x_next, xn);
             if (CHECK) {
                 const double4 bb = a.xbuild[t];
                 // non-negative doubles order like their bit patterns
@@ -1138,7 +1186,7 @@ __global__ void k_kick_drift(int n_own, double4* __restrict__ x, const int* __re
                              double* __restrict__ vx, double* __restrict__ vy, double* __restrict__ vz,
                              const double* __restrict__ fx, const double* __restrict__ fy,
                              const double* __restrict__ fz, double h, double dt,
-                             const double4* __restrict__ xbuild, DevFlags* fl) {
+                             const double4* __restrict__ xbuild, DevFlags* fl, Images im, Geo g) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long bits = 0ull;
     if (t < n_own) {
@@ -1151,6 +1199,7 @@ __global__ void k_kick_drift(int n_own, double4* __restrict__ x, const int* __re
         p.y = __dadd_rn(p.y, __dmul_rn(dt, b));
         p.z = __dadd_rn(p.z, __dmul_rn(dt, c));
         x[si] = p;
+        write_images(im, t, g, x, p);
         vx[t] = a; vy[t] = b; vz[t] = c;
         if (CHECK) {
             double4 q = xbuild[t];

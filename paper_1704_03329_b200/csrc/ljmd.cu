@@ -81,6 +81,12 @@ struct ljmd_ctx {
     int* ecell_src = nullptr;
     int4* gflat = nullptr;            // ghost slots {dst, src, shift code} (k_ghost_flat)
     int n_gflat = 0;
+    int* slot2t = nullptr;            // owned slot -> owned index (image build)
+    int* img_cnt = nullptr;           // [own_cap] images per owned particle (scratch)
+    int* img_off = nullptr;           // [own_cap + 1] CSR offsets of the ghost images
+    int2* img = nullptr;              // {dst slot, shift code}
+    int4* grecv = nullptr;            // images of received halo planes (nranks > 1)
+    int n_grecv = 0;
     int* gc_dst = nullptr;
     int* gc_src = nullptr;
     int* gc_shift = nullptr;
@@ -412,6 +418,8 @@ ljmd_status alloc_owned(ljmd_ctx* c, int cap) {
     TRY(dalloc(c, &c->rank_in, cap));
     TRY(dalloc(c, &c->perm, cap));
     TRY(dalloc(c, &c->ncount, cap));
+    TRY(dalloc(c, &c->img_cnt, cap));
+    TRY(dalloc(c, &c->img_off, (size_t)cap + 1));
     TRY(dalloc(c, &c->d_stage, (size_t)3 * cap));
     if (c->opt.rebuild_check) TRY(dalloc(c, &c->xbuild, cap));
     c->n_fblocks = c->n_tiles;   // one force CTA per tile
@@ -445,6 +453,9 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     TRY(dalloc(c, &c->xf, cap));
     TRY(dalloc(c, &c->slot_gid, cap));
     TRY(dalloc(c, &c->gflat, cap));
+    TRY(dalloc(c, &c->slot2t, cap));
+    TRY(dalloc(c, &c->img, cap));
+    TRY(dalloc(c, &c->grecv, cap));
     if (c->newton3 || c->dsl_on) {
         TRY(dalloc(c, &c->slot_t, cap));
         c->slot_t_valid = false;
@@ -507,6 +518,11 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     return LJMD_OK;
 }
 
+// the Newton-3 path moves particles in k_vv and refreshes every ghost slot per step instead
+Images images(ljmd_ctx* c) {
+    return c->newton3 ? Images{nullptr, nullptr} : Images{c->img_off, c->img};
+}
+
 ForceArgs force_args(ljmd_ctx* c) {
     ForceArgs a;
     const double s2 = c->sigma * c->sigma, s6 = s2 * s2 * s2, s12 = s6 * s6;
@@ -530,6 +546,7 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.pe_part = c->pe_part;
     a.ke_part = c->ke_part;
     a.xbuild = c->xbuild;
+    a.im = images(c);
     a.fl = c->d_fl;
     a.n_own = c->n_own;
     a.n_pad = c->n_pad;
@@ -774,6 +791,37 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
     return LJMD_OK;
 }
 
+// images of received halo planes, after each exchange (nranks > 1)
+ljmd_status refresh_recv(ljmd_ctx* c) {
+    if (c->n_grecv > 0) {
+        k_ghost_flat<<<nblk(c->n_grecv, 256), 256, 0, c->stream>>>(c->n_grecv, c->grecv, c->geo, c->x[c->xc]);
+        CKL();
+    }
+    return LJMD_OK;
+}
+
+// CSR of the ghost images of every owned particle (written by the kernels that move it) and
+// the list of received-plane images; from the build-time ghost list
+ljmd_status build_images(ljmd_ctx* c) {
+    if (c->newton3 || c->n_gflat == 0) {
+        CK(cudaMemsetAsync(c->img_off, 0, sizeof(int) * ((size_t)c->n_own + 1), c->stream));
+        return LJMD_OK;
+    }
+    k_slot2t<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->own_slot, c->slot2t);
+    CKL();
+    CK(cudaMemsetAsync(c->img_cnt, 0, sizeof(int) * (size_t)c->n_own, c->stream));
+    k_img_build<false><<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->n_slots, c->slot2t,
+                                                                     c->img_cnt, c->img_off, c->img, c->grecv,
+                                                                     c->d_fl);
+    CKL();
+    TRY(scan(c, c->img_cnt, c->n_own, c->img_off));
+    k_img_build<true><<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->n_slots, c->slot2t,
+                                                                    c->img_cnt, c->img_off, c->img, c->grecv,
+                                                                    c->d_fl);
+    CKL();
+    return LJMD_OK;
+}
+
 // Particle migration: leavers of the slab go to the adjacent rank; stayers and
 // arrivals are compacted into (xs, vs, gs), the input of the binning below.
 ljmd_status migrate(ljmd_ctx* c) {
@@ -919,12 +967,14 @@ ljmd_status rebuild(ljmd_ctx* c) {
     TRY(sync_flags(c));
     c->max_staged = c->h_fl->max_staged;
     c->n_gflat = c->h_fl->n_gflat;
+    TRY(build_images(c));
     if (16 * (size_t)(c->max_staged + 1) > kMaxStageSmem || c->max_staged > 65535)
         return set_err(c, LJMD_E_CAPACITY,
                        "a force tile needs %d staged particles (> %zu B of shared memory): density too high",
                        c->max_staged, kMaxStageSmem);
     TRY(launch_nlist(c));
     TRY(sync_flags(c));
+    c->n_grecv = c->h_fl->n_grecv;
     if (c->h_fl->overlap_gid != INT_MAX)
         return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)", c->h_fl->overlap_gid,
                        c->h_fl->overlap_gid_j);
@@ -1356,11 +1406,11 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         if (check)
             k_kick_drift<true><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
                 c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl);
+                c->dt, c->xbuild, c->d_fl, images(c), c->geo);
         else
             k_kick_drift<false><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
                 c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl);
+                c->dt, c->xbuild, c->d_fl, images(c), c->geo);
         CKL();
     }
     for (int64_t s = 1; s <= nsteps; ++s) {
@@ -1381,8 +1431,13 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
             ++c->n_rebuilds;
             c->rebuild_steps.push_back(c->steps_done);
         } else {
-            if (c->split) TRY(halo_exchange(c));
-            TRY(refresh_ghosts(c, false));
+            // ghost images of owned particles were written with the positions (force
+            // epilogue / kick-drift); received halo planes need theirs after the exchange
+            if (c->split) {
+                TRY(halo_exchange(c));
+                TRY(refresh_recv(c));
+            }
+            if (c->newton3) TRY(refresh_ghosts(c, false));
         }
         const bool sample = ee > 0 && (c->steps_done % ee) == 0;
         const bool last = s == nsteps;
@@ -1561,7 +1616,8 @@ void ljmd_destroy(ljmd_ctx* c) {
         if (p) cudaFree(p);
     dsl_destroy(c);
     for (void* p : {(void*)c->nbr8h, (void*)c->ncount_h, (void*)c->slot_t, (void*)c->tmap, (void*)c->tile_R,
-                    (void*)c->ld_pos, (void*)c->ld_vel, (void*)c->ld_gid, (void*)c->stay_t})
+                    (void*)c->ld_pos, (void*)c->ld_vel, (void*)c->ld_gid, (void*)c->stay_t, (void*)c->gflat,
+                    (void*)c->slot2t, (void*)c->img_cnt, (void*)c->img_off, (void*)c->img, (void*)c->grecv})
         if (p) cudaFree(p);
     void* ptrs2[] = {c->send_cnt, c->send_off, c->recv_cnt, c->recv_off, c->send_idx, c->send_buf, c->mig_send[0],
                      c->mig_send[1], c->mig_recv[0], c->mig_recv[1], c->mig_cnt, c->xs, c->vs, c->gs, c->iota};
