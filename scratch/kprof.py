@@ -7,11 +7,11 @@ import ljinputs as li
 from paper_1704_03329_b200 import LJMD, ljmd
 
 cycles = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-pos, box = li.fcc(64, 64, 64)
-vel = li.velocities(len(pos), 1.44)
+cfg = li.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "C2"]
+pos, vel, box = cfg.build()
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
-opts = ljmd.default_options(device=0, stream=s.cuda_stream)
+opts = ljmd.default_options(device=0, stream=s.cuda_stream, rebuild_check=cfg.rebuild_check)
 ctx = LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=opts)
 for _ in range(3):
     ctx.step(20)
@@ -32,7 +32,7 @@ for e in prof.key_averages():
     rows.append((t, e.count, e.key))
     tot += t
 tag = os.path.basename(os.environ.get("LJMD_LIB", "libljmd.so"))
-print(f"== {tag}: {tot / cycles:.1f} us per 20-step cycle")
+print(f"== {tag} {cfg.name}: {tot / cycles:.1f} us per 20-step cycle, rebuilds {ctx.stats()['n_rebuilds']}")
 for t, c, k in sorted(rows, reverse=True)[:14]:
     print(f"  {t / cycles:8.1f} us/cycle  {t / c:8.1f} us/launch  x{c // cycles:<3d} {k[:70]}")
 ctx.close()
