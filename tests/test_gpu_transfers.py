@@ -83,3 +83,21 @@ def test_staged_needs_single_rank(states):
               nccl_id=ljmd.local_group_id(uuid.uuid4().hex)) as ctx:
         with pytest.raises(ljmd.LjmdError, match="single rank"):
             ctx.stage_state_ptr(hp.data_ptr(), hv.data_ptr())
+
+
+def test_set_profile(states):
+    """ljmd_set_profile switches the per-launch force timing on and off between steps."""
+    from paper_1704_03329_b200 import LJMD, ljmd
+    pos0, vel0, box = states[0]
+    with LJMD(pos0, vel0, box, rc=li.RC, dt=li.DT, device=0) as ctx:
+        ctx.step(5)
+        s0 = ctx.stats()
+        assert s0["force_launches"] == 0 and s0["force_ms"] == 0.0
+        ctx.set_profile(True)
+        ctx.step(5)
+        s1 = ctx.stats()
+        assert s1["force_launches"] == 5 and s1["force_ms"] > 0.0
+        ctx.set_profile(False)
+        ctx.step(5)
+        assert ctx.stats()["force_launches"] == 5
+        assert ctx._lib.ljmd_set_profile(ctx._h, 2) == -1    # LJMD_E_ARG
