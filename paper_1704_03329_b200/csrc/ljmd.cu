@@ -571,7 +571,21 @@ constexpr size_t kStageBytes = 24;   // packed {x, y, z} per staged particle
 
 template <bool E, int M, bool C>
 void force_launch(ljmd_ctx* c, const ForceArgs& a) {
+#if LJMD_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)c->n_tiles);
+    cfg.blockDim = dim3(kForceThreads);
+    cfg.dynamicSmemBytes = kStageBytes * (size_t)(c->max_staged + 1);
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_force<E, M, C>, a);
+#else
     k_force<E, M, C><<<c->n_tiles, kForceThreads, kStageBytes * (size_t)(c->max_staged + 1), c->stream>>>(a);
+#endif
 }
 
 template <bool E, int M, bool C>
