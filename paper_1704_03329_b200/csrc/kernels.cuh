@@ -309,17 +309,29 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
     lex_xyz(g, g.lex_of_oc[oc], cx, cy, cz);
     int ec = ((cz + 1) * g.ey + (cy + 1)) * g.ex + (cx + 1);
     int sb = ebegin[ec];
-    for (int k = lane; k < m; k += 32) {
-        int t_old = perm[b + k];
-        int gk = gid_old[t_old];
-        const double xk = xw[t_old].x;
+    for (int k = lane; k < m + (m <= 32 ? 32 - m : 0); k += 32) {
+        // rank of member k by (x, gid); cells of <= 32 particles (all of them at liquid
+        // densities) exchange the keys by shuffles instead of re-reading them per member
+        const bool mine = k < m;
+        const int t_old = mine ? perm[b + k] : 0;
+        const int gk = mine ? gid_old[t_old] : 0;
+        const double xk = mine ? xw[t_old].x : 0.0;
         int r = 0;
-        for (int s = 0; s < m; ++s) {
-            const int ts = perm[b + s];
-            const double xs = xw[ts].x;
-            const int gs = gid_old[ts];
-            r += (xs < xk) || (xs == xk && gs < gk);
+        if (m <= 32) {
+            for (int s = 0; s < m; ++s) {
+                const double xs = __shfl_sync(0xffffffffu, xk, s);
+                const int gs = __shfl_sync(0xffffffffu, gk, s);
+                r += (xs < xk) || (xs == xk && gs < gk);
+            }
+        } else {
+            for (int s = 0; s < m; ++s) {
+                const int ts = perm[b + s];
+                const double xs = xw[ts].x;
+                const int gs = gid_old[ts];
+                r += (xs < xk) || (xs == xk && gs < gk);
+            }
         }
+        if (!mine) continue;
         int t = b + r;
         int slot = sb + r;
         double4 p = xw[t_old];
