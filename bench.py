@@ -193,6 +193,7 @@ def main():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-boa", action="store_true")
     ap.add_argument("--no-dsl", action="store_true")
+    ap.add_argument("--no-policy", action="store_true", help="skip the other rebuild policy's timing")
     ap.add_argument("--newton3", action="store_true",
                     help="NEXT-1 half-list force with reaction reductions (single GPU; slower)")
     args = ap.parse_args()
@@ -362,6 +363,30 @@ def main():
                "h2d_bytes_per_step": int(2 * 24 * n), "d2h_bytes_per_step": int(24 * n + 16),
                "steps": k_e2e, "transfers": "overlapped (copy stream)" if overlapped else "synchronous"}
 
+    # the other rebuild policy on the same workload (reading R7) -- the
+    # displacement-checked one when the headline ran the paper's fixed Ns = 20, and vice versa;
+    # a fresh context, W warm-up cycles, 10 timed cycles (not the headline number)
+    policy = None
+    if not args.no_policy and world == 1:
+        other = 0 if check else 1
+        o2 = ljmd.default_options(device=local, stream=stream.cuda_stream, rebuild_check=other)
+        with LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=o2) as c2:
+            for _ in range(args.warmup):
+                c2.step(MD_PER_STEP)
+            r0 = c2.stats()["n_rebuilds"]
+            torch.cuda.synchronize()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            kq = 10
+            q0.record(stream)
+            for _ in range(kq):
+                c2.step(MD_PER_STEP)
+            q1.record(stream)
+            torch.cuda.synchronize()
+            ms_q = q0.elapsed_time(q1)
+            policy = {"rebuild_policy": "safe" if other else "paper-fixed-20",
+                      "value": n * MD_PER_STEP * kq / (ms_q * 1e-3), "unit": UNIT,
+                      "rebuilds_per_20_steps": (c2.stats()["n_rebuilds"] - r0) / kq, "cycles": kq}
+
     # §8(f) NEXT-2 bond-order analysis on the same state (not part of the headline metric):
     # Q_6 with the first-shell cutoff 1.5 sigma, CUDA events around the call (kernel +
     # D2H of Q and |N(i)| + host scatter into caller order)
@@ -438,6 +463,7 @@ def main():
         "force_timing": {"region_steps": k_prof, "ms_per_step_with_events": ms_prof / k_prof},
         "neighbours_per_particle": cand / n,
         "e2e": e2e,
+        "other_rebuild_policy": policy,
         "cpu_baseline": cpu,
         "boa": boa,
         "dsl": dsl_info,
