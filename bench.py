@@ -152,6 +152,11 @@ def run_reference(args, cfg):
         return 0
     import oracle
     oracle.build()
+    full = cfg
+    if args.gpus > 1 and args.config is None:
+        # bounded sample: the oracle's cost per particle-step does not depend on N, so the
+        # weak-scaling workload (1,048,576 x N particles) is timed on one GPU's share (C2)
+        cfg = workload(1, None)
     pos, vel, box = cfg.build()
     n = len(pos)
     cores, model = cpu_info()
@@ -166,10 +171,12 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "md_steps_per_step": 1, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic FCC (ljinputs, seeded)",
-        "config": {"workload": cfg.name, "n_particles": n, "rho": li.RHO, "rc": li.RC,
-                   "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "dt": li.DT, "t0": cfg.t0},
+        "config": {"workload": full.name, "n_particles": full.n, "rho": li.RHO,
+                   "rc": li.RC, "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "dt": li.DT, "t0": cfg.t0},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"{cfg.name}: oracle list-mode VV, {args.steps} MD steps in one call "
+                         "sample": f"{cfg.name} (N={n}"
+                                   + (f", one GPU's share of {full.name}" if full is not cfg else "")
+                                   + f"): oracle list-mode VV, {args.steps} MD steps in one call "
                                    f"(init build + rebuilds every {li.NS}), 1 thread, {model}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "rebuilds": int(len(r.rebuild_steps)),
