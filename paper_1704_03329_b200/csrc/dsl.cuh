@@ -237,7 +237,7 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
              "  int* ljmd_sO = (int*)(ljmd_sP + 3 * ljmd_total);\n"
              "  for (int ljmd_r = 0; ljmd_r < ljmd_R; ++ljmd_r) {\n"
              "    const int ljmd_b0 = ljmd_rb[ljmd_r], ljmd_o0 = ljmd_ro[ljmd_r];\n"
-             "    const int ljmd_len = ljmd_ro[ljmd_r + 1] - ljmd_o0;\n"
+             "    const int ljmd_len = ljmd_p.tr_len[ljmd_tile * ljmd_p.rows_max + ljmd_r];\n"
              "    for (int ljmd_k = threadIdx.x; ljmd_k < ljmd_len; ljmd_k += blockDim.x) {\n"
              "      const double* ljmd_q = ljmd_p.x + 4 * (long long)(ljmd_b0 + ljmd_k);\n"
              "      ljmd_sP[3 * (ljmd_o0 + ljmd_k)] = ljmd_q[0];\n"
@@ -721,6 +721,7 @@ extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
     p.tile_oc0 = c->tile_oc0;
     p.tr_begin = c->tr_begin;
     p.tr_off = c->tr_off;
+    p.tr_len = c->tr_len;
     p.tile_R = c->tile_R;
     p.slot_t = c->slot_t;
     p.n_own = c->n_own;

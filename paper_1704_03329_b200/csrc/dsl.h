@@ -21,6 +21,7 @@ namespace ljmd {
     const int* tile_oc0;                                                                      \
     const int* tr_begin;                                                                      \
     const int* tr_off;                                                                        \
+    const int* tr_len;           /* true row lengths (rows are padded in the layout)  */     \
     const int* tile_R;                                                                        \
     const int* slot_t;           /* slot -> owned index (one rank); null: j by slot    */     \
     void* ptr[24];               /* argument k: data base pointer                     */     \

@@ -59,6 +59,13 @@ __device__ __forceinline__ void st256(double4* p, double4 v) {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};"
                  :: "l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
 }
+// packed positions (24 B per slot): what the force kernel's bulk copies stage
+__device__ __forceinline__ void st_packed(double* xp, int slot, double4 v) {
+    double* q = xp + 3 * (size_t)slot;
+    q[0] = v.x;
+    q[1] = v.y;
+    q[2] = v.z;
+}
 
 // Wrap into [0,L) -- reading R10; same operation sequence as the oracle's O1 (the
 // two are written independently).  IEEE division / explicit roundings, no FMA.
@@ -298,7 +305,8 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
                             double* __restrict__ vx_n, double* __restrict__ vy_n,
                             double* __restrict__ vz_n, int* __restrict__ gid_new,
                             int* __restrict__ own_slot, int* __restrict__ ocell_of,
-                            int* __restrict__ slot_gid, double4* __restrict__ xbuild) {
+                            int* __restrict__ slot_gid, double4* __restrict__ xbuild,
+                            double* __restrict__ xp_new) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= n_ocell) return;
@@ -336,6 +344,7 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
         int slot = sb + r;
         double4 p = xw[t_old];
         x_new[slot] = p;
+        st_packed(xp_new, slot, p);
         xf[slot] = make_float4((float)p.x, (float)p.y, (float)p.z, 0.f);
         if (xbuild) xbuild[t] = p;
         vx_n[t] = vx_o[t_old];
@@ -367,7 +376,7 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
                                 const int* __restrict__ ecount, Geo g, double4* __restrict__ x,
                                 float4* __restrict__ xf, int* __restrict__ slot_gid,
                                 const int* __restrict__ recv_cnt, const int* __restrict__ recv_off,
-                                int n_slots, int4* __restrict__ gflat, DevFlags* fl) {
+                                int n_slots, int4* __restrict__ gflat, double* __restrict__ xp, DevFlags* fl) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= gc.n) return;
@@ -393,6 +402,7 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
         double4 p = ld256(x + sb + k);
         double4 q = make_double4(__dadd_rn(p.x, Lx), __dadd_rn(p.y, Ly), __dadd_rn(p.z, Lz), 0.0);
         st256(x + db + k, q);
+        st_packed(xp, db + k, q);
         if (AT_BUILD) {
             xf[db + k] = make_float4((float)q.x, (float)q.y, (float)q.z, 0.f);
             slot_gid[db + k] = slot_gid[sb + k];
@@ -404,15 +414,17 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
 // Per-step ghost refresh: thread per ghost slot from the build-time list (one 16-byte
 // descriptor, one 32-byte read, one 32-byte write; every lane busy).
 __global__ void __launch_bounds__(256) k_ghost_flat(int n, const int4* __restrict__ gflat, Geo g,
-                                                    double4* __restrict__ x) {
+                                                    double4* __restrict__ x, double* __restrict__ xp) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int4 e = gflat[i];
     const double sx = (double)((e.z & 3) - 1), sy = (double)(((e.z >> 2) & 3) - 1),
                  sz = (double)(((e.z >> 4) & 3) - 1);
     const double4 p = ld256(x + e.y);
-    st256(x + e.x, make_double4(__dadd_rn(p.x, sx * g.L[0]), __dadd_rn(p.y, sy * g.L[1]),
-                                __dadd_rn(p.z, sz * g.L[2]), 0.0));
+    const double4 q = make_double4(__dadd_rn(p.x, sx * g.L[0]), __dadd_rn(p.y, sy * g.L[1]),
+                                   __dadd_rn(p.z, sz * g.L[2]), 0.0);
+    st256(x + e.x, q);
+    st_packed(xp, e.x, q);
 }
 
 // Ghost images per owned particle (CSR, built at the rebuild from the ghost list): the
@@ -426,14 +438,16 @@ struct Images {
 };
 
 __device__ __forceinline__ void write_images(const Images& im, int t, const Geo& g, double4* __restrict__ x,
-                                             double4 p) {
+                                             double* __restrict__ xp, double4 p) {
     if (!im.off) return;
     const int b = im.off[t], e = im.off[t + 1];
     for (int i = b; i < e; ++i) {
         const int2 d = im.e[i];
-        st256(x + d.x, make_double4(__dadd_rn(p.x, (double)((d.y & 3) - 1) * g.L[0]),
-                                    __dadd_rn(p.y, (double)(((d.y >> 2) & 3) - 1) * g.L[1]),
-                                    __dadd_rn(p.z, (double)(((d.y >> 4) & 3) - 1) * g.L[2]), 0.0));
+        const double4 q = make_double4(__dadd_rn(p.x, (double)((d.y & 3) - 1) * g.L[0]),
+                                       __dadd_rn(p.y, (double)(((d.y >> 2) & 3) - 1) * g.L[1]),
+                                       __dadd_rn(p.z, (double)(((d.y >> 4) & 3) - 1) * g.L[2]), 0.0);
+        st256(x + d.x, q);
+        st_packed(xp, d.x, q);
     }
 }
 
@@ -590,6 +604,7 @@ __global__ void k_unpack_gid(int n, const double4* __restrict__ xr, int* __restr
 struct TileRows {
     int* begin;   // [n_tiles][kRowsMax]
     int* off;     // [n_tiles][kRowsMax + 1]
+    int* len;     // [n_tiles][kRowsMax] true row lengths (rows are padded in the layout)
 };
 
 __global__ void k_tile_rows(int n_tiles, Geo g, const int* __restrict__ ebegin,
@@ -607,14 +622,21 @@ __global__ void k_tile_rows(int n_tiles, Geo g, const int* __restrict__ ebegin,
         beg = ebegin[e0];
         len = ebegin[e1] + ecount[e1] - beg;
     }
-    int x = len;
+    // padded rows: each starts at an offset of the same parity as its first slot (24-byte
+    // records then start 16-byte aligned in the packed positions and in shared memory up to
+    // the same 8-byte shift, as the bulk copy needs) and is followed by a spare record
+    const int plen = lane < T.R ? len + 2 : 0;
+    int x = plen;
     for (int o = 1; o < 32; o <<= 1) {
         int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
     if (lane < T.R) {
+        int o0 = x - plen;
+        o0 += (o0 ^ beg) & 1;
+        tr.len[tile * kRowsMax + lane] = len;
         tr.begin[tile * kRowsMax + lane] = beg;
-        tr.off[tile * (kRowsMax + 1) + lane] = x - len;
+        tr.off[tile * (kRowsMax + 1) + lane] = o0;
     }
     const int total = __shfl_sync(0xffffffffu, x, 31);
     if (lane == 0) {
@@ -683,7 +705,7 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
     for (int r = warp; r < T.R; r += kBuildThreads / 32) {
         const int b0 = __shfl_sync(0xffffffffu, rb, r);
         const int o0 = __shfl_sync(0xffffffffu, ro, r);
-        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
+        const int len = a.tr.len[tile * kRowsMax + r];
         for (int k = lane; k < len; k += 32) {
             const unsigned d = (unsigned)__cvta_generic_to_shared(sF + o0 + k);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" :: "r"(d), "l"(a.xf + b0 + k) : "memory");
@@ -916,6 +938,8 @@ struct ForceArgs {
     Geo g;
     const double4* x;        // current positions (slot space)
     double4* x_next;         // kKKD output buffer (slot space)
+    const double* xp;        // packed {x, y, z} per slot (24 B) of the current positions
+    double* xp_next;         // kKKD: packed x(n+1)
     const int* own_slot;
     const uint4* nbr;        // blocks of 8 16-bit local indices: nbr[b * n_pad + t]
     const int* ncount;
@@ -1114,7 +1138,8 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
                                             __dadd_rn(xi.y, __dmul_rn(a.dt, vy)),
                                             __dadd_rn(xi.z, __dmul_rn(a.dt, vz)), 0.0);
             st256(a.x_next + P.si, xn);
-            write_images(a.im, t, a.g, a.x_next, xn);
+            st_packed(a.xp_next, P.si, xn);
+            write_images(a.im, t, a.g, a.x_next, a.xp_next, xn);
             if (CHECK) {
                 const double4 bb = a.xbuild[t];
                 // non-negative doubles order like their bit patterns
@@ -1172,25 +1197,44 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
     const int total = __shfl_sync(0xffffffffu, ro, T.R);
     double* sP = reinterpret_cast<double*>(smem);   // packed {x, y, z} per staged particle
-    for (int r = warp; r < T.R; r += kForceThreads / 32) {
-        const int b0 = __shfl_sync(0xffffffffu, rb, r);
-        const int o0 = __shfl_sync(0xffffffffu, ro, r);
-        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
-        for (int k = lane; k < len; k += 32) {
-            const double* src = reinterpret_cast<const double*>(a.x + b0 + k);
-            double* dst = sP + 3 * (o0 + k);
-            cp_async8(dst, src);
-            cp_async8(dst + 1, src + 1);
-            cp_async8(dst + 2, src + 2);
-        }
-    }
-    if (threadIdx.x == 0) {   // sentinel (list padding): far away, contributes exactly 0
-        sP[3 * total] = 1e30;
+    // one bulk copy per halo row (TMA engine), issued by warp 0, completion on an mbarrier
+    __shared__ __align__(8) unsigned long long mbar;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sP[3 * total] = 1e30;   // sentinel (list padding): far away, contributes exactly 0
         sP[3 * total + 1] = 1e30;
         sP[3 * total + 2] = 1e30;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    if (warp == 0) {
+        unsigned sz = 0u;
+        unsigned long long src = 0ull;
+        unsigned dst = 0u;
+        if (lane < T.R) {
+            const int len = a.tr.len[tile * kRowsMax + lane];
+            const unsigned d = (unsigned)(rb & 1) * 8u;
+            src = reinterpret_cast<unsigned long long>(a.xp + 3 * (size_t)rb) - d;
+            dst = (unsigned)__cvta_generic_to_shared(sP + 3 * ro) - d;
+            sz = (24u * (unsigned)len + d + 15u) & ~15u;
+        }
+        unsigned tot = sz;
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(tot) : "memory");
+        __syncwarp();
+        if (sz)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         :: "r"(dst), "l"(src), "r"(sz), "r"(mb) : "memory");
+    }
+    {
+        unsigned done = 0u;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(mb) : "memory");
+    }
+
     const char* sPb = reinterpret_cast<const char*>(sP);
     double epart = 0.0, ke = 0.0;
     unsigned long long dbits = 0ull;
@@ -1222,7 +1266,8 @@ __global__ void k_kick_drift(int n_own, double4* __restrict__ x, const int* __re
                              double* __restrict__ vx, double* __restrict__ vy, double* __restrict__ vz,
                              const double* __restrict__ fx, const double* __restrict__ fy,
                              const double* __restrict__ fz, double h, double dt,
-                             const double4* __restrict__ xbuild, DevFlags* fl, Images im, Geo g) {
+                             const double4* __restrict__ xbuild, DevFlags* fl, Images im, Geo g,
+                             double* __restrict__ xp) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long bits = 0ull;
     if (t < n_own) {
@@ -1235,7 +1280,8 @@ __global__ void k_kick_drift(int n_own, double4* __restrict__ x, const int* __re
         p.y = __dadd_rn(p.y, __dmul_rn(dt, b));
         p.z = __dadd_rn(p.z, __dmul_rn(dt, c));
         x[si] = p;
-        write_images(im, t, g, x, p);
+        st_packed(xp, si, p);
+        write_images(im, t, g, x, xp, p);
         vx[t] = a; vy[t] = b; vz[t] = c;
         if (CHECK) {
             double4 q = xbuild[t];
@@ -1382,7 +1428,7 @@ __global__ void __launch_bounds__(kForceThreads) k_boa(BoaArgs a) {
     for (int r = warp; r < T.R; r += kForceThreads / 32) {
         const int b0 = __shfl_sync(0xffffffffu, rb, r);
         const int o0 = __shfl_sync(0xffffffffu, ro, r);
-        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
+        const int len = a.tr.len[tile * kRowsMax + r];
         for (int k = lane; k < len; k += 32) {
             const double4 p = ld256(a.x + b0 + k);
             sP[3 * (o0 + k)] = p.x;
@@ -1700,7 +1746,7 @@ __global__ void __launch_bounds__(kForceThreads, 3) k_force_half(HalfArgs a) {
     for (int r = warp; r < T.R; r += kForceThreads / 32) {
         const int b0 = __shfl_sync(0xffffffffu, rb, r);
         const int o0 = __shfl_sync(0xffffffffu, ro, r);
-        const int len = __shfl_sync(0xffffffffu, ro, r + 1) - o0;
+        const int len = a.tr.len[tile * kRowsMax + r];
         for (int k = lane; k < len; k += 32) {
             const double4 p = a.x[b0 + k];
             sP[3 * (o0 + k)] = p.x;

@@ -97,6 +97,8 @@ struct ljmd_ctx {
     float* ylo_f = nullptr;           // fp32 cell faces (list-build pruning)
     float* zlo_f = nullptr;
     int* tr_off = nullptr;
+    int* tr_len = nullptr;
+    double* xp[2] = {nullptr, nullptr};   // packed {x, y, z} per slot, kept with x[2] (force staging)
     int* scan_tmp = nullptr;
     int scan_tmp_n = 0;
     // ---- list
@@ -331,6 +333,7 @@ ljmd_status plan_geometry(ljmd_ctx* c, const double box[3]) {
     TRY(dalloc(c, &c->tile_oc0, c->n_tiles + 1));
     TRY(dalloc(c, &c->tr_begin, (size_t)c->n_tiles * kRowsMax));
     TRY(dalloc(c, &c->tr_off, (size_t)c->n_tiles * (kRowsMax + 1)));
+    TRY(dalloc(c, &c->tr_len, (size_t)c->n_tiles * kRowsMax));
     CK(cudaMemcpy(c->oc_of_lex, oc_of_lex.data(), sizeof(int) * c->n_ocell, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->lex_of_oc, lex_of_oc.data(), sizeof(int) * c->n_ocell, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->tile_oc0, tile_oc0.data(), sizeof(int) * (c->n_tiles + 1), cudaMemcpyHostToDevice));
@@ -453,6 +456,7 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     TRY(dalloc(c, &c->xf, cap));
     TRY(dalloc(c, &c->slot_gid, cap));
     TRY(dalloc(c, &c->gflat, cap));
+    for (int b = 0; b < 2; ++b) TRY(dalloc(c, &c->xp[b], (size_t)3 * cap + 8));   // +8: bulk-copy overrun
     TRY(dalloc(c, &c->slot2t, cap));
     TRY(dalloc(c, &c->img, cap));
     TRY(dalloc(c, &c->grecv, cap));
@@ -482,7 +486,7 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     a.ocount = c->ocount;
     a.ebegin = c->ebegin;
     a.ecount = c->ecount;
-    a.tr = TileRows{c->tr_begin, c->tr_off};
+    a.tr = TileRows{c->tr_begin, c->tr_off, c->tr_len};
     a.nbr8 = c->nbr8;
     a.ncount = c->ncount;
     a.n_own = c->n_own;
@@ -529,9 +533,11 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.g = c->geo;
     a.obegin = c->obegin;
     a.tile_oc0 = c->tile_oc0;
-    a.tr = TileRows{c->tr_begin, c->tr_off};
+    a.tr = TileRows{c->tr_begin, c->tr_off, c->tr_len};
     a.x = c->x[c->xc];
     a.x_next = c->x[c->xc ^ 1];
+    a.xp = c->xp[c->xc];
+    a.xp_next = c->xp[c->xc ^ 1];
     a.own_slot = c->own_slot;
     a.nbr = c->bank_order ? c->nbr8b : c->nbr8;
     a.ncount = c->ncount;
@@ -638,7 +644,7 @@ ljmd_status launch_half(ljmd_ctx* c, bool energy, int mode, bool check, cudaEven
     h.obegin = c->obegin;
     h.tile_oc0 = c->tile_oc0;
     h.slot_t = c->slot_t;
-    h.tr = TileRows{c->tr_begin, c->tr_off};
+    h.tr = TileRows{c->tr_begin, c->tr_off, c->tr_len};
     h.fx = c->F;
     h.fy = c->F + oc;
     h.fz = c->F + 2 * oc;
@@ -798,9 +804,10 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
     if (at_build)
         k_ghost_refresh<true><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo, c->x[c->xc],
                                                              c->xf, c->slot_gid, c->recv_cnt, c->recv_off,
-                                                             c->n_slots, c->gflat, c->d_fl);
+                                                             c->n_slots, c->gflat, c->xp[c->xc], c->d_fl);
     else if (c->n_gflat > 0)
-        k_ghost_flat<<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->geo, c->x[c->xc]);
+        k_ghost_flat<<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->geo, c->x[c->xc],
+                                                                    c->xp[c->xc]);
     CKL();
     return LJMD_OK;
 }
@@ -808,7 +815,8 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
 // images of received halo planes, after each exchange (nranks > 1)
 ljmd_status refresh_recv(ljmd_ctx* c) {
     if (c->n_grecv > 0) {
-        k_ghost_flat<<<nblk(c->n_grecv, 256), 256, 0, c->stream>>>(c->n_grecv, c->grecv, c->geo, c->x[c->xc]);
+        k_ghost_flat<<<nblk(c->n_grecv, 256), 256, 0, c->stream>>>(c->n_grecv, c->grecv, c->geo, c->x[c->xc],
+                                                                    c->xp[c->xc]);
         CKL();
     }
     return LJMD_OK;
@@ -957,7 +965,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
         c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, gid_old, c->xw, vo, vo + oc, vo + 2 * oc,
         xn, c->xf, vn, vn + oc, vn + 2 * oc, c->gid[on], c->own_slot, c->ocell_of, c->slot_gid,
-        c->opt.rebuild_check ? c->xbuild : nullptr);
+        c->opt.rebuild_check ? c->xbuild : nullptr, c->xp[c->xc ^ 1]);
     CKL();
     c->oc_cur = on;
     c->xc ^= 1;
@@ -976,7 +984,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     }
     TRY(refresh_ghosts(c, true));
     k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
-        c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off}, c->d_fl);
+        c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl);
     CKL();
     TRY(sync_flags(c));
     c->max_staged = c->h_fl->max_staged;
@@ -1009,7 +1017,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
         k_slot_owner<<<nblk(c->n_slots, 256), 256, 0, c->stream>>>(c->n_slots, c->slot_gid, c->tmap, c->slot_t);
         CKL();
         k_list_half<<<nblk(c->n_own, 128), 128, 0, c->stream>>>(c->n_own, c->n_pad, c->geo, c->nbr8, c->ncount,
-                                                                 c->ocell_of, TileRows{c->tr_begin, c->tr_off},
+                                                                 c->ocell_of, TileRows{c->tr_begin, c->tr_off, c->tr_len},
                                                                  c->slot_gid, g, c->nbr8h, c->ncount_h);
         CKL();
     } else if (c->bank_order) {
@@ -1420,11 +1428,11 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         if (check)
             k_kick_drift<true><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
                 c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl, images(c), c->geo);
+                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc]);
         else
             k_kick_drift<false><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
                 c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl, images(c), c->geo);
+                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc]);
         CKL();
     }
     for (int64_t s = 1; s <= nsteps; ++s) {
@@ -1572,7 +1580,7 @@ ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, in
     CK(cudaMemcpyAsync(d_off, toff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, c->stream));
     k_list_gids<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->n_pad, c->geo, (const unsigned short*)c->nbr8,
                                                      c->ncount, c->ocell_of,
-                                                     TileRows{c->tr_begin, c->tr_off}, c->slot_gid, d_off, d_out);
+                                                     TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->slot_gid, d_off, d_out);
     CKL();
     std::vector<long long> h((size_t)toff[n]);
     CK(cudaMemcpyAsync(h.data(), d_out, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, c->stream));
@@ -1631,7 +1639,8 @@ void ljmd_destroy(ljmd_ctx* c) {
     dsl_destroy(c);
     for (void* p : {(void*)c->nbr8h, (void*)c->ncount_h, (void*)c->slot_t, (void*)c->tmap, (void*)c->tile_R,
                     (void*)c->ld_pos, (void*)c->ld_vel, (void*)c->ld_gid, (void*)c->stay_t, (void*)c->gflat,
-                    (void*)c->slot2t, (void*)c->img_cnt, (void*)c->img_off, (void*)c->img, (void*)c->grecv})
+                    (void*)c->slot2t, (void*)c->img_cnt, (void*)c->img_off, (void*)c->img, (void*)c->grecv,
+                    (void*)c->xp[0], (void*)c->xp[1], (void*)c->tr_len})
         if (p) cudaFree(p);
     void* ptrs2[] = {c->send_cnt, c->send_off, c->recv_cnt, c->recv_off, c->send_idx, c->send_buf, c->mig_send[0],
                      c->mig_send[1], c->mig_recv[0], c->mig_recv[1], c->mig_cnt, c->xs, c->vs, c->gs, c->iota};
@@ -1682,7 +1691,7 @@ extern "C" ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q
     a.ncount = c->ncount;
     a.obegin = c->obegin;
     a.tile_oc0 = c->tile_oc0;
-    a.tr = TileRows{c->tr_begin, c->tr_off};
+    a.tr = TileRows{c->tr_begin, c->tr_off, c->tr_len};
     a.Q = c->d_stage;
     a.nnb = c->d_stage + c->own_cap;
     a.n_own = c->n_own;
@@ -1763,7 +1772,7 @@ extern "C" ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t*
     a.ocell_of = c->ocell_of;
     a.slot_gid = c->slot_gid;
     a.gid = c->gid[c->oc_cur];
-    a.tr = TileRows{c->tr_begin, c->tr_off};
+    a.tr = TileRows{c->tr_begin, c->tr_off, c->tr_len};
     a.tab = tab;
     a.tcnt = tcnt;
     a.tmap = tmap;
