@@ -1050,10 +1050,6 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" :: "l"(p) : "memory");   // pinned: no sinking
 }
 
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(gsrc) : "memory");
-}
 
 // Per-particle state loaded before the tile is staged (hides the list/position latency).
 struct FPart {
@@ -1157,9 +1153,10 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
 }
 
 // One CTA per tile.  (1) Each thread issues the global loads of its particle (slot, count,
-// first index block, position); (2) the warps copy the tile's halo rows -- x, y, z of every
-// particle any of its particles can list -- into shared memory with cp.async (LDGSTS, no
-// register round trip), packed 24 B per particle plus a far-away sentinel for list padding;
+// first index block, position); (2) warp 0 copies the tile's halo rows -- x, y, z of every
+// particle any of its particles can list -- into shared memory with one TMA bulk copy per
+// row from the packed positions (24 B per particle), plus a far-away sentinel for list
+// padding;
 // (3) thread per particle over its list of 16-bit local indices: each neighbour is three
 // LDS.64 from one address (bank group = 3 l mod 16, spread across a half-warp by the
 // bank-aware list order) instead of a scattered 32 B global gather.
