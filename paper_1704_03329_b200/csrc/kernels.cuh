@@ -1171,6 +1171,23 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
     const bool has = (int)threadIdx.x < m;
     FPart P;
+    // halo rows of this tile: lane r holds (begin, offset, length) of row r -- tables of the
+    // rebuild, read before waiting for the previous launch
+    const int rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
+    const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
+    const int rl = lane < T.R ? a.tr.len[tile * kRowsMax + lane] : 0;
+    const int total = __shfl_sync(0xffffffffu, ro, T.R);
+    double* sP = reinterpret_cast<double*>(smem);   // packed {x, y, z} per staged particle
+    // one bulk copy per halo row (TMA engine), issued by warp 0, completion on an mbarrier
+    __shared__ __align__(8) unsigned long long mbar;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sP[3 * total] = 1e30;   // sentinel (list padding): far away, contributes exactly 0
+        sP[3 * total + 1] = 1e30;
+        sP[3 * total + 2] = 1e30;
+    }
 #if LJMD_PDL
     // programmatic dependent launch: the next force launch may start its CTAs on SMs this
     // one frees, loading the list indices (not written by this kernel) before it waits for
@@ -1185,36 +1202,16 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         if (P.cnt > 8) prefetch_l1(a.nbr + (size_t)a.n_pad + t);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (has) P.xi = ld256(a.x + P.si);
-#else
-    if (has) P = fpart_load(a, t0 + threadIdx.x);
 #endif
-    // halo rows of this tile: lane r holds (begin, offset) of row r
-    const int rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
-    const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
-    const int total = __shfl_sync(0xffffffffu, ro, T.R);
-    double* sP = reinterpret_cast<double*>(smem);   // packed {x, y, z} per staged particle
-    // one bulk copy per halo row (TMA engine), issued by warp 0, completion on an mbarrier
-    __shared__ __align__(8) unsigned long long mbar;
-    const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        sP[3 * total] = 1e30;   // sentinel (list padding): far away, contributes exactly 0
-        sP[3 * total + 1] = 1e30;
-        sP[3 * total + 2] = 1e30;
-    }
-    __syncthreads();
-    if (warp == 0) {
+    if (warp == 0) {   // the copies go out as soon as the positions may be read
         unsigned sz = 0u;
         unsigned long long src = 0ull;
         unsigned dst = 0u;
         if (lane < T.R) {
-            const int len = a.tr.len[tile * kRowsMax + lane];
             const unsigned d = (unsigned)(rb & 1) * 8u;
             src = reinterpret_cast<unsigned long long>(a.xp + 3 * (size_t)rb) - d;
             dst = (unsigned)__cvta_generic_to_shared(sP + 3 * ro) - d;
-            sz = (24u * (unsigned)len + d + 15u) & ~15u;
+            sz = (24u * (unsigned)rl + d + 15u) & ~15u;
         }
         unsigned tot = sz;
         for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
@@ -1225,6 +1222,12 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                          :: "r"(dst), "l"(src), "r"(sz), "r"(mb) : "memory");
     }
+#if LJMD_PDL
+    if (has) P.xi = ld256(a.x + P.si);
+#else
+    if (has) P = fpart_load(a, t0 + threadIdx.x);
+#endif
+    __syncthreads();   // the barrier's initialisation and the sentinel are visible
     {
         unsigned done = 0u;
         while (!done)
