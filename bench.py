@@ -269,13 +269,23 @@ def main():
     clk = (None, None) if args.no_clocks else clocks_start(clk_path)
     time.sleep(0.3 if clk[0] is not None else 0.0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # also the spread over 5 equal parts of the timed region (events between
+    # ljmd_step calls, which end with a host synchronisation anyway)
+    n_rep = 5 if args.steps >= 5 else 1
+    cuts = sorted({round(i * args.steps / n_rep) for i in range(1, n_rep)})
+    evs = {k: torch.cuda.Event(enable_timing=True) for k in cuts}
     barrier()
     ev0.record(stream)
-    for _ in range(args.steps):
+    for k in range(args.steps):
+        if k in evs:
+            evs[k].record(stream)
         ctx.step(MD_PER_STEP)
     ev1.record(stream)
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
+    marks = [(0, ev0)] + [(k, evs[k]) for k in cuts] + [(args.steps, ev1)]
+    part_rates = [n * MD_PER_STEP * (k1 - k0) / (a.elapsed_time(b) * 1e-3)
+                  for (k0, a), (k1, b) in zip(marks, marks[1:]) if k1 > k0]
     clocks = clocks_stop(clk, clk_path, local) if clk[0] is not None else None
     st1 = ctx.stats()
     md_steps = args.steps * MD_PER_STEP
@@ -466,6 +476,8 @@ def main():
                      "traffic_source": traffic_src,
                      "flops_per_launch": flops, "avg_launch_ms": f_ms, "peak_source": peak_src,
                      "flop_count": "Listing 9: 21 flops per list candidate (+5 with PE every 10th step)"},
+        "repeats": {"parts": len(part_rates), "median": statistics.median(part_rates), "min": min(part_rates),
+                    "max": max(part_rates), "unit": UNIT, "note": "rank-0 rates of equal parts of the timed region"},
         "force_share": (sp1["force_ms"] - sp0["force_ms"]) / ms_prof,
         "force_timing": {"region_steps": k_prof, "ms_per_step_with_events": ms_prof / k_prof},
         "neighbours_per_particle": cand / n,
