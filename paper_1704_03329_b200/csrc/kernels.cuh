@@ -1,16 +1,20 @@
 // kernels.cuh -- sm_100a kernels of the LJ PairLoop hot path (arXiv 1704.03329).
 //
-// Data layout in HBM (DESIGN.md "Data layout"):
-//   slot space  : every particle image the list can reference -- owned particles and
-//                 ghosts (periodic images / halo copies) -- sorted by EXTENDED cell
-//                 (x fastest over ncx+2, then y over ncy+2, then z over nzl+2), within a
-//                 cell by gid.  A 3-cell x-row of the 27-cell stencil is therefore one
-//                 contiguous slot range.  Positions: double4 {x,y,z,0} (32 B, one sector,
-//                 one 256-bit LDG per neighbour); fp32 mirror float4 for the list build.
-//   owned space : owned particles t = 0..n_own-1 in owned-cell order (same order as their
-//                 slots); v (SoA), F (SoA), gid, own_slot[t], e_i.
-//   list        : ELL, row-major nbr[t * K + k] (int32 slot), ncount[t]; a team of T lanes
-//                 reads k..k+T-1 of one particle (coalesced, spatially coherent gathers).
+// Data layout in HBM (DESIGN.md §5):
+//   slot space  : every particle image a list can reference -- owned particles and ghosts
+//                 (periodic images / halo copies) -- sorted by EXTENDED cell (x fastest
+//                 over ncx+2, then y over ncy+2, then z over nzl+2), within a cell by
+//                 (x, gid): a 3-cell x-row of the 27-cell stencil is one contiguous,
+//                 x-sorted slot range.  Positions double4 {x,y,z,0} (x[2], double-buffered),
+//                 a packed 24-byte copy xp[2] (the force kernel's bulk-copy source) and an
+//                 fp32 float4 mirror for the list build.
+//   owned space : owned particles t = 0..n_own-1, tile-major (one force CTA's particles
+//                 are contiguous); v, F SoA fp64, gid, own_slot[t], e_i, ghost-image CSR.
+//   tile halo   : per force tile the (ty+2)(tz+2) halo x-rows as slot ranges with padded
+//                 offsets into the tile's shared-memory staging buffer (tr_begin/off/len).
+//   list        : 16-bit local indices into that staging buffer, blocks of 8 entries,
+//                 nbr8[b * n_pad + t] (one 16-byte load per 8 neighbours), ncount[t];
+//                 a short last block is padded with the tile's sentinel.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
