@@ -141,6 +141,36 @@ def test_random_uniform_box(eng, orc):
         check_forces(ctx, orc, x, box, 0.25)
 
 
+def test_dilute_gas_empty_cells(eng, orc):
+    """A dilute gas (rho ~ 0.02): most cells, and whole halo rows of the force tiles, are
+    empty -- zero-length rows in the staging layout and bulk copies -- and a few clusters
+    are dense; lists and forces at init and after 30 steps (one rebuild) against brute
+    force."""
+    box = np.array([22.0, 24.5, 27.0])
+    rng = np.random.default_rng(5)
+    pos = li.uniform_random(240, box, seed=13, min_sep=0.9)
+    # a few dense clusters so that some tiles are populated while most rows are empty
+    c = pos[:6]
+    extra = (c[:, None, :] + rng.normal(0, 0.6, (6, 12, 3))).reshape(-1, 3)
+    allp = np.concatenate([pos, extra])
+    keep = [0]
+    for i in range(1, len(allp)):   # keep a minimum separation (no overlapping particles)
+        d = allp[keep] - allp[i]
+        d -= box * np.round(d / box)
+        if np.min(np.sum(d * d, axis=1)) > 0.81:
+            keep.append(i)
+    pos = allp[keep]
+    vel = li.velocities(len(pos), 1.0)
+    with eng.LJMD(pos, vel, box) as ctx:
+        x = ctx.positions()
+        off, nbr = ctx.neighbours()
+        assert gid_pairs(off, nbr) == gid_pairs(*orc.neighbours(x, box, RN, "brute"))
+        check_forces(ctx, orc, x, box, 0.25)
+        ctx.step(30)
+        x = ctx.positions()
+        check_forces(ctx, orc, orc.wrap(x, box), box, 0.25)
+
+
 # ------------------------------------------------------------------------------ stepping
 
 def test_one_step_forces(eng, orc):
