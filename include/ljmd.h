@@ -71,9 +71,12 @@ typedef struct {
                                every rank (broadcast by the caller, e.g. torch.distributed) */
     void*   stream;         /* cudaStream_t to launch on; NULL = library-created stream    */
     int64_t profile;        /* 1: time every force launch with CUDA events (ljmd_get_stats) */
-    int64_t list_order;     /* 1 (default): bank-aware neighbour order (fastest); 0: build order
-                               (stencil row, slot) -- results then do not depend on the number
-                               of slabs (bitwise), at ~15 % more force-kernel time          */
+    int64_t list_order;     /* 1 (default): bank-aware neighbour order (fastest) for lists
+                               expected to serve >= 10 steps (always with the fixed Ns = 20;
+                               with rebuild_check as long as recent lists lasted that long),
+                               build order otherwise; 0: always the build order (stencil
+                               row, slot) -- results then do not depend on the number of
+                               slabs (bitwise), at ~13 % more force-kernel time             */
     int64_t split_self;     /* 1: with nranks = 1, still run the slab-exchange path (halo
                                planes sent to itself through the transport; testing)        */
     int64_t newton3;        /* 1: Newton-3 half list: each pair

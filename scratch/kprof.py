@@ -11,7 +11,8 @@ cfg = li.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "C2"]
 pos, vel, box = cfg.build()
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
-opts = ljmd.default_options(device=0, stream=s.cuda_stream, rebuild_check=cfg.rebuild_check)
+opts = ljmd.default_options(device=0, stream=s.cuda_stream, rebuild_check=cfg.rebuild_check,
+                            list_order=int(os.environ.get("LJMD_LIST_ORDER", "1")))
 ctx = LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=opts)
 for _ in range(3):
     ctx.step(20)
