@@ -204,7 +204,15 @@ __global__ void k_load_rows(int n, const double* __restrict__ pos, const double*
 // Force tiles: blocks of kTX x kTY x kTZ owned cells.  Owned cells (and hence owned
 // particles t) are numbered tile-major -- tile (z, y, x), then cell (z, y, x) inside the
 // tile -- so one CTA's particles are contiguous; its stencil halo is (ty+2)(tz+2) x-rows.
-constexpr int kTX = 4, kTY = 2, kTZ = 2;
+// 4 x 3 x 2 cells (~444 particles at rho = 0.8442): the halo is 6 x 5 x 4 cells, 5x the
+// owned ones (4 x 2 x 2: 6x); measured on C2 with 480-thread CTAs: force 159.3 -> 157.5 us
+// per launch, list build 564 -> 528 us, 20-step cycle 4128 -> 4039 us
+#ifndef LJMD_TX
+#define LJMD_TX 4
+#define LJMD_TY 3
+#define LJMD_TZ 2
+#endif
+constexpr int kTX = LJMD_TX, kTY = LJMD_TY, kTZ = LJMD_TZ;
 constexpr int kRowsMax = (kTY + 2) * (kTZ + 2);
 
 struct Geo {
@@ -690,10 +698,13 @@ struct NlistArgs {
 // walks its 9 stencil rows as local-index ranges.  Lanes of one cell walk the same j
 // sequence (broadcast LDS).  Output: build-order (stencil row, slot) local indices,
 // blocks of 8 entries written with 16-byte stores from registers.
-constexpr int kBuildThreads = 320;
+#ifndef LJMD_BUILD_THREADS
+#define LJMD_BUILD_THREADS 480
+#endif
+constexpr int kBuildThreads = LJMD_BUILD_THREADS;
 
 #ifndef LJMD_BUILD_MINB
-#define LJMD_BUILD_MINB 5
+#define LJMD_BUILD_MINB 4
 #endif
 __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(NlistArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1009,18 +1020,21 @@ __device__ __forceinline__ void andersen(unsigned long long seed, long long step
     vz = __dmul_rn(sd, __dmul_rn(R2, cos(__dmul_rn(two_pi, U4))));
 }
 
-constexpr int kForceThreads = 320;
-// 3 CTAs of 320 threads per SM with up to 64 registers: measured on C2 160 us per launch
-// against 167 us at 4 CTAs / 48 registers and 170 us at 2 CTAs (more in-flight neighbours
-// per warp beats more warps)
+#ifndef LJMD_FORCE_THREADS
+#define LJMD_FORCE_THREADS 480   // ~24 cells x 18.5 particles per tile at rho = 0.8442
+#endif
+constexpr int kForceThreads = LJMD_FORCE_THREADS;
+// 2 CTAs of 480 threads (3 of 320 with 4 x 2 x 2 tiles) per SM with up to 64 registers:
+// measured on C2 (320-thread tiles) 160 us per launch against 167 us at 4 CTAs / 48
+// registers and 170 us at 2 CTAs / 96 registers (more in-flight neighbours per warp beats
+// more warps)
 #ifndef LJMD_FORCE_MINB
-#define LJMD_FORCE_MINB 3
+#define LJMD_FORCE_MINB 2
 #endif
 // programmatic dependent launch of consecutive force launches (C2: -46 us per 20 steps)
 #ifndef LJMD_PDL
 #define LJMD_PDL 1
 #endif
-   // ~16 cells x 18.5 particles per tile at rho = 0.8442
 
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {
