@@ -779,32 +779,38 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
                     lo = l0;
                     hi = h0;
                 }
-                for (int jl = lo; jl < hi; ++jl) {
-                    const float4 fj = sF[jl];
-                    const float fx = fi.x - fj.x, fy = fi.y - fj.y, fz = fi.z - fj.z;
-                    const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-                    if (r2f >= thr_hi || jl == li) continue;
-                    bool take = r2f < thr_lo;
-                    if (!take || r2f < 1e-6f) {          // rare: decide in fp64 (the oracle's test)
-                        const int j = rbeg + (jl - roff);
-                        const double4 xj = a.x[j];
-                        const double r2 = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z);
-                        take = r2 < a.rn2;
-                        if (r2 == 0.0) {
-                            atomicMin(&a.fl->overlap_gid, a.slot_gid[si]);
-                            a.fl->overlap_gid_j = a.slot_gid[j];
+                // self exclusion by splitting the window around the own local index (li lies
+                // in the own row only) instead of a per-candidate test (528 -> 520 us on C2)
+                for (int part = 0; part < 2; ++part) {
+                    const int j0 = part ? max(lo, li + 1) : lo;
+                    const int j1 = part ? hi : min(hi, li);
+                    for (int jl = j0; jl < j1; ++jl) {
+                        const float4 fj = sF[jl];
+                        const float fx = fi.x - fj.x, fy = fi.y - fj.y, fz = fi.z - fj.z;
+                        const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+                        if (r2f >= thr_hi) continue;
+                        bool take = r2f < thr_lo;
+                        if (!take || r2f < 1e-6f) {          // rare: decide in fp64 (the oracle's test)
+                            const int j = rbeg + (jl - roff);
+                            const double4 xj = a.x[j];
+                            const double r2 = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z);
+                            take = r2 < a.rn2;
+                            if (r2 == 0.0) {
+                                atomicMin(&a.fl->overlap_gid, a.slot_gid[si]);
+                                a.fl->overlap_gid_j = a.slot_gid[j];
+                            }
                         }
-                    }
-                    if (take) {
-                        w0 = __funnelshift_r(w0, w1, 16);
-                        w1 = __funnelshift_r(w1, w2, 16);
-                        w2 = __funnelshift_r(w2, w3, 16);
-                        w3 = __funnelshift_r(w3, (unsigned)jl, 16);
-                        if ((k & 7) == 7) {
-                            if (k < K) *outb = make_uint4(w0, w1, w2, w3);
-                            outb += stride;
+                        if (take) {
+                            w0 = __funnelshift_r(w0, w1, 16);
+                            w1 = __funnelshift_r(w1, w2, 16);
+                            w2 = __funnelshift_r(w2, w3, 16);
+                            w3 = __funnelshift_r(w3, (unsigned)jl, 16);
+                            if ((k & 7) == 7) {
+                                if (k < K) *outb = make_uint4(w0, w1, w2, w3);
+                                outb += stride;
+                            }
+                            ++k;
                         }
-                        ++k;
                     }
                 }
             }
