@@ -274,6 +274,23 @@ def test_capacity_regrow(eng, orc):
         check_forces(ctx, orc, ctx.positions(), box, 0.25)
 
 
+def test_dense_liquid(eng, orc):
+    """rho = 1.2: ~630 particles per 4 x 3 x 2-cell force tile, more than one CTA's 480
+    threads (the second per-thread pass), longer staging rows and lists (capacity regrowth
+    from the density-derived default); lists and forces against brute force at init and
+    after 25 steps (one rebuild)."""
+    pos, box = li.fcc(10, 10, 10, rho=1.2)
+    pos = li.perturb(pos, 0.03)
+    vel = li.velocities(len(pos), 1.0)
+    with eng.LJMD(pos, vel, box) as ctx:
+        x = ctx.positions()
+        off, nbr = ctx.neighbours()
+        assert gid_pairs(off, nbr) == gid_pairs(*orc.neighbours(x, box, RN, "brute"))
+        check_forces(ctx, orc, x, box, 0.25)
+        ctx.step(25)
+        check_forces(ctx, orc, orc.wrap(ctx.positions(), box), box, 0.25)
+
+
 def test_errors(eng):
     pos, vel, box = c1(cells=6)
     bad = pos.copy()
