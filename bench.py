@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--no-boa", action="store_true")
     ap.add_argument("--no-dsl", action="store_true")
     ap.add_argument("--no-policy", action="store_true", help="skip the other rebuild policy's timing")
+    ap.add_argument("--split-self", action="store_true",
+                    help="one GPU through the full z-slab exchange path (halo planes sent to itself over NCCL)")
     ap.add_argument("--newton3", action="store_true",
                     help="NEXT-1 half-list force with reaction reductions (single GPU; slower)")
     args = ap.parse_args()
@@ -255,7 +257,10 @@ def main():
     check = 1 if (args.check or cfg.rebuild_check) else 0
     opts = ljmd.default_options(device=local, stream=stream.cuda_stream, profile=0,
                                 rebuild_check=check, rank=rank, nranks=world,
-                                newton3=1 if args.newton3 else 0)
+                                newton3=1 if args.newton3 else 0, split_self=1 if args.split_self else 0)
+    if id_buf is None and args.split_self and world == 1:
+        import ctypes
+        id_buf = ctypes.create_string_buffer(bytes(ljmd.nccl_unique_id()), 128)
     if id_buf is not None:
         import ctypes
         opts.nccl_id = ctypes.cast(id_buf, ctypes.c_void_p)
@@ -342,7 +347,7 @@ def main():
         hv = [torch.from_numpy(vel.copy()).pin_memory() for _ in range(2)]
         ho = [torch.empty((n, 3), dtype=torch.float64).pin_memory() for _ in range(2)]
         k_e2e = max(2, min(args.steps, 10))
-        overlapped = world == 1
+        overlapped = world == 1 and not args.split_self
         if overlapped:   # warm-up (allocates the copy stream and staging buffers)
             ctx.stage_state_ptr(hp[0].data_ptr(), hv[0].data_ptr())
             ctx.set_staged_state()
@@ -463,13 +468,13 @@ def main():
         "config": {"workload": cfg.name, "n_particles": n, "rho": li.RHO, "rc": li.RC,
                    "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "energy_every": 10, "dt": li.DT,
                    "t0": cfg.t0, "rebuild_policy": "safe" if check else "paper-fixed-20",
-                   "parallelism": f"z-slab x{world}",
+                   "parallelism": f"z-slab x{world}" + (" (slab exchange through NCCL to itself)" if args.split_self else ""),
                    "force_path": "newton3 half list + reductions (NEXT-1)" if args.newton3 else
                    "full list, fused velocity Verlet",
                    "l2": "working set > L2 (list %.0f MB + positions %.0f MB)" % (
                        4 * cand / 1e6, 32 * (n + st1["n_ghost"]) / 1e6)},
         "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
-        "transport": "nccl" if world > 1 else "none",
+        "transport": "nccl" if (world > 1 or args.split_self) else "none",
         "roofline": {"bound": "alu",
                      "kernel": "k_force_half (fp64 LJ pair loop)" if args.newton3 else "k_force (fp64 LJ pair loop)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
