@@ -11,8 +11,13 @@ cfg = li.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "C2"]
 pos, vel, box = cfg.build()
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
+split = int(os.environ.get("LJMD_SPLIT_SELF", "0"))
 opts = ljmd.default_options(device=0, stream=s.cuda_stream, rebuild_check=cfg.rebuild_check,
-                            list_order=int(os.environ.get("LJMD_LIST_ORDER", "1")))
+                            list_order=int(os.environ.get("LJMD_LIST_ORDER", "1")), split_self=split)
+if split:
+    import ctypes
+    _idb = ctypes.create_string_buffer(bytes(ljmd.nccl_unique_id()), 128)
+    opts.nccl_id = ctypes.cast(_idb, ctypes.c_void_p)
 ctx = LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=opts)
 for _ in range(3):
     ctx.step(20)
