@@ -974,6 +974,7 @@ struct ForceArgs {
     double* ke_part;
     const double4* xbuild;   // displacement check (may be null)
     Images im;               // ghost images written with x(n+1) (kKKD)
+    int tile_base;           // first tile of this launch
     DevFlags* fl;
     int n_own, n_pad;
     double rc2, c12, nc6, a12, na6, a0;   // nc6 = -c6, na6 = -a6 (fold into DFMA operands)
@@ -1192,7 +1193,7 @@ template <bool ENERGY, int MODE, bool CHECK>
 __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double sh[kForceThreads / 32];
-    const int tile = blockIdx.x;
+    const int tile = a.tile_base + blockIdx.x;   // a launch may cover a range of tiles
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const TileGeo T = tile_geo(a.g, tile);
     const int t0 = a.obegin[a.tile_oc0[tile]];
@@ -1289,8 +1290,8 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         const double pe = block_sum<kForceThreads>(epart, sh);
         const double k2 = block_sum<kForceThreads>(ke, sh);
         if (threadIdx.x == 0) {
-            a.pe_part[blockIdx.x] = pe;
-            a.ke_part[blockIdx.x] = k2;
+            a.pe_part[tile] = pe;
+            a.ke_part[tile] = k2;
         }
     }
 }

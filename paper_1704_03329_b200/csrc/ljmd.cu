@@ -45,6 +45,10 @@ struct ljmd_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // nranks > 1: the per-step halo exchange runs on aux_stream while the interior tiles'
+    // force launch runs on `stream`; the boundary tile layers wait for ev_halo
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     // ---- status
     ljmd_status err = LJMD_OK;
     std::string msg;
@@ -579,13 +583,14 @@ ForceArgs force_args(ljmd_ctx* c) {
 constexpr size_t kStageBytes = 24;   // packed {x, y, z} per staged particle
 
 template <bool E, int M, bool C>
-void force_launch(ljmd_ctx* c, const ForceArgs& a) {
+void force_launch(ljmd_ctx* c, const ForceArgs& a, int n_launch, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
 #if LJMD_PDL
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)c->n_tiles);
+    cfg.gridDim = dim3((unsigned)n_launch);
     cfg.blockDim = dim3(kForceThreads);
     cfg.dynamicSmemBytes = kStageBytes * (size_t)(c->max_staged + 1);
-    cfg.stream = c->stream;
+    cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
@@ -593,7 +598,7 @@ void force_launch(ljmd_ctx* c, const ForceArgs& a) {
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_force<E, M, C>, a);
 #else
-    k_force<E, M, C><<<c->n_tiles, kForceThreads, kStageBytes * (size_t)(c->max_staged + 1), c->stream>>>(a);
+    k_force<E, M, C><<<n_launch, kForceThreads, kStageBytes * (size_t)(c->max_staged + 1), st>>>(a);
 #endif
 }
 
@@ -707,7 +712,31 @@ ljmd_status launch_half(ljmd_ctx* c, bool energy, int mode, bool check, cudaEven
     return LJMD_OK;
 }
 
-ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check) {
+template <bool E, int M, bool C>
+void force_range(ljmd_ctx* c, ForceArgs a, int first, int count, cudaStream_t st = nullptr) {
+    if (count <= 0) return;
+    a.tile_base = first;
+    force_launch<E, M, C>(c, a, count, st);
+}
+
+// One force evaluation.  halo_pending (nranks > 1): the halo exchange of this step is in
+// flight on aux_stream; the interior tile layers go first, the first and last z layers
+// (whose halos hold the received planes) after ev_halo.  (Launching the boundary layers on
+// aux_stream, concurrently with the interior, measured slower.)
+template <bool E, int M, bool C>
+void force_all(ljmd_ctx* c, const ForceArgs& a, bool halo_pending) {
+    const int layer = c->geo.ntx * c->geo.nty;
+    if (!halo_pending) {
+        force_range<E, M, C>(c, a, 0, c->n_tiles);
+        return;
+    }
+    force_range<E, M, C>(c, a, layer, c->n_tiles - 2 * layer);
+    cudaStreamWaitEvent(c->stream, c->ev_halo, 0);
+    force_range<E, M, C>(c, a, 0, layer);
+    force_range<E, M, C>(c, a, c->n_tiles - layer, layer);
+}
+
+ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check, bool halo_pending = false) {
     if (c->newton3) {
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (c->opt.profile) {
@@ -738,16 +767,17 @@ ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check) {
     }
     constexpr int KT = kKick | kThermo, DT = kKKD | kThermo;
     const bool th = c->nu_dt > 0.0 && mode != kStore;
+    const bool h = halo_pending;
     if (energy) {
-        if (mode == kStore) force_launch<true, kStore, false>(c, a);
-        else if (mode == kKick) th ? force_launch<true, KT, false>(c, a) : force_launch<true, kKick, false>(c, a);
-        else if (check) th ? force_launch<true, DT, true>(c, a) : force_launch<true, kKKD, true>(c, a);
-        else th ? force_launch<true, DT, false>(c, a) : force_launch<true, kKKD, false>(c, a);
+        if (mode == kStore) force_all<true, kStore, false>(c, a, h);
+        else if (mode == kKick) th ? force_all<true, KT, false>(c, a, h) : force_all<true, kKick, false>(c, a, h);
+        else if (check) th ? force_all<true, DT, true>(c, a, h) : force_all<true, kKKD, true>(c, a, h);
+        else th ? force_all<true, DT, false>(c, a, h) : force_all<true, kKKD, false>(c, a, h);
     } else {
-        if (mode == kStore) force_launch<false, kStore, false>(c, a);
-        else if (mode == kKick) th ? force_launch<false, KT, false>(c, a) : force_launch<false, kKick, false>(c, a);
-        else if (check) th ? force_launch<false, DT, true>(c, a) : force_launch<false, kKKD, true>(c, a);
-        else th ? force_launch<false, DT, false>(c, a) : force_launch<false, kKKD, false>(c, a);
+        if (mode == kStore) force_all<false, kStore, false>(c, a, h);
+        else if (mode == kKick) th ? force_all<false, KT, false>(c, a, h) : force_all<false, kKick, false>(c, a, h);
+        else if (check) th ? force_all<false, DT, true>(c, a, h) : force_all<false, kKKD, true>(c, a, h);
+        else th ? force_all<false, DT, false>(c, a, h) : force_all<false, kKKD, false>(c, a, h);
     }
     CKL();
     if (c->opt.profile) {
@@ -771,11 +801,11 @@ ljmd_status collect_profile(ljmd_ctx* c, int64_t first_launch) {
 // nranks = 2 (both neighbours are the same rank): send (up, down), receive (from below,
 // from above).  hi/lo payloads: what goes to the upper / lower neighbour.
 ljmd_status exchange(ljmd_ctx* c, void* to_hi, size_t b_hi, void* to_lo, size_t b_lo, void* from_lo, size_t r_lo,
-                     void* from_hi, size_t r_hi) {
+                     void* from_hi, size_t r_hi, cudaStream_t st = nullptr) {
     std::vector<Xfer> sends{{c->hi_rank, to_hi, b_hi}, {c->lo_rank, to_lo, b_lo}};
     std::vector<Xfer> recvs{{c->lo_rank, from_lo, r_lo}, {c->hi_rank, from_hi, r_hi}};
     std::string err;
-    if (!c->tr->exchange(c->stream, sends, recvs, err)) return set_err(c, LJMD_E_NCCL, "%s", err.c_str());
+    if (!c->tr->exchange(st ? st : c->stream, sends, recvs, err)) return set_err(c, LJMD_E_NCCL, "%s", err.c_str());
     return LJMD_OK;
 }
 
@@ -788,16 +818,17 @@ ljmd_status allreduce(ljmd_ctx* c, double* dbuf, int n, bool max) {
 
 // Halo: the boundary planes' positions travel to the neighbours' ghost planes, received
 // after the slot range of the current position buffer (nranks > 1, every step).
-ljmd_status halo_exchange(ljmd_ctx* c) {
+ljmd_status halo_exchange(ljmd_ctx* c, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
     const int ns = c->n_send[0] + c->n_send[1];
     if (ns) {
-        k_pack<<<nblk(ns, 256), 256, 0, c->stream>>>(ns, c->send_idx, c->x[c->xc], c->slot_gid, c->send_buf);
+        k_pack<<<nblk(ns, 256), 256, 0, st>>>(ns, c->send_idx, c->x[c->xc], c->slot_gid, c->send_buf);
         CKL();
     }
     double4* rx = c->x[c->xc] + c->n_slots;
     const size_t e = sizeof(double4);
     return exchange(c, c->send_buf + c->n_send[0], e * c->n_send[1], c->send_buf, e * c->n_send[0], rx,
-                    e * c->n_recv[0], rx + c->n_recv[0], e * c->n_recv[1]);
+                    e * c->n_recv[0], rx + c->n_recv[0], e * c->n_recv[1], st);
 }
 
 ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
@@ -816,10 +847,10 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
 }
 
 // images of received halo planes, after each exchange (nranks > 1)
-ljmd_status refresh_recv(ljmd_ctx* c) {
+ljmd_status refresh_recv(ljmd_ctx* c, cudaStream_t st = nullptr) {
     if (c->n_grecv > 0) {
-        k_ghost_flat<<<nblk(c->n_grecv, 256), 256, 0, c->stream>>>(c->n_grecv, c->grecv, c->geo, c->x[c->xc],
-                                                                    c->xp[c->xc]);
+        k_ghost_flat<<<nblk(c->n_grecv, 256), 256, 0, st ? st : c->stream>>>(c->n_grecv, c->grecv, c->geo,
+                                                                               c->x[c->xc], c->xp[c->xc]);
         CKL();
     }
     return LJMD_OK;
@@ -1311,6 +1342,16 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         }
     }
     if ((s = plan_geometry(c, box)) != LJMD_OK) return fail(s);
+    // overlapped halo (nranks > 1, not Newton-3): needs interior tile layers besides the two
+    // boundary ones
+    if (c->split && !c->newton3 && c->geo.ntz >= 3) {
+        if (cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
+            set_err(c, LJMD_E_CUDA, "aux stream creation failed");
+            return fail(LJMD_E_CUDA);
+        }
+    }
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
         cudaHostAlloc(&c->h_fl, sizeof(DevFlags), cudaHostAllocMapped) != cudaSuccess ||
@@ -1456,6 +1497,7 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         ++c->since;
         ++c->steps_done;
         bool due = c->since >= c->opt.rebuild_every;
+        bool halo_pending = false;
         if (!due && check) {
             // global max displacement (non-negative doubles: max of the bit patterns)
             TRY(allreduce(c, reinterpret_cast<double*>(&c->d_fl->maxdisp2), 1, true));
@@ -1472,7 +1514,15 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         } else {
             // ghost images of owned particles were written with the positions (force
             // epilogue / kick-drift); received halo planes need theirs after the exchange
-            if (c->split) {
+            if (c->split && c->aux_stream) {
+                // the halo travels on aux_stream while the interior tiles compute
+                CK(cudaEventRecord(c->ev_ready, c->stream));
+                CK(cudaStreamWaitEvent(c->aux_stream, c->ev_ready, 0));
+                TRY(halo_exchange(c, c->aux_stream));
+                TRY(refresh_recv(c, c->aux_stream));
+                CK(cudaEventRecord(c->ev_halo, c->aux_stream));
+                halo_pending = true;
+            } else if (c->split) {
                 TRY(halo_exchange(c));
                 TRY(refresh_recv(c));
             }
@@ -1481,7 +1531,7 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         const bool sample = ee > 0 && (c->steps_done % ee) == 0;
         const bool last = s == nsteps;
         if (check && !last) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
-        TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last));
+        TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last, halo_pending));
         if (sample) {
             TRY(finalize_energy(c, c->hist + 2 * nsamp));
             TRY(allreduce(c, c->hist + 2 * nsamp, 2, false));
@@ -1680,6 +1730,12 @@ void ljmd_destroy(ljmd_ctx* c) {
         }
         cudaStreamDestroy(c->copy_stream);
     }
+    if (c->aux_stream) {
+        cudaStreamSynchronize(c->aux_stream);
+        cudaStreamDestroy(c->aux_stream);
+    }
+    if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
