@@ -318,7 +318,7 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
                             double* __restrict__ vz_n, int* __restrict__ gid_new,
                             int* __restrict__ own_slot, int* __restrict__ ocell_of,
                             int* __restrict__ slot_gid, double4* __restrict__ xbuild,
-                            double* __restrict__ xp_new) {
+                            double* __restrict__ xp_new, DevFlags* fl) {
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= n_ocell) return;
@@ -337,11 +337,13 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
         const int gk = mine ? gid_old[t_old] : 0;
         const double xk = mine ? xw[t_old].x : 0.0;
         int r = 0;
+        bool samex = false;   // another member with the same x: candidate for coincidence
         if (m <= 32) {
             for (int s = 0; s < m; ++s) {
                 const double xs = __shfl_sync(0xffffffffu, xk, s);
                 const int gs = __shfl_sync(0xffffffffu, gk, s);
                 r += (xs < xk) || (xs == xk && gs < gk);
+                samex |= xs == xk && gs != gk;
             }
         } else {
             for (int s = 0; s < m; ++s) {
@@ -349,6 +351,18 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
                 const double xs = xw[ts].x;
                 const int gs = gid_old[ts];
                 r += (xs < xk) || (xs == xk && gs < gk);
+                samex |= xs == xk && gs != gk;
+            }
+        }
+        if (mine && samex) {   // rare: coincident particles (r^2 == 0) are an error
+            const double4 pk = xw[t_old];
+            for (int s = 0; s < m; ++s) {
+                const int ts = perm[b + s];
+                const double4 ps = xw[ts];
+                if (ts != t_old && ps.x == pk.x && ps.y == pk.y && ps.z == pk.z && gk < gid_old[ts]) {
+                    atomicMin(&fl->overlap_gid, gk);
+                    fl->overlap_gid_j = gid_old[ts];
+                }
             }
         }
         if (!mine) continue;
@@ -790,7 +804,8 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
                         const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
                         if (r2f >= thr_hi) continue;
                         bool take = r2f < thr_lo;
-                        if (!take || r2f < 1e-6f) {          // rare: decide in fp64 (the oracle's test)
+                        if (!take) {          // rare: decide in fp64 (the oracle's test); coincident
+                                              // particles are caught by the cell sort
                             const int j = rbeg + (jl - roff);
                             const double4 xj = a.x[j];
                             const double r2 = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z);

@@ -1013,7 +1013,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
         c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, gid_old, c->xw, vo, vo + oc, vo + 2 * oc,
         xn, c->xf, vn, vn + oc, vn + 2 * oc, c->gid[on], c->own_slot, c->ocell_of, c->slot_gid,
-        c->opt.rebuild_check ? c->xbuild : nullptr, c->xp[c->xc ^ 1]);
+        c->opt.rebuild_check ? c->xbuild : nullptr, c->xp[c->xc ^ 1], c->d_fl);
     CKL();
     c->oc_cur = on;
     c->xc ^= 1;
