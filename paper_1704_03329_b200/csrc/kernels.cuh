@@ -672,16 +672,15 @@ __global__ void k_tile_rows(int n_tiles, Geo g, const int* __restrict__ ebegin,
 }
 
 // --------------------------------------------------------------------------- neighbour list
-// One warp per pair of x-adjacent owned cells (Sec. 3.4 cell method):
-// lanes hold the pair's particles i (thread per i, <= 32 per pass), the warp walks the
-// union of their stencil rows -- 9 contiguous slot ranges of 4 cells -- with every j
-// fetched once as a broadcast load.  Decision r^2 < rbar_c^2 (strict, R4): an fp32
-// distance decides every candidate outside a provably conservative band around rbar_c^2;
-// candidates inside the band (and r^2 ~ 0) take the canonical fp64 test, which is the
-// oracle's decision.  Each list is emitted in (stencil row, slot) = (stencil offset, gid)
-// order as 16-bit indices into the tile's shared-memory staging buffer, in blocks of 8
-// (nbr8[b * n_pad + t], one 16-byte load per 8 neighbours in the force kernel; the last
-// block is padded with the tile's sentinel index).
+// Cell method (Sec. 3.4) on the force tiles: one CTA per tile stages the
+// fp32 mirror of the tile's halo rows; thread per particle i walks its 9 stencil rows (each
+// a contiguous, x-sorted run of 3 cells) inside a binary-searched x-window.  Decision
+// r^2 < rbar_c^2 (strict, R4): an fp32 distance decides every candidate outside a provably
+// conservative band around rbar_c^2; candidates inside the band take the canonical fp64
+// test, which is the oracle's decision (coincident particles are caught by the cell sort).
+// Each list is emitted in (stencil row, slot) order as 16-bit indices into the tile's
+// shared-memory staging buffer, in blocks of 8 (nbr8[b * n_pad + t], one 16-byte load per 8
+// neighbours in the force kernel; the last block is padded with the tile's sentinel).
 struct NlistArgs {
     Geo g;
     const double4* x;
