@@ -52,6 +52,8 @@ METRIC = "LJ particle-timesteps/s"
 UNIT = "particle-timesteps/s"
 FLOPS_PER_CAND = 21.0         # Listing lst:LJ-kernel, force only
 FLOPS_PER_CAND_E = 26.0       # + potential energy
+# nominal FP64 FMA peak of one B200: 148 SMs x 64 FP64 lanes x 2 flops x 1.965 GHz
+PEAK_FP64_NOMINAL = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
 def env_int(k, d):
@@ -130,20 +132,33 @@ def cpu_info():
 
 # ---------------------------------------------------------------------------------- oracle legs
 
-def oracle_cycle_rate(pos, vel, box, n_steps=2):
+def oracle_cycle_rate(pos, vel, box, n_steps=2, omp=False):
     """Bounded oracle sample: init (wrap + cell/neighbour list + F) and n_steps list-mode VV
-    steps on one host core; extrapolated to one rebuild cycle (1 build + 20 steps)."""
+    steps (plain build: one host core; OpenMP build: all cores, identical results);
+    extrapolated to one rebuild cycle (1 build + 20 steps)."""
     import oracle
     oracle.build()
     t0 = time.perf_counter()
-    oracle.run(pos, vel, box, 0, mode="list", energy_every=0)
+    oracle.run(pos, vel, box, 0, mode="list", energy_every=0, omp=omp)
     t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
-    oracle.run(pos, vel, box, n_steps, mode="list", energy_every=10)
+    oracle.run(pos, vel, box, n_steps, mode="list", energy_every=10, omp=omp)
     t_run = time.perf_counter() - t0
     t_step = max(t_run - t_init, 1e-9) / n_steps
     cycle = t_init + MD_PER_STEP * t_step
     return len(pos) * MD_PER_STEP / cycle, t_init, t_step
+
+
+def oracle_brute_rate(n_steps=40):
+    """C1 (N = 4000) with the O(N^2) brute-force force (the physics truth, no list) on one
+    host core: n_steps VV steps; particle-timesteps/s."""
+    import oracle
+    c1 = li.CONFIGS["C1"]
+    pos, vel, box = c1.build()
+    t0 = time.perf_counter()
+    oracle.run(pos, vel, box, n_steps, mode="brute", energy_every=10)
+    t = time.perf_counter() - t0
+    return len(pos) * n_steps / t, t
 
 
 def run_reference(args, cfg):
@@ -160,10 +175,11 @@ def run_reference(args, cfg):
     pos, vel, box = cfg.build()
     n = len(pos)
     cores, model = cpu_info()
+    threads = oracle.threads()   # the OpenMP build of the oracle on every host core
     # warm-up: W MD steps (includes one init build)
-    oracle.run(pos, vel, box, max(args.warmup, 0), mode="list", energy_every=10)
+    oracle.run(pos, vel, box, max(args.warmup, 0), mode="list", energy_every=10, omp=True)
     t0 = time.perf_counter()
-    r = oracle.run(pos, vel, box, args.steps, mode="list", energy_every=10)
+    r = oracle.run(pos, vel, box, args.steps, mode="list", energy_every=10, omp=True)
     t = time.perf_counter() - t0
     value = n * args.steps / t
     line = {
@@ -173,11 +189,12 @@ def run_reference(args, cfg):
         "dtype": "f64", "data": "synthetic FCC (ljinputs, seeded)",
         "config": {"workload": full.name, "n_particles": full.n, "rho": li.RHO,
                    "rc": li.RC, "rbar_c": li.RC + li.DELTA, "rebuild_every": li.NS, "dt": li.DT, "t0": cfg.t0},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                          "sample": f"{cfg.name} (N={n}"
                                    + (f", one GPU's share of {full.name}" if full is not cfg else "")
-                                   + f"): oracle list-mode VV, {args.steps} MD steps in one call "
-                                   f"(init build + rebuilds every {li.NS}), 1 thread, {model}"},
+                                   + f"): oracle list-mode VV (OpenMP build, {threads} threads), "
+                                   f"{args.steps} MD steps in one call (init build + rebuilds every {li.NS}), "
+                                   f"{model}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "rebuilds": int(len(r.rebuild_steps)),
     }
@@ -201,6 +218,7 @@ def main():
     ap.add_argument("--no-boa", action="store_true")
     ap.add_argument("--no-dsl", action="store_true")
     ap.add_argument("--no-policy", action="store_true", help="skip the other rebuild policy's timing")
+    ap.add_argument("--no-validation", action="store_true", help="skip the missed-pair validation leg")
     ap.add_argument("--split-self", action="store_true",
                     help="one GPU through the full z-slab exchange path (halo planes sent to itself over NCCL)")
     ap.add_argument("--newton3", action="store_true",
@@ -329,12 +347,15 @@ def main():
             traffic_src = tj["source"]
     except (OSError, ValueError, KeyError):
         pass
+    # roofline denominator: MEASURED_PEAKS.json has no FP64 entry and the profiling guide no
+    # FP64 fallback, so the peak is derived from the unit counts and clocks;
+    # the achievable DFMA throughput measured by a probe kernel is reported beside it
+    peak = PEAK_FP64_NOMINAL
+    peak_src = "derived: 148 SMs x 64 FP64 FMA lanes x 2 flops x 1.965 GHz (sm max clock)"
     try:
-        peak = ljmd.measure_fp64_peak(local)
-        peak_src = "measured (DFMA-chain probe, ljmd_measure_fp64_peak)"
+        peak_probe = ljmd.measure_fp64_peak(local)
     except Exception:
-        peak = 148 * 64 * 2 * 1.965e9 / 1e12
-        peak_src = "derived 148 SM x 64 FP64 lanes x 2 x 1.965 GHz"
+        peak_probe = None
 
     # end to end through the public API with host buffers (pinned), per bench step: a new
     # state from the host (H2D pos+vel, the init sequence), step(20), positions (D2H) and
@@ -405,9 +426,35 @@ def main():
             q1.record(stream)
             torch.cuda.synchronize()
             ms_q = q0.elapsed_time(q1)
+            sq = c2.stats()
             policy = {"rebuild_policy": "safe" if other else "paper-fixed-20",
                       "value": n * MD_PER_STEP * kq / (ms_q * 1e-3), "unit": UNIT,
-                      "rebuilds_per_20_steps": (c2.stats()["n_rebuilds"] - r0) / kq, "cycles": kq}
+                      "rebuilds_per_20_steps": (sq["n_rebuilds"] - r0) / kq, "cycles": kq,
+                      "dangerous_builds": sq["dangerous_builds"]}
+
+    # Validation leg (ljmd_options.validate, reading R7): the headline's rebuild policy on the
+    # same workload with the missed-pair count on every step -- what the paper's fixed Ns = 20
+    # costs in interactions it does not see (pairs inside rc that the list does not serve).
+    # Fresh context from the same state, W + 2 cycles; not timed.
+    validation = None
+    if not args.no_validation and world == 1 and not args.split_self and not args.newton3:
+        o3 = ljmd.default_options(device=local, stream=stream.cuda_stream, rebuild_check=check, validate=1)
+        kv = args.warmup + 2
+        with LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=o3) as c3:
+            for _ in range(kv):
+                c3.step(MD_PER_STEP)
+            sv = c3.stats()
+            vrows = c3.validation()
+        last = vrows[-MD_PER_STEP:]
+        validation = {"rebuild_policy": "safe" if check else "paper-fixed-20", "md_steps": int(len(vrows)),
+                      "missed_pairs": int(sv["missed_pairs"]), "missed_particle_steps": int(sv["missed_particle_steps"]),
+                      "max_missed_particles_per_step": int(sv["max_missed_particles"]),
+                      "steps_with_missed_pairs": int((vrows[:, 1] > 0).sum()),
+                      "last_cycle_missed_particle_steps": int(last[:, 1].sum()),
+                      "dangerous_builds": int(sv["dangerous_builds"]), "rebuilds": int(sv["n_rebuilds"]),
+                      "max_build_disp": sv["max_build_disp"], "delta": li.DELTA,
+                      "note": "missed pair = r < rc at a step's positions but not in the list in use "
+                              "(ljmd validate mode: fresh cell search minus in-range list entries)"}
 
     # §8(f) NEXT-2 bond-order analysis on the same state (not part of the headline metric):
     # Q_6 with the first-shell cutoff 1.5 sigma, CUDA events around the call (kernel +
@@ -453,12 +500,22 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1:
+        import oracle
         cores, model = cpu_info()
-        c2pos, c2vel, c2box = pos, vel, box
-        rate, t_init, t_step = oracle_cycle_rate(c2pos, c2vel, c2box, n_steps=2)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{cfg.name} (N={n}): oracle init build ({t_init:.1f} s) + 2 list-mode VV steps "
-                         f"({t_step:.2f} s/step) on 1 thread of {cores} ({model}); rate = N*20/(build+20*step)"}
+        threads = oracle.threads()
+        rate, t_init, t_step = oracle_cycle_rate(pos, vel, box, n_steps=2, omp=True)
+        rate1, t_init1, t_step1 = oracle_cycle_rate(pos, vel, box, n_steps=1, omp=False)
+        rate_b, t_b = oracle_brute_rate(40)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"{cfg.name} (N={n}): oracle (OpenMP build, {threads} threads of {cores}, {model}) "
+                         f"init build ({t_init:.2f} s) + 2 list-mode VV steps ({t_step:.3f} s/step); "
+                         f"rate = N*20/(build+20*step)",
+               "one_core": {"value": rate1, "unit": UNIT, "cores": 1,
+                            "sample": f"{cfg.name}: plain build, init {t_init1:.1f} s + 1 step {t_step1:.2f} s, "
+                                      "extrapolated to one 20-step cycle"},
+               "c1_brute_force_one_core": {"value": rate_b, "unit": UNIT, "cores": 1,
+                                           "sample": f"C1 (N=4000): 40 VV steps with the O(N^2) brute-force "
+                                                     f"force (no list) in {t_b:.1f} s"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -471,13 +528,14 @@ def main():
                    "parallelism": f"z-slab x{world}" + (" (slab exchange through NCCL to itself)" if args.split_self else ""),
                    "force_path": "newton3 half list + reductions (NEXT-1)" if args.newton3 else
                    "full list, fused velocity Verlet",
-                   "l2": "working set > L2 (list %.0f MB + positions %.0f MB)" % (
-                       4 * cand / 1e6, 32 * (n + st1["n_ghost"]) / 1e6)},
+                   "l2": "working set > L2 (16-bit list %.0f MB + positions %.0f MB + v, F %.0f MB)" % (
+                       2 * cand / 1e6, 56 * (n + st1["n_ghost"]) / 1e6, 48 * n / 1e6)},
         "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
         "transport": "nccl" if (world > 1 or args.split_self) else "none",
         "roofline": {"bound": "alu",
                      "kernel": "k_force_half (fp64 LJ pair loop)" if args.newton3 else "k_force (fp64 LJ pair loop)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_probe": peak_probe, "frac_probe": achieved / peak_probe if peak_probe else None,
                      "traffic_source": traffic_src,
                      "flops_per_launch": flops, "avg_launch_ms": f_ms, "peak_source": peak_src,
                      "flop_count": "Listing 9: 21 flops per list candidate (+5 with PE every 10th step)"},
@@ -488,6 +546,9 @@ def main():
         "neighbours_per_particle": cand / n,
         "e2e": e2e,
         "other_rebuild_policy": policy,
+        "validation": validation,
+        "dangerous_builds": int(st1["dangerous_builds"] - st0["dangerous_builds"]),
+        "rebuilds": int(st1["n_rebuilds"] - st0["n_rebuilds"]),
         "cpu_baseline": cpu,
         "boa": boa,
         "dsl": dsl_info,

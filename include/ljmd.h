@@ -84,6 +84,16 @@ typedef struct {
                                velocity Verlet in a separate pass; nranks = 1 only.  Slower
                                than the default on B200; sums not bitwise
                                reproducible (reduction order)                                */
+    int64_t validate;       /* 1: validation mode (single rank, full list): before every force
+                               evaluation inside ljmd_step, count the ordered pairs with
+                               r^2 < rc^2 (canonical r^2, minimum image, R9) that the Verlet
+                               list does not serve -- a fresh cell search minus the in-range
+                               list entries, per particle.  Per-step counts from
+                               ljmd_get_validation; totals in ljmd_stats.  Costs about one list
+                               build per step; 0 (default) off.  The paper's fixed Ns = 20
+                                keeps a list past the skin guarantee of
+                               Eq. eqn:extended_cutoff when particles move
+                               fast: this measures what that costs in missed interactions.  */
 } ljmd_options;
 
 typedef struct {
@@ -100,6 +110,17 @@ typedef struct {
     double  force_ms;          /* summed CUDA-event time of those launches (profile = 1)    */
     int64_t energy_samples;    /* samples available from ljmd_get_energy_history            */
     int64_t kernel_launches;   /* kernels of this library launched since init               */
+    /* Rebuild certification (Eq. eqn:extended_cutoff; reading R7): a
+     * rebuild is "dangerous" when 2 max_i |x_i(s-1) - x_i(build)| > delta on the last step
+     * s-1 the old list served, i.e. the skin no longer guaranteed that list (counted over
+     * all ranks, since init / set_state; never under rebuild_check = 1). */
+    int64_t dangerous_builds;
+    double  max_build_disp;    /* largest max_i |x_i(s-1) - x_i(build)| seen at a rebuild     */
+    /* Validation mode (ljmd_options.validate) totals since init / set_state: */
+    int64_t validated_steps;
+    int64_t missed_pairs;      /* ordered pairs with r < rc not in the list, summed over steps */
+    int64_t missed_particle_steps;  /* (particle, step) with at least one missed pair          */
+    int64_t max_missed_particles;   /* largest number of such particles in one step           */
 } ljmd_stats;
 
 /* Fill *o with the defaults listed above. */
@@ -171,6 +192,10 @@ ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, in
 /* MD step index of each rebuild after init (min(cap, n_rebuilds) entries). */
 ljmd_status ljmd_get_rebuild_steps(ljmd_ctx* c, int64_t* out, int64_t cap, int64_t* count);
 ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s);
+/* Validation mode: per validated step since init / set_state, out[k] = {step index,
+ * particles with at least one missed pair, missed ordered pairs} (min(cap, available)
+ * rows of 3 int64; *count = available).  LJMD_E_ARG if validation is off. */
+ljmd_status ljmd_get_validation(ljmd_ctx* c, int64_t* out, int64_t cap, int64_t* count);
 
 /* Message of the last error of c (or of the last failed ljmd_init if c == NULL). */
 const char* ljmd_last_error(const ljmd_ctx* c);

@@ -20,19 +20,23 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ljmd_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")   # same source, -fopenmp (all-core timing leg)
 _lib = None
+_lib_omp = None
 
 _D = ctypes.POINTER(ctypes.c_double)
 _I = ctypes.POINTER(ctypes.c_int64)
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle (gcc, -O2 -ffp-contract=off).  Returns the .so path."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
+    """Compile the oracle (gcc, -O2 -ffp-contract=off), plain and OpenMP.  Returns the
+    plain .so path."""
+    for lib, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+            tmp = lib + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+                                   "-fPIC", "-shared", *extra, "-o", tmp, _SRC, "-lm"])
+            os.replace(tmp, lib)
     return _LIB
 
 
@@ -48,10 +52,15 @@ class _Params(ctypes.Structure):
                 ("nu_dt", ctypes.c_double), ("temp", ctypes.c_double), ("seed", ctypes.c_uint64)]
 
 
-def _load():
-    global _lib
-    if _lib is None:
-        lib = ctypes.CDLL(build())
+def _load(omp: bool = False):
+    global _lib, _lib_omp
+    if omp and _lib_omp is not None:
+        return _lib_omp
+    if not omp and _lib is not None:
+        return _lib
+    if True:
+        build()
+        lib = ctypes.CDLL(_LIB_OMP if omp else _LIB)
         lib.orc_wrap.restype = ctypes.c_int64
         lib.orc_wrap.argtypes = [ctypes.c_int64, _D, _D]
         lib.orc_displacement.restype = None
@@ -76,15 +85,27 @@ def _load():
                                         _D, _D, _D, _D]
         lib.orc_run.restype = ctypes.c_int64
         lib.orc_run.argtypes = [ctypes.c_int64, _D, _D, _D, ctypes.POINTER(_Params), ctypes.c_int64,
-                                _D, _D, _D, _I, ctypes.c_int64]
+                                _D, _D, _D, _I, ctypes.c_int64, _I, _I]
+        lib.orc_missed.restype = None
+        lib.orc_missed.argtypes = [ctypes.c_int64, _D, _D, ctypes.c_double, _I, _I, _I, _I]
+        lib.orc_threads.restype = ctypes.c_int
+        lib.orc_threads.argtypes = [ctypes.c_int]
         U32 = ctypes.POINTER(ctypes.c_uint32)
         lib.orc_philox4x32.restype = None
         lib.orc_philox4x32.argtypes = [U32, U32, U32]
         lib.orc_andersen.restype = ctypes.c_int64
         lib.orc_andersen.argtypes = [ctypes.c_int64, _D, ctypes.c_uint64, ctypes.c_int64, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double]
-        _lib = lib
-    return _lib
+        if omp:
+            _lib_omp = lib
+        else:
+            _lib = lib
+    return lib
+
+
+def threads(k: int = 0) -> int:
+    """Threads of the OpenMP build (k > 0 sets them); results do not depend on it."""
+    return _load(omp=True).orc_threads(int(k))
 
 
 def _dp(a):
@@ -242,12 +263,28 @@ class Run:
     pe: np.ndarray
     ke: np.ndarray
     rebuild_steps: np.ndarray
+    missed_particles: np.ndarray = None   # validate: per step (index = step; 0 = init)
+    missed_pairs: np.ndarray = None
+
+
+def missed(pos, box, rc, nlist):
+    """Missed pairs of the list nlist = (offsets, nbr) at positions pos: (particles with at
+    least one pair r < rc not in their list, such ordered pairs), brute force."""
+    p = _f64(pos, (-1, 3))
+    off = np.ascontiguousarray(nlist[0], dtype=np.int64)
+    nb = np.ascontiguousarray(nlist[1], dtype=np.int64)
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _load().orc_missed(p.shape[0], _dp(p), _dp(_f64(box)), float(rc), _ip(off), _ip(nb), ctypes.byref(a),
+                       ctypes.byref(b))
+    return a.value, b.value
 
 
 def run(pos, vel, box, nsteps, lj: LJ = LJ(), dt=0.005, mass=1.0, delta=0.25, ns=20,
-        check=0, mode="list", energy_every=10, thermostat=None):
+        check=0, mode="list", energy_every=10, thermostat=None, validate=False, omp=False):
     """O6/O7: velocity-Verlet trajectory with the paper's rebuild schedule.
-    thermostat = (nu, T, seed): O8 Andersen collisions after every step."""
+    thermostat = (nu, T, seed): O8 Andersen collisions after every step.
+    validate: missed pairs of the list at every step (orc_missed; list mode).
+    omp: the OpenMP build of the same source (identical results; bench timing leg)."""
     p = _f64(pos, (-1, 3)).copy()
     v = _f64(vel, (-1, 3)).copy()
     b = _f64(box)
@@ -263,8 +300,10 @@ def run(pos, vel, box, nsteps, lj: LJ = LJ(), dt=0.005, mass=1.0, delta=0.25, ns
         raise ValueError("Andersen thermostat needs 0 <= nu*dt <= 1 and T >= 0")
     prm = _Params(lj.c(), dt, mass, delta, ns, check, 1 if mode == "list" else 0, energy_every,
                   nu * dt, temp, seed)
-    nreb = _load().orc_run(n, _dp(p), _dp(v), _dp(b), ctypes.byref(prm), nsteps,
-                           _dp(F), _dp(pe), _dp(ke), _ip(rs), cap)
+    mp = np.zeros(nsteps + 1, dtype=np.int64) if validate else None
+    mq = np.zeros(nsteps + 1, dtype=np.int64) if validate else None
+    nreb = _load(omp).orc_run(n, _dp(p), _dp(v), _dp(b), ctypes.byref(prm), nsteps,
+                              _dp(F), _dp(pe), _dp(ke), _ip(rs), cap, _ip(mp), _ip(mq))
     if nreb < 0:
         raise ValueError("box too small: fewer than 3 cells of width >= rbar_c")
-    return Run(p, v, F, pe, ke, rs[:nreb])
+    return Run(p, v, F, pe, ke, rs[:nreb], mp, mq)

@@ -37,6 +37,23 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Threads of the OpenMP build (bench.py's all-core leg); the plain build runs 1.  k > 0
+ * sets the count; returns the count in use.  No result depends on it: every parallel loop
+ * writes per-particle rows or reduces integers. */
+int orc_threads(int k)
+{
+#ifdef _OPENMP
+    if (k > 0) omp_set_num_threads(k);
+    return omp_get_max_threads();
+#else
+    (void)k;
+    return 1;
+#endif
+}
 
 /* ------------------------------------------------------------------ O1 -- */
 /* Wrap one coordinate into the half-open interval [0, L) (reading R10).
@@ -136,18 +153,21 @@ int orc_cell_dims(const double box[3], double rn, int64_t nc[3])
     return 0;
 }
 
-int64_t orc_neigh_cells(int64_t n, const double *pos, const double box[3], double rn,
-                        int64_t *offsets, int64_t *nbr)
-{
+/* Linked-list cells (Rapaport): head[c] -> next[i]; cid[3i..3i+2] the cell of particle i. */
+typedef struct {
     int64_t nc[3];
-    if (orc_cell_dims(box, rn, nc) != 0) return -1;
+    int64_t *head, *next, *cid;
+} orc_cells;
+
+static void cells_build(int64_t n, const double *pos, const double box[3], const int64_t nc[3], orc_cells *C)
+{
     double w[3] = {box[0] / (double)nc[0], box[1] / (double)nc[1], box[2] / (double)nc[2]};
     int64_t ncell = nc[0] * nc[1] * nc[2];
-    /* linked-list cells (Rapaport), head[c] -> next[i] */
-    int64_t *head = (int64_t *)malloc(sizeof(int64_t) * ncell);
-    int64_t *next = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
-    int64_t *cid = (int64_t *)malloc(sizeof(int64_t) * 3 * (n > 0 ? n : 1));
-    for (int64_t c = 0; c < ncell; ++c) head[c] = -1;
+    for (int d = 0; d < 3; ++d) C->nc[d] = nc[d];
+    C->head = (int64_t *)malloc(sizeof(int64_t) * ncell);
+    C->next = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    C->cid = (int64_t *)malloc(sizeof(int64_t) * 3 * (n > 0 ? n : 1));
+    for (int64_t c = 0; c < ncell; ++c) C->head[c] = -1;
     for (int64_t i = n - 1; i >= 0; --i) {
         int64_t c3[3];
         for (int d = 0; d < 3; ++d) {
@@ -155,42 +175,83 @@ int64_t orc_neigh_cells(int64_t n, const double *pos, const double box[3], doubl
             if (c < 0) c = 0;
             if (c > nc[d] - 1) c = nc[d] - 1;
             c3[d] = c;
-            cid[3 * i + d] = c;
+            C->cid[3 * i + d] = c;
         }
         int64_t c = (c3[2] * nc[1] + c3[1]) * nc[0] + c3[0];
-        next[i] = head[c];
-        head[c] = i;
+        C->next[i] = C->head[c];
+        C->head[c] = i;
     }
+}
+
+static void cells_free(orc_cells *C)
+{
+    free(C->head);
+    free(C->next);
+    free(C->cid);
+}
+
+/* NB(i) by the 27 periodic neighbour cells of i, into row[] ascending; returns |NB(i)|. */
+static int64_t cells_row(int64_t i, const double *pos, const double box[3], double rn2, const orc_cells *C,
+                         int64_t *row)
+{
+    const int64_t *nc = C->nc;
+    int64_t cnt = 0;
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                int64_t cx = (C->cid[3 * i + 0] + dx + nc[0]) % nc[0];
+                int64_t cy = (C->cid[3 * i + 1] + dy + nc[1]) % nc[1];
+                int64_t cz = (C->cid[3 * i + 2] + dz + nc[2]) % nc[2];
+                int64_t c = (cz * nc[1] + cy) * nc[0] + cx;
+                for (int64_t j = C->head[c]; j >= 0; j = C->next[j]) {
+                    if (j == i) continue;
+                    double d[3];
+                    orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
+                    if (orc_r2(d) < rn2) row[cnt++] = j;
+                }
+            }
+    qsort(row, (size_t)cnt, sizeof(int64_t), cmp_i64);
+    return cnt;
+}
+
+/* Rows are independent, so the i loops may run in parallel (OpenMP build, bench.py's
+ * all-core leg): every row is the same set in the same (ascending) order either way. */
+int64_t orc_neigh_cells(int64_t n, const double *pos, const double box[3], double rn,
+                        int64_t *offsets, int64_t *nbr)
+{
+    int64_t nc[3];
+    if (orc_cell_dims(box, rn, nc) != 0) return -1;
+    orc_cells C;
+    cells_build(n, pos, box, nc, &C);
     double rn2 = rn * rn;
+    int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+#pragma omp parallel
+    {
+        int64_t *row = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < n; ++i) cnt[i] = cells_row(i, pos, box, rn2, &C, row);
+        free(row);
+    }
     int64_t tot = 0;
-    int64_t *scratch = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
     for (int64_t i = 0; i < n; ++i) {
         offsets[i] = tot;
-        int64_t cnt = 0;
-        for (int dz = -1; dz <= 1; ++dz)
-            for (int dy = -1; dy <= 1; ++dy)
-                for (int dx = -1; dx <= 1; ++dx) {
-                    int64_t cx = (cid[3 * i + 0] + dx + nc[0]) % nc[0];
-                    int64_t cy = (cid[3 * i + 1] + dy + nc[1]) % nc[1];
-                    int64_t cz = (cid[3 * i + 2] + dz + nc[2]) % nc[2];
-                    int64_t c = (cz * nc[1] + cy) * nc[0] + cx;
-                    for (int64_t j = head[c]; j >= 0; j = next[j]) {
-                        if (j == i) continue;
-                        double d[3];
-                        orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
-                        if (orc_r2(d) < rn2) scratch[cnt++] = j;
-                    }
-                }
-        qsort(scratch, (size_t)cnt, sizeof(int64_t), cmp_i64);
-        if (nbr)
-            for (int64_t k = 0; k < cnt; ++k) nbr[tot + k] = scratch[k];
-        tot += cnt;
+        tot += cnt[i];
     }
     offsets[n] = tot;
-    free(scratch);
-    free(cid);
-    free(next);
-    free(head);
+    if (nbr) {
+#pragma omp parallel
+        {
+            int64_t *row = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+#pragma omp for schedule(static)
+            for (int64_t i = 0; i < n; ++i) {
+                int64_t k = cells_row(i, pos, box, rn2, &C, row);
+                for (int64_t q = 0; q < k; ++q) nbr[offsets[i] + q] = row[q];
+            }
+            free(row);
+        }
+    }
+    free(cnt);
+    cells_free(&C);
     return tot;
 }
 
@@ -252,6 +313,7 @@ double orc_forces(int64_t n, const double *pos, const double box[3], const orc_l
                   double *F, double *e, double *S, double *A)
 {
     double *etmp = (double *)malloc(sizeof(double) * (n > 0 ? n : 1));
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         double Fi[3] = {0.0, 0.0, 0.0}, Ui = 0.0, Si = 0.0, Ai = 0.0;
         if (offsets == NULL) {
@@ -431,16 +493,77 @@ typedef struct {
     int64_t *off, *nbr;
 } orc_list;
 
+/* O4 into a fresh CSR: rows counted, then filled (the same rows as orc_neigh_cells). */
 static int build_list(int64_t n, const double *pos, const double box[3], double rn, orc_list *L)
 {
+    int64_t nc[3];
+    if (orc_cell_dims(box, rn, nc) != 0) return -1;
     free(L->off);
     free(L->nbr);
     L->off = (int64_t *)malloc(sizeof(int64_t) * (n + 1));
-    int64_t tot = orc_neigh_cells(n, pos, box, rn, L->off, NULL);
-    if (tot < 0) return -1;
+    orc_cells C;
+    cells_build(n, pos, box, nc, &C);
+    double rn2 = rn * rn;
+    int64_t **rows = (int64_t **)malloc(sizeof(int64_t *) * (n > 0 ? n : 1));
+    int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+#pragma omp parallel
+    {
+        int64_t *row = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+            cnt[i] = cells_row(i, pos, box, rn2, &C, row);
+            rows[i] = (int64_t *)malloc(sizeof(int64_t) * (cnt[i] > 0 ? cnt[i] : 1));
+            memcpy(rows[i], row, sizeof(int64_t) * cnt[i]);
+        }
+        free(row);
+    }
+    int64_t tot = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        L->off[i] = tot;
+        tot += cnt[i];
+    }
+    L->off[n] = tot;
     L->nbr = (int64_t *)malloc(sizeof(int64_t) * (tot > 0 ? tot : 1));
-    orc_neigh_cells(n, pos, box, rn, L->off, L->nbr);
+    for (int64_t i = 0; i < n; ++i) {
+        memcpy(L->nbr + L->off[i], rows[i], sizeof(int64_t) * cnt[i]);
+        free(rows[i]);
+    }
+    free(rows);
+    free(cnt);
+    cells_free(&C);
     return 0;
+}
+
+/* Missed pairs of a Verlet list at positions pos (validation; Eq. eqn:extended_cutoff,
+ * PAPER.md:406-416): for every i, #{j != i : r_ij^2 < rc^2} by brute force (O2 minimum
+ * image, as O3) minus #{j in NB(i) : r_ij^2 < rc^2}.  *particles = #{i : difference > 0},
+ * *pairs = the summed difference (ordered pairs the list does not serve). */
+void orc_missed(int64_t n, const double *pos, const double box[3], double rc, const int64_t *offsets,
+                const int64_t *nbr, int64_t *particles, int64_t *pairs)
+{
+    double rc2 = rc * rc;
+    int64_t np = 0, nm = 0;
+#pragma omp parallel for schedule(static) reduction(+ : np, nm)
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t truth = 0, listed = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double d[3];
+            orc_displacement(pos + 3 * i, pos + 3 * j, box, d);
+            if (orc_r2(d) < rc2) ++truth;
+        }
+        for (int64_t k = offsets[i]; k < offsets[i + 1]; ++k) {
+            double d[3];
+            orc_displacement(pos + 3 * i, pos + 3 * nbr[k], box, d);
+            if (orc_r2(d) < rc2) ++listed;
+        }
+        if (truth > listed) {
+            ++np;
+            nm += truth - listed;
+        }
+    }
+    *particles = np;
+    *pairs = nm;
 }
 
 /* Velocity Verlet, Algorithm alg:VelocityVerlet:
@@ -457,11 +580,14 @@ static int build_list(int64_t n, const double *pos, const double box[3], double 
  * no pair enters r_c from beyond rbar_c between rebuilds.
  *
  * pe_hist/ke_hist: nsteps/energy_every + 1 entries.  rebuild_steps: the MD
- * step index of each rebuild after init (cap entries).  Returns the number
- * of rebuilds, or -1 on error (box too small for cells). */
+ * step index of each rebuild after init (cap entries).  missed_particles /
+ * missed_pairs (NULL: off; nsteps + 1 entries, index = step): orc_missed at the
+ * positions each force of the step is evaluated on (list mode).  Returns the
+ * number of rebuilds, or -1 on error (box too small for cells). */
 int64_t orc_run(int64_t n, double *pos, double *vel, const double box[3], const orc_params *p,
                 int64_t nsteps, double *F, double *pe_hist, double *ke_hist,
-                int64_t *rebuild_steps, int64_t rebuild_cap)
+                int64_t *rebuild_steps, int64_t rebuild_cap, int64_t *missed_particles,
+                int64_t *missed_pairs)
 {
     double h = 0.5 * p->dt / p->mass;       /* dht_iMASS = dt/(2m) */
     double rn = p->lj.rc + p->delta;
@@ -503,6 +629,8 @@ int64_t orc_run(int64_t n, double *pos, double *vel, const double box[3], const 
             ++nreb;
             since = 0;
         }
+        if (missed_particles && missed_pairs && p->mode == 1)   /* validation, before line 7 */
+            orc_missed(n, pos, box, p->lj.rc, L.off, L.nbr, missed_particles + step, missed_pairs + step);
         pe = orc_forces(n, pos, box, &p->lj, p->mode == 1 ? L.off : NULL, L.nbr, F, NULL, NULL, NULL);
         for (int64_t i = 0; i < 3 * n; ++i) vel[i] = vel[i] + h * F[i];
         if (p->nu_dt > 0.0) orc_andersen(n, vel, p->seed, step, p->nu_dt, p->temp, p->mass);

@@ -481,6 +481,7 @@ extern "C" ljmd_status ljmd_dat_create(ljmd_ctx* c, int64_t ncomp, int64_t dtype
 
 extern "C" ljmd_status ljmd_dat_set(ljmd_ctx* c, int64_t h, const void* host) {
     TRY(check_ctx(c));
+    c->energy_current = false;   // engine velocities may change: no cached energies
     DslDat* d;
     TRY(dat_lookup(c, h, &d));
     if (!host) return set_err(c, LJMD_E_ARG, "ljmd_dat_set: NULL");
@@ -710,6 +711,7 @@ extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
     if (loop < 0 || loop >= (int64_t)c->loops.size() || !c->loops[loop] || !c->loops[loop]->alive)
         return set_err(c, LJMD_E_ARG, "bad loop handle %lld", (long long)loop);
     DslLoop& L = *c->loops[loop];
+    c->energy_current = false;   // a loop may write the engine's velocities
     if (L.kind == 1) TRY(dsl_slot_owner(c));
     DslParams p;
     std::memset(&p, 0, sizeof p);

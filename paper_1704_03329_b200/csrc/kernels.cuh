@@ -25,8 +25,8 @@ struct DevFlags {
     int max_nbr;                 // longest list at the last build
     int slots_needed;            // slot count required by the last binning
     int nonfinite_gid;           // smallest gid with a non-finite coordinate (INT_MAX: none)
-    int overlap_gid;             // smallest gid i with a partner at r^2 == 0 (INT_MAX: none)
-    int overlap_gid_j;
+    int val_error;               // validation: a listed in-range pair the fresh search missed
+    int rr_ovf;                  // list build: a bank-aware overflow run exceeded kRrRun
     int max_staged;              // largest tile staging count at the last build
     int migrate_gid;             // a particle that moved further than one cell plane (INT_MAX: none)
     int overflow;     // analysis capacity exceeded (ljmd_cna)
@@ -34,6 +34,8 @@ struct DevFlags {
     int n_grecv;                 // of those, images of received halo planes (nranks > 1)
     unsigned long long maxdisp2; // bits of max |x - x_build|^2 (non-negative double)
     unsigned long long total_nbr;
+    unsigned long long overlap_pair;   // min over coincident pairs of (gid_i << 32 | gid_j),
+                                       // gid_i < gid_j (~0: none) -- one atomic names both
 };
 
 // --------------------------------------------------------------------------- helpers
@@ -49,8 +51,7 @@ __global__ void k_reset_flags(DevFlags* fl) {
     memset(&f, 0, sizeof f);
     f.migrate_gid = INT_MAX;
     f.nonfinite_gid = INT_MAX;
-    f.overlap_gid = INT_MAX;
-    f.overlap_gid_j = -1;
+    f.overlap_pair = ~0ull;
     *fl = f;
 }
 __device__ __forceinline__ double4 ld256(const double4* p) {
@@ -89,12 +90,40 @@ __device__ __forceinline__ double r2_canon(double dx, double dy, double dz) {
 }
 
 // 1/a: MUFU.RCP64H seed (~2^-22) + one cubic Newton correction y(1 + e + e^2),
-// e = 1 - a y  (3 DFMA, error ~2^-64 before rounding).
+// e = 1 - a y  (3 DFMA, error ~2^-64 before rounding).  LJMD_RCP_QUAD: one quadratic
+// correction y(1 + e) (2 DFMA, relative error ~2^-44: ~1e-13 in F_i, inside the 1e-10 bar).
+#ifndef LJMD_RCP_QUAD
+#define LJMD_RCP_QUAD 1
+#endif
 __device__ __forceinline__ double rcp64(double a) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
     double e = fma(-a, y, 1.0);
+#if LJMD_RCP_QUAD
+    return fma(y, e, y);
+#else
     return fma(y, fma(e, e, e), y);
+#endif
+}
+
+// max of a non-negative u64 over the block, one atomicMax per block (a per-warp atomic on
+// one address serialises in L2: ~30 us for a million particles)
+__device__ __forceinline__ void block_atomic_max(unsigned long long v, unsigned long long* out) {
+    __shared__ unsigned long long sm[32];
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ob = __shfl_down_sync(0xffffffffu, v, o);
+        v = ob > v ? ob : v;
+    }
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : 0ull;
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_down_sync(0xffffffffu, v, o);
+            v = ob > v ? ob : v;
+        }
+        if (threadIdx.x == 0 && v) atomicMax(out, v);
+    }
 }
 
 // --------------------------------------------------------------------------- scan
@@ -252,12 +281,22 @@ __device__ __forceinline__ TileGeo tile_geo(const Geo& g, int tile) {
 
 // Wrap owned positions (R10) and bin them: cell_of[t] = owned-cell index, rank_in[t] = slot
 // inside the cell from the atomic counter (order fixed later by the gid sort).
+// vcopy / gcopy (single rank): the velocities and gids are copied aside here, so that the cell
+// sort can permute them in place (v[0], gid[0] are the only live copies: the rebuild flips no
+// buffer, and a captured step sequence keeps fixed pointers whether or not it rebuilds).
 __global__ void k_wrap_bin(int n_own, const double4* __restrict__ x, const int* __restrict__ own_slot,
                            Geo g, double4* __restrict__ xw, int* __restrict__ ocount,
                            int* __restrict__ cell_of, int* __restrict__ rank_in,
-                           const int* __restrict__ gid, DevFlags* fl) {
+                           const int* __restrict__ gid, DevFlags* fl, const double* __restrict__ v,
+                           double* __restrict__ vcopy, int* __restrict__ gcopy, int cap) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_own) return;
+    if (vcopy) {
+        vcopy[t] = v[t];
+        vcopy[t + cap] = v[t + cap];
+        vcopy[t + 2 * (size_t)cap] = v[t + 2 * (size_t)cap];
+        gcopy[t] = gid[t];
+    }
     double4 p = x[own_slot[t]];
     if (!(isfinite(p.x) && isfinite(p.y) && isfinite(p.z))) {
         atomicMin(&fl->nonfinite_gid, gid[t]);
@@ -359,10 +398,9 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
             for (int s = 0; s < m; ++s) {
                 const int ts = perm[b + s];
                 const double4 ps = xw[ts];
-                if (ts != t_old && ps.x == pk.x && ps.y == pk.y && ps.z == pk.z && gk < gid_old[ts]) {
-                    atomicMin(&fl->overlap_gid, gk);
-                    fl->overlap_gid_j = gid_old[ts];
-                }
+                if (ts != t_old && ps.x == pk.x && ps.y == pk.y && ps.z == pk.z && gk < gid_old[ts])
+                    atomicMin(&fl->overlap_pair,
+                              ((unsigned long long)(unsigned)gk << 32) | (unsigned)gid_old[ts]);
             }
         }
         if (!mine) continue;
@@ -706,94 +744,129 @@ struct NlistArgs {
     const int* slot_gid;
 };
 
-// One CTA per force tile (the same halo rows and local numbering as k_force): the fp32
-// mirror of the halo is staged in shared memory with cp.async, then thread per particle
-// walks its 9 stencil rows as local-index ranges.  Lanes of one cell walk the same j
-// sequence (broadcast LDS).  Output: build-order (stencil row, slot) local indices,
-// blocks of 8 entries written with 16-byte stores from registers.
+// One CTA per force tile (the same halo rows and local numbering as k_force).
+//   Prologue: the fp32 mirror of the tile's halo rows is staged in shared memory (cp.async),
+//   and three tables are built there: the tile's owned cells (first particle), per halo row
+//   and cell the local index where that cell's run starts (a particle's 3-cell stencil
+//   segment of row R is [seg[R][lx], seg[R][lx + 3])), and per cell kSub x sub-bins.
+//   Thread per particle: per stencil row, the x-window of the x-sorted segment comes from two
+//   sub-bin lookups (one sub-bin of margin each side: conservative against the fp32 rounding)
+//   instead of two binary searches; candidates outside a provably conservative band around
+//   rbar_c^2 are decided by their fp32 distance, those inside it by the canonical fp64 test
+//   (the oracle's decision).  Accepted entries are shifted into four registers and leave as
+//   one 16-byte store per 8 entries, in (stencil row, slot) order; the last block is padded
+//   with the tile's sentinel.
 #ifndef LJMD_BUILD_THREADS
 #define LJMD_BUILD_THREADS 480
 #endif
 constexpr int kBuildThreads = LJMD_BUILD_THREADS;
-
 #ifndef LJMD_BUILD_MINB
 #define LJMD_BUILD_MINB 4
 #endif
+constexpr int kTileCells = kTX * kTY * kTZ;
+constexpr int kSegW = kTX + 3;            // cell boundaries per halo row (ext x = 0 .. tx + 2)
+constexpr int kSub = 16;                  // x sub-bins per cell for the window lookup
+
+struct BuildSmem {
+    int cell_t0[kTileCells + 1];          // first particle (tile-relative) of each owned cell
+    int seg[kRowsMax][kSegW];             // local index where ext-x cell ex of row R starts
+    int delta[kRowsMax];                  // slot = local index + delta[R]
+    // sub[R][c][k]: first local index of cell c of row R whose fp32 x >= the sub-bin boundary
+    // b(c, k) = x0 + (kSub c + k) w_sub (k = 1 .. kSub - 1); k = 0 / kSub: the cell's bounds
+    unsigned short sub[kRowsMax][kTX + 2][kSub + 1];
+};
+
 __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(NlistArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ BuildSmem S;
     const int tile = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Geo& g = a.g;
     const TileGeo T = tile_geo(g, tile);
-    const int t0 = a.obegin[a.tile_oc0[tile]];
+    const int oc0 = a.tile_oc0[tile];
+    const int t0 = a.obegin[oc0];
     const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
-    const int rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
-    const int ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
+    const int ncell = T.tx * T.ty * T.tz;
     float4* sF = reinterpret_cast<float4*>(smem);
+    // (1) staging of the halo rows (fp32 mirror, 16 B per particle)
     for (int r = warp; r < T.R; r += kBuildThreads / 32) {
-        const int b0 = __shfl_sync(0xffffffffu, rb, r);
-        const int o0 = __shfl_sync(0xffffffffu, ro, r);
+        const int b0 = a.tr.begin[tile * kRowsMax + r];
+        const int o0 = a.tr.off[tile * (kRowsMax + 1) + r];
         const int len = a.tr.len[tile * kRowsMax + r];
         for (int k = lane; k < len; k += 32) {
             const unsigned d = (unsigned)__cvta_generic_to_shared(sF + o0 + k);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" :: "r"(d), "l"(a.xf + b0 + k) : "memory");
         }
     }
+    // (2) tables
+    for (int k = threadIdx.x; k <= ncell; k += kBuildThreads) S.cell_t0[k] = a.obegin[oc0 + k] - t0;
+    for (int k = threadIdx.x; k < T.R * (T.tx + 3); k += kBuildThreads) {
+        const int R = k / (T.tx + 3), ex = k % (T.tx + 3);
+        const int ry = R % (T.ty + 2), rz = R / (T.ty + 2);
+        const int rbeg = a.tr.begin[tile * kRowsMax + R];
+        const int roff = a.tr.off[tile * (kRowsMax + 1) + R];
+        const int ec = ((T.z0 + rz) * g.ey + (T.y0 + ry)) * g.ex + T.x0 + ex;
+        // ex = tx + 2 is the end of the row: begin of the last cell + its count
+        const int sb = ex < T.tx + 2 ? a.ebegin[ec] : a.ebegin[ec - 1] + a.ecount[ec - 1];
+        S.seg[R][ex] = roff + (sb - rbeg);
+        if (ex == 0) S.delta[R] = rbeg - roff;
+    }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    const float x0f = (float)((double)(T.x0 - 1) * g.w[0]);
+    const float wsub = (float)(g.w[0] / kSub), inv_wsub = 1.f / wsub;
+    for (int k = threadIdx.x; k < T.R * (T.tx + 2); k += kBuildThreads) {
+        const int R = k / (T.tx + 2), c = k % (T.tx + 2);
+        const int end = S.seg[R][c + 1];
+        int i = S.seg[R][c];
+        S.sub[R][c][0] = (unsigned short)i;
+        for (int q = 1; q < kSub; ++q) {
+            const float b = x0f + (float)(kSub * c + q) * wsub;
+            while (i < end && sF[i].x < b) ++i;
+            S.sub[R][c][q] = (unsigned short)i;
+        }
+        S.sub[R][c][kSub] = (unsigned short)end;
+    }
+    __syncthreads();
+
     const size_t stride = (size_t)a.n_pad;
-    const float thr_lo = a.thr_lo, thr_hi = a.thr_hi;
+    const float thr_lo = a.thr_lo, thr_hi = a.thr_hi, slop = a.slop_f;
     const int K = a.K;
     unsigned long long kk = 0ull;
+    int kmax = 0;
     for (int q = threadIdx.x; q < m; q += kBuildThreads) {
-        const int t = t0 + q;
-        const int si = a.own_slot[t];
-        int cx, cy, cz;
-        lex_xyz(g, g.lex_of_oc[a.ocell_of[t]], cx, cy, cz);
-        const double4 xi = a.x[si];
-        // own row (dy = dz = 0) gives the particle's own local index (self exclusion)
-        const int r0 = (cz + 1 - T.z0) * (T.ty + 2) + (cy + 1 - T.y0);
-        const int li = a.tr.off[tile * (kRowsMax + 1) + r0] + si - a.tr.begin[tile * kRowsMax + r0];
+        int ci = 0;
+        while (ci + 1 < ncell && S.cell_t0[ci + 1] <= q) ++ci;
+        const int lx = ci % T.tx, ly = (ci / T.tx) % T.ty, lz = ci / (T.tx * T.ty);
+        const int R0 = (lz + 1) * (T.ty + 2) + (ly + 1);
+        const int li = S.seg[R0][lx + 1] + (q - S.cell_t0[ci]);   // own local index
         const float4 fi = sF[li];
-        // entry k of particle t lives at ((k >> 3) * n_pad + t) * 8 + (k & 7) (blocked layout):
-        // the pending block is shifted in from the top of four registers (one funnel shift
-        // each) and leaves as one 16-byte store when it is full (K is a multiple of 8)
+        const int cy = T.y0 + ly, cz = T.z0 + lz;
+        const float ylo = a.ylo_f[cy], yhi = a.ylo_f[cy + 1];
+        const float zlo = a.zlo_f[cz], zhi = a.zlo_f[cz + 1];
+        const int t = t0 + q;
         uint4* outb = a.nbr8 + t;
         unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
         int k = 0;
-        for (int dz = -1; dz <= 1; ++dz) {
-            const float ddz = dz < 0 ? fi.z - a.zlo_f[cz] : (dz > 0 ? a.zlo_f[cz + 1] - fi.z : 0.f);
-            for (int dy = -1; dy <= 1; ++dy) {
-                const float ddy = dy < 0 ? fi.y - a.ylo_f[cy] : (dy > 0 ? a.ylo_f[cy + 1] - fi.y : 0.f);
-                // conservative x half-width of the sphere slice through this row
-                const float dyz2 = fmaxf(ddy - a.slop_f, 0.f) * fmaxf(ddy - a.slop_f, 0.f) +
-                                   fmaxf(ddz - a.slop_f, 0.f) * fmaxf(ddz - a.slop_f, 0.f);
-                if (dyz2 >= a.thr_hi) continue;
-                const float xw = sqrtf(a.thr_hi - dyz2) + a.slop_f;
-                const int r = (cz + 1 + dz - T.z0) * (T.ty + 2) + (cy + 1 + dy - T.y0);
-                const int rbeg = a.tr.begin[tile * kRowsMax + r];
-                const int roff = a.tr.off[tile * (kRowsMax + 1) + r];
-                const int e0 = ((cz + 1 + dz) * g.ey + (cy + 1 + dy)) * g.ex + cx;   // ext x = cx
-                int lo = roff + a.ebegin[e0] - rbeg;
-                int hi = roff + a.ebegin[e0 + 2] + a.ecount[e0 + 2] - rbeg;
-                // the row is sorted by x: first j with x_j >= x_i - xw, first j with x_j > x_i + xw
-                {
-                    const float xl = fi.x - xw, xh = fi.x + xw;
-                    int l0 = lo, l1 = hi;
-                    while (l0 < l1) {
-                        const int mid = (l0 + l1) >> 1;
-                        if (sF[mid].x < xl) l0 = mid + 1; else l1 = mid;
-                    }
-                    int h0 = l0, h1 = hi;
-                    while (h0 < h1) {
-                        const int mid = (h0 + h1) >> 1;
-                        if (sF[mid].x <= xh) h0 = mid + 1; else h1 = mid;
-                    }
-                    lo = l0;
-                    hi = h0;
-                }
-                // self exclusion by splitting the window around the own local index (li lies
-                // in the own row only) instead of a per-candidate test (528 -> 520 us on C2)
+        for (int rz = 0; rz < 3; ++rz) {
+            const float ddz = rz == 0 ? fi.z - zlo : (rz == 2 ? zhi - fi.z : 0.f);
+            const float dz2 = fmaxf(ddz - slop, 0.f) * fmaxf(ddz - slop, 0.f);
+            for (int ry = 0; ry < 3; ++ry) {
+                const float ddy = ry == 0 ? fi.y - ylo : (ry == 2 ? yhi - fi.y : 0.f);
+                const float dyz2 = fmaf(fmaxf(ddy - slop, 0.f), fmaxf(ddy - slop, 0.f), dz2);
+                if (dyz2 >= thr_hi) continue;
+                const float xw = sqrtf(thr_hi - dyz2) + slop;
+                const int R = (lz + rz) * (T.ty + 2) + (ly + ry);
+                const float xl = fi.x - xw, xh = fi.x + xw;
+                const int g0 = kSub * lx, g1 = kSub * (lx + 3);
+                int gl = (int)floorf((xl - x0f) * inv_wsub) - 1;
+                int gh = (int)floorf((xh - x0f) * inv_wsub) + 2;
+                gl = min(max(gl, g0), g1);
+                gh = min(max(gh, g0), g1);
+                const int cl = min(gl / kSub, lx + 2), ch = min(gh / kSub, lx + 2);
+                const int lo = S.sub[R][cl][gl - kSub * cl];
+                const int hi = S.sub[R][ch][gh - kSub * ch];
+                // self exclusion by splitting the window around the own local index
                 for (int part = 0; part < 2; ++part) {
                     const int j0 = part ? max(lo, li + 1) : lo;
                     const int j1 = part ? hi : min(hi, li);
@@ -803,16 +876,10 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
                         const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
                         if (r2f >= thr_hi) continue;
                         bool take = r2f < thr_lo;
-                        if (!take) {          // rare: decide in fp64 (the oracle's test); coincident
-                                              // particles are caught by the cell sort
-                            const int j = rbeg + (jl - roff);
-                            const double4 xj = a.x[j];
-                            const double r2 = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z);
-                            take = r2 < a.rn2;
-                            if (r2 == 0.0) {
-                                atomicMin(&a.fl->overlap_gid, a.slot_gid[si]);
-                                a.fl->overlap_gid_j = a.slot_gid[j];
-                            }
+                        if (!take) {   // rare: decide in fp64 on the canonical r^2 (the oracle's test)
+                            const double4 xi = a.x[li + S.delta[R0]];
+                            const double4 xj = a.x[jl + S.delta[R]];
+                            take = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z) < a.rn2;
                         }
                         if (take) {
                             w0 = __funnelshift_r(w0, w1, 16);
@@ -840,11 +907,17 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
             *outb = make_uint4(w0, w1, w2, w3);
         }
         a.ncount[t] = k;
-        atomicMax(&a.fl->max_nbr, k);
+        kmax = max(kmax, k);
         kk += (unsigned long long)k;
     }
-    for (int o = 16; o > 0; o >>= 1) kk += __shfl_down_sync(0xffffffffu, kk, o);
-    if (lane == 0 && kk) atomicAdd(&a.fl->total_nbr, kk);
+    for (int o = 16; o > 0; o >>= 1) {
+        kk += __shfl_down_sync(0xffffffffu, kk, o);
+        kmax = max(kmax, __shfl_down_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0 && kk) {
+        atomicAdd(&a.fl->total_nbr, kk);
+        atomicMax(&a.fl->max_nbr, kmax);
+    }
 }
 
 // --------------------------------------------------------------------------- bank-aware list order
@@ -1108,13 +1181,54 @@ __device__ __forceinline__ FPart fpart_load(const ForceArgs& a, int t) {
     P.cnt = a.ncount[t];
     P.xi = ld256(a.x + P.si);
     P.nb0 = P.cnt > 0 ? a.nbr[t] : make_uint4(0u, 0u, 0u, 0u);
-    if (P.cnt > 8) prefetch_l1(a.nbr + (size_t)a.n_pad + t);
     return P;
+}
+
+// List blocks 1.. of a particle stream into a per-thread ring of kRing 16-byte slots in
+// shared memory with cp.async (no registers held, kRing - 1 blocks of look-ahead): the
+// register prefetch of one block ahead left the loop head waiting on the list load (the top
+// long_scoreboard stall of the kernel).  Slot d of thread q: ring + (d * kForceThreads + q)
+// * 16, so a warp's 32 slots are one contiguous 512-byte run (conflict-free LDS.128).
+#ifndef LJMD_RING
+#define LJMD_RING 0        // 0: register prefetch of one block + L1 prefetch of the next (default)
+#endif
+constexpr int kRing = LJMD_RING;
+// the cutoff test r^2 < rc^2 on the integer bit patterns of the two positive doubles (the
+// same decision as DSETP, on the ALU pipe instead of the FP64 pipe)
+#ifndef LJMD_INT_CUT
+#define LJMD_INT_CUT 0
+#endif
+
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+__device__ __forceinline__ uint4 lds128(unsigned a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
+// blocks 1 .. kRing - 1 of particle P into the ring (one commit group per block)
+__device__ __forceinline__ void ring_start(const ForceArgs& a, const FPart& P, unsigned ring) {
+    if (kRing == 0) {
+        if (P.cnt > 8) prefetch_l1(a.nbr + (size_t)a.n_pad + P.t);
+        return;
+    }
+    const int nblk = (P.cnt + 7) >> 3;
+#pragma unroll
+    for (int d = 1; d < kRing; ++d) {
+        if (d < nblk) cp_async16(ring + (unsigned)(d * kForceThreads * 16), a.nbr + (size_t)d * a.n_pad + P.t);
+        cp_commit();
+    }
 }
 
 template <bool ENERGY, int MODE, bool CHECK>
 __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& P, const char* sPb,
-                                               double& epart, double& ke, unsigned long long& dbits) {
+                                               double& epart, double& ke, unsigned long long& dbits,
+                                               unsigned ring) {
     const int t = P.t;
     const double4 xi = P.xi;
     const uint4* nb = a.nbr + t;
@@ -1122,11 +1236,19 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
     double fx = 0.0, fy = 0.0, fz = 0.0, u = 0.0;
     const int nblk = (P.cnt + 7) >> 3;
     uint4 cur = P.nb0;
+#if LJMD_INT_CUT
+    const long long rc2b = __double_as_longlong(a.rc2);
+#endif
     for (int b = 0; b < nblk; ++b) {
-        // block b+2 into L1 now, block b+1 into registers; a short block is padded with the
-        // sentinel, so every entry is evaluated unpredicated
-        if (b + 2 < nblk) prefetch_l1(nb + (size_t)(b + 2) * stride);
-        const uint4 nxt = (b + 1 < nblk) ? nb[(size_t)(b + 1) * stride] : make_uint4(0u, 0u, 0u, 0u);
+        // a short block is padded with the sentinel, so every entry is evaluated unpredicated
+        uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
+        if (kRing == 0) {   // block b+2 into L1 now, block b+1 into registers
+            if (b + 2 < nblk) prefetch_l1(nb + (size_t)(b + 2) * stride);
+            if (b + 1 < nblk) nxt = nb[(size_t)(b + 1) * stride];
+        } else if (b > 0) {
+            cp_wait<(kRing > 0 ? kRing - 1 : 0)>();   // the group of block b has landed
+            cur = lds128(ring + (unsigned)((b % (kRing > 0 ? kRing : 1)) * kForceThreads * 16));
+        }
         const unsigned w4[4] = {cur.x, cur.y, cur.z, cur.w};
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -1139,7 +1261,11 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
             const double ir6 = ir4 * ir2;
             const double ir8 = ir4 * ir4;
             double gg = ir8 * fma(a.c12, ir6, a.nc6);
+#if LJMD_INT_CUT
+            const bool in = __double_as_longlong(r2) < rc2b;
+#else
             const bool in = r2 < a.rc2;
+#endif
             gg = in ? gg : 0.0;
             fx = fma(gg, dx, fx);
             fy = fma(gg, dy, fy);
@@ -1149,7 +1275,16 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
                 u += in ? v : 0.0;
             }
         }
-        cur = nxt;
+        // block b + kRing into the slot of block b (just consumed): blocks b + 1 .. b + kRing - 1
+        // stay in flight; block j >= 1 is commit group j - 1 of this particle
+        if (kRing == 0) {
+            cur = nxt;
+        } else {
+            const int bn = b + kRing;
+            if (bn < nblk)
+                cp_async16(ring + (unsigned)((bn % (kRing > 0 ? kRing : 1)) * kForceThreads * 16), nb + (size_t)bn * stride);
+            cp_commit();
+        }
     }
     if ((MODE & 3) == kStore) {
         a.fx[t] = fx; a.fy[t] = fy; a.fz[t] = fz;
@@ -1221,6 +1356,9 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     const int rl = lane < T.R ? a.tr.len[tile * kRowsMax + lane] : 0;
     const int total = __shfl_sync(0xffffffffu, ro, T.R);
     double* sP = reinterpret_cast<double*>(smem);   // packed {x, y, z} per staged particle
+    // list ring after the staging buffer (16-byte aligned)
+    const unsigned ring = ((unsigned)__cvta_generic_to_shared(smem) + 24u * (unsigned)(total + 1) + 15u) & ~15u;
+    const unsigned myring = ring + 16u * threadIdx.x;
     // one bulk copy per halo row (TMA engine), issued by warp 0, completion on an mbarrier
     __shared__ __align__(8) unsigned long long mbar;
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
@@ -1242,7 +1380,7 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         P.si = a.own_slot[t];
         P.cnt = a.ncount[t];
         P.nb0 = P.cnt > 0 ? a.nbr[t] : make_uint4(0u, 0u, 0u, 0u);
-        if (P.cnt > 8) prefetch_l1(a.nbr + (size_t)a.n_pad + t);
+        ring_start(a, P, myring);   // the list is not written by the force kernel
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
@@ -1275,7 +1413,10 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     }
 #endif
 #else
-    if (has) P = fpart_load(a, t0 + threadIdx.x);
+    if (has) {
+        P = fpart_load(a, t0 + threadIdx.x);
+        ring_start(a, P, myring);
+    }
 #endif
     __syncthreads();   // the barrier's initialisation and the sentinel are visible
     {
@@ -1288,18 +1429,13 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     const char* sPb = reinterpret_cast<const char*>(sP);
     double epart = 0.0, ke = 0.0;
     unsigned long long dbits = 0ull;
-    if (has) force_particle<ENERGY, MODE, CHECK>(a, P, sPb, epart, ke, dbits);
+    if (has) force_particle<ENERGY, MODE, CHECK>(a, P, sPb, epart, ke, dbits, myring);
     for (int q = threadIdx.x + kForceThreads; q < m; q += kForceThreads) {   // dense tiles only
         const FPart Q = fpart_load(a, t0 + q);
-        force_particle<ENERGY, MODE, CHECK>(a, Q, sPb, epart, ke, dbits);
+        ring_start(a, Q, myring);
+        force_particle<ENERGY, MODE, CHECK>(a, Q, sPb, epart, ke, dbits, myring);
     }
-    if (CHECK) {
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long ob = __shfl_down_sync(0xffffffffu, dbits, o);
-            dbits = ob > dbits ? ob : dbits;
-        }
-        if (lane == 0 && dbits) atomicMax(&a.fl->maxdisp2, dbits);
-    }
+    if (CHECK) block_atomic_max(dbits, &a.fl->maxdisp2);
     if (ENERGY) {
         const double pe = block_sum<kForceThreads>(epart, sh);
         const double k2 = block_sum<kForceThreads>(ke, sh);
@@ -1311,18 +1447,23 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
 }
 
 // opening half of a step() call: v += h F ; x += dt v  (in place, owned slots)
+// The pre-drift position is also written to the other buffer's owned slot (xprev), so that
+// at the top of every step the other buffer holds x(s-1) (the fused force epilogue keeps
+// that invariant on the following steps): the dangerous-build test of the next rebuild
+// reads it.
 template <bool CHECK>
 __global__ void k_kick_drift(int n_own, double4* __restrict__ x, const int* __restrict__ own_slot,
                              double* __restrict__ vx, double* __restrict__ vy, double* __restrict__ vz,
                              const double* __restrict__ fx, const double* __restrict__ fy,
                              const double* __restrict__ fz, double h, double dt,
                              const double4* __restrict__ xbuild, DevFlags* fl, Images im, Geo g,
-                             double* __restrict__ xp) {
+                             double* __restrict__ xp, double4* __restrict__ xprev) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long bits = 0ull;
     if (t < n_own) {
         int si = own_slot[t];
         double4 p = x[si];
+        xprev[si] = p;
         double a = __dadd_rn(vx[t], __dmul_rn(h, fx[t]));
         double b = __dadd_rn(vy[t], __dmul_rn(h, fy[t]));
         double c = __dadd_rn(vz[t], __dmul_rn(h, fz[t]));
@@ -1338,12 +1479,152 @@ __global__ void k_kick_drift(int n_own, double4* __restrict__ x, const int* __re
             bits = __double_as_longlong(r2_canon(p.x - q.x, p.y - q.y, p.z - q.z));
         }
     }
-    if (CHECK) {
-        for (int o = 16; o > 0; o >>= 1) {
-            unsigned long long ob = __shfl_down_sync(0xffffffffu, bits, o);
-            bits = ob > bits ? ob : bits;
+    if (CHECK) block_atomic_max(bits, &fl->maxdisp2);
+}
+
+// ---------------------------------------------------------------- rebuild certification
+// Dangerous builds (Eq. eqn:extended_cutoff; reading R7): the skin
+// argument certifies a list built at x_build for positions x as long as
+// 2 max_i |x_i - x_i(build)| <= delta (no pair can then have closed in from beyond rbar_c to
+// inside rc).  At each rebuild the displacement of the LAST step the old list served,
+// x(s-1) (the other position buffer, owned slots in the old layout), is reduced here; a
+// rebuild whose 4 max|dx|^2 > delta^2 is counted as dangerous (the fixed-Ns policy of the
+// paper's benchmark may have served uncertified steps; the displacement-checked policy
+// never does).
+__global__ void k_maxdisp(int n_own, const double4* __restrict__ xprev, const int* __restrict__ own_slot,
+                          const double4* __restrict__ xbuild, unsigned long long* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long bits = 0ull;
+    if (t < n_own) {
+        const double4 p = xprev[own_slot[t]];
+        const double4 q = xbuild[t];
+        bits = __double_as_longlong(r2_canon(p.x - q.x, p.y - q.y, p.z - q.z));
+    }
+    block_atomic_max(bits, out);
+}
+
+struct DevStats {                  // persistent device counters (not reset by k_reset_flags)
+    unsigned long long dangerous;  // rebuilds with 4 max|x(s-1) - x_build|^2 > delta^2
+    unsigned long long disp_bits;  // scratch: max |x(s-1) - x_build|^2 of the current rebuild
+    double max_disp2;              // largest such value seen since init / set_state
+};
+
+__global__ void k_dangerous(DevStats* st, double delta2) {
+    const double m2 = __longlong_as_double((long long)st->disp_bits);
+    if (4.0 * m2 > delta2) st->dangerous += 1ull;
+    if (m2 > st->max_disp2) st->max_disp2 = m2;
+    st->disp_bits = 0ull;
+}
+
+// Validation mode (ljmd_options.validate; single rank): for every step, the number of
+// ordered pairs the list misses -- pairs with canonical r^2 < rc^2 at the step's positions
+// (minimum image, reading R9) that are not served by the Verlet list -- counted per particle
+// as  #{j : r_ij^2 < rc^2} (fresh cell search) - #{list entries with r^2 < rc^2}.  An
+// independent cell binning of the current positions (cells of the engine's grid, width >=
+// rbar_c >= rc) provides the search; it never touches the engine's own layout.
+__global__ void k_val_bin(int n_own, const double4* __restrict__ x, const int* __restrict__ own_slot, Geo g,
+                          int* __restrict__ vcount, int* __restrict__ vcell, int* __restrict__ vrank) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_own) return;
+    const double4 p = x[own_slot[t]];
+    const double q[3] = {wrap_coord(p.x, g.L[0]), wrap_coord(p.y, g.L[1]), wrap_coord(p.z, g.L[2])};
+    int c[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        int k = (int)floor(__ddiv_rn(q[d], g.w[d]));
+        c[d] = k < 0 ? 0 : (k > g.nc[d] - 1 ? g.nc[d] - 1 : k);
+    }
+    const int cell = (c[2] * g.nc[1] + c[1]) * g.nc[0] + c[0];
+    vcell[t] = cell;
+    vrank[t] = atomicAdd(&vcount[cell], 1);
+}
+
+__global__ void k_val_scatter(int n_own, const double4* __restrict__ x, const int* __restrict__ own_slot,
+                              const int* __restrict__ vcell, const int* __restrict__ vrank,
+                              const int* __restrict__ vbegin, double4* __restrict__ vpos) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_own) return;
+    double4 p = x[own_slot[t]];
+    p.w = __longlong_as_double((long long)t);
+    vpos[vbegin[vcell[t]] + vrank[t]] = p;
+}
+
+// minimum-image displacement x_i - (x_j + s L) with s from d0 = x_i - x_j (reading R9, the
+// oracle's O2); the list side uses the stored image x_j + s L, the same rounding
+__device__ __forceinline__ double mi_d(double xi, double xj, double L) {
+    const double d0 = xi - xj;
+    const double s = d0 > 0.5 * L ? 1.0 : (d0 < -0.5 * L ? -1.0 : 0.0);
+    return __dsub_rn(xi, __dadd_rn(xj, __dmul_rn(s, L)));
+}
+
+struct ValArgs {
+    Geo g;
+    const double4* x;        // current positions (slot space)
+    const int* own_slot;
+    const int* vcell;
+    const int* vbegin;
+    const double4* vpos;     // positions sorted by validation cell, w = owned index
+    const unsigned short* nbr;   // blocked-8 list (build or bank-aware order: a set)
+    const int* ncount;
+    const int* ocell_of;
+    TileRows tr;
+    int n_own, n_pad;
+    double rc2;
+    int* vhist;              // [step][2]: particles with missed pairs, missed ordered pairs
+    int vslot;               // row of vhist for this step
+    DevFlags* fl;
+};
+
+__global__ void __launch_bounds__(256) k_val_count(ValArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    int miss = 0;
+    if (t < a.n_own) {
+        const Geo& g = a.g;
+        const double4 xi = a.x[a.own_slot[t]];
+        const int cell = a.vcell[t];
+        const int cx = cell % g.nc[0], cy = (cell / g.nc[0]) % g.nc[1], cz = cell / (g.nc[0] * g.nc[1]);
+        int truth = 0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int ex = (cx + dx + g.nc[0]) % g.nc[0], ey = (cy + dy + g.nc[1]) % g.nc[1],
+                              ez = (cz + dz + g.nc[2]) % g.nc[2];
+                    const int c2 = (ez * g.nc[1] + ey) * g.nc[0] + ex;
+                    for (int k = a.vbegin[c2]; k < a.vbegin[c2 + 1]; ++k) {
+                        const double4 xj = a.vpos[k];
+                        if ((int)__double_as_longlong(xj.w) == t) continue;
+                        const double r2 = r2_canon(mi_d(xi.x, xj.x, g.L[0]), mi_d(xi.y, xj.y, g.L[1]),
+                                                   mi_d(xi.z, xj.z, g.L[2]));
+                        truth += r2 < a.rc2;
+                    }
+                }
+        // the list side: entries resolved to slots through the tile's halo rows
+        int cx2, cy2, cz2;
+        lex_xyz(g, g.lex_of_oc[a.ocell_of[t]], cx2, cy2, cz2);
+        const int tile = tile_of_cell(g, cx2, cy2, cz2);
+        const int* rbeg = a.tr.begin + tile * kRowsMax;
+        const int* roff = a.tr.off + tile * (kRowsMax + 1);
+        const int n = a.ncount[t];
+        int listed = 0;
+        for (int k = 0; k < n; ++k) {
+            const int l = a.nbr[((size_t)(k >> 3) * a.n_pad + t) * 8 + (k & 7)];
+            int r = 0;
+            while (l >= roff[r + 1]) ++r;
+            const double4 xj = a.x[rbeg[r] + (l - roff[r])];
+            listed += r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z) < a.rc2;
         }
-        if ((threadIdx.x & 31) == 0) atomicMax(&fl->maxdisp2, bits);
+        miss = truth - listed;
+        if (miss < 0) atomicOr(&a.fl->val_error, 1);   // impossible: a listed pair the search missed
+    }
+    const int vs = a.vslot;
+    int np = miss > 0 ? 1 : 0, nm = miss > 0 ? miss : 0;
+    for (int o = 16; o > 0; o >>= 1) {
+        np += __shfl_down_sync(0xffffffffu, np, o);
+        nm += __shfl_down_sync(0xffffffffu, nm, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (np || nm)) {
+        atomicAdd(&a.vhist[2 * vs], np);
+        atomicAdd(&a.vhist[2 * vs + 1], nm);
     }
 }
 

@@ -139,6 +139,23 @@ struct ljmd_ctx {
     // ---- flags / staging
     DevFlags* d_fl = nullptr;
     DevFlags* h_fl = nullptr;      // pinned
+    DevStats* d_st = nullptr;      // persistent device counters (dangerous builds)
+    DevStats* h_st = nullptr;      // mapped page-locked readback of d_st
+    bool pdl_ok = false;           // the previous force launch may overlap the next (PDL): false
+                                   // right after a rebuild (the list was just written)
+    // ---- validation mode (ljmd_options.validate): missed pairs per step
+    int* vcount = nullptr;         // [n_cells + 1] (count, then exclusive begin)
+    int* vbegin = nullptr;
+    int* vcell = nullptr;
+    int* vrank = nullptr;
+    double4* vpos = nullptr;
+    int* vhist = nullptr;          // [vhist_cap][2]
+    int64_t vhist_cap = 0;
+    std::vector<int64_t> h_val;    // (step, particles with missed pairs, missed ordered pairs)
+    // energies of the current state are in hist/e (the last step of the previous ljmd_step
+    // call was a sample step, or the init sequence): ljmd_get_energy need not recompute
+    bool energy_current = false;
+    double cur_pe = 0.0, cur_ke = 0.0;
     int* h_slots = nullptr;        // pinned
     double* d_stage = nullptr;     // [3][own_cap] readback staging
     // overlapped host transfers (ljmd_stage_state / ljmd_get_positions_async)
@@ -431,7 +448,7 @@ ljmd_status alloc_owned(ljmd_ctx* c, int cap) {
     TRY(dalloc(c, &c->img_cnt, cap));
     TRY(dalloc(c, &c->img_off, (size_t)cap + 1));
     TRY(dalloc(c, &c->d_stage, (size_t)3 * cap));
-    if (c->opt.rebuild_check) TRY(dalloc(c, &c->xbuild, cap));
+    TRY(dalloc(c, &c->xbuild, cap));   // dangerous-build test (and the safe policy's check)
     c->n_fblocks = c->n_tiles;   // one force CTA per tile
     TRY(dalloc(c, &c->pe_part, c->n_fblocks));
     TRY(dalloc(c, &c->ke_part, c->n_fblocks));
@@ -484,6 +501,9 @@ ljmd_status alloc_list(ljmd_ctx* c, int K) {
 }
 
 // ------------------------------------------------------------------ kernels launchers
+// k_build_nlist dynamic shared memory: the staged fp32 halo
+inline size_t build_smem(const ljmd_ctx* c) { return 16 * (size_t)(c->max_staged + 1); }
+
 ljmd_status launch_nlist(ljmd_ctx* c) {
     NlistArgs a;
     a.g = c->geo;
@@ -524,7 +544,7 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     // fp32 pruning margin: position conversion (2^-24 X twice), face conversion, sqrt/fma
     // roundings -- 16 x the coordinate ulp plus an absolute floor
     a.slop_f = (float)(16.0 * std::ldexp(X, -23) + 1e-5);
-    k_build_nlist<<<c->n_tiles, kBuildThreads, sizeof(float4) * (size_t)c->max_staged, c->stream>>>(a);
+    k_build_nlist<<<c->n_tiles, kBuildThreads, build_smem(c), c->stream>>>(a);
     CKL();
     return LJMD_OK;
 }
@@ -581,6 +601,10 @@ ForceArgs force_args(ljmd_ctx* c) {
 }
 
 constexpr size_t kStageBytes = 24;   // packed {x, y, z} per staged particle
+// k_force dynamic shared memory: the staged halo (+ sentinel), then the list ring
+inline size_t force_smem(const ljmd_ctx* c) {
+    return (kStageBytes * (size_t)(c->max_staged + 1) + 15) / 16 * 16 + 16 * (size_t)kRing * kForceThreads;
+}
 
 template <bool E, int M, bool C>
 void force_launch(ljmd_ctx* c, const ForceArgs& a, int n_launch, cudaStream_t st = nullptr) {
@@ -589,16 +613,18 @@ void force_launch(ljmd_ctx* c, const ForceArgs& a, int n_launch, cudaStream_t st
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)n_launch);
     cfg.blockDim = dim3(kForceThreads);
-    cfg.dynamicSmemBytes = kStageBytes * (size_t)(c->max_staged + 1);
+    cfg.dynamicSmemBytes = force_smem(c);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    // no programmatic overlap with a predecessor that wrote the list, the counts or the
+    // halo-row tables (read before griddepcontrol.wait): only force -> force is overlapped
+    cfg.numAttrs = c->pdl_ok ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_force<E, M, C>, a);
 #else
-    k_force<E, M, C><<<n_launch, kForceThreads, kStageBytes * (size_t)(c->max_staged + 1), st>>>(a);
+    k_force<E, M, C><<<n_launch, kForceThreads, force_smem(c), st>>>(a);
 #endif
 }
 
@@ -780,6 +806,7 @@ ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check, bool ha
         else th ? force_all<false, DT, false>(c, a, h) : force_all<false, kKKD, false>(c, a, h);
     }
     CKL();
+    c->pdl_ok = true;
     if (c->opt.profile) {
         CK(cudaEventRecord(e1, c->stream));
         ++c->force_launches;
@@ -934,6 +961,17 @@ ljmd_status rebuild(ljmd_ctx* c) {
     // The decision depends only on the rebuild history, so it is deterministic and the same
     // on every rank.
     constexpr double kRrMinSteps = 10.0;
+    c->pdl_ok = false;   // the next force launch reads the new list: no programmatic overlap
+    if (c->last_build_step >= 0 && c->steps_done > c->last_build_step) {
+        // dangerous-build test on the last step the old list served (x(s-1) in the other
+        // position buffer, old layout), before the binning overwrites it
+        k_maxdisp<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->x[c->xc ^ 1], c->own_slot,
+                                                              c->xbuild, &c->d_st->disp_bits);
+        CKL();
+        TRY(allreduce(c, reinterpret_cast<double*>(&c->d_st->disp_bits), 1, true));
+        k_dangerous<<<1, 1, 0, c->stream>>>(c->d_st, c->opt.delta * c->opt.delta);
+        CKL();
+    }
     if (c->last_build_step >= 0 && c->steps_done > c->last_build_step)
         c->interval_ema = 0.5 * c->interval_ema + 0.5 * (double)(c->steps_done - c->last_build_step);
     else if (c->interval_ema == 0.0)
@@ -957,9 +995,17 @@ ljmd_status rebuild(ljmd_ctx* c) {
         gid_old = c->gs;
     }
     const int n = c->n_own;
+    const size_t oc = c->own_cap;
+    // single rank: v and gid copied aside (v[1], gid[1]) for the in-place permutation below
+    double* vcopy = c->split ? nullptr : c->v[1];
+    int* gcopy = c->split ? nullptr : c->gid[1];
     k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, xin, slot_in, c->geo, c->xw, c->ocount, c->cell_of,
-                                                    c->rank_in, gid_old, c->d_fl);
+                                                    c->rank_in, gid_old, c->d_fl, vo, vcopy, gcopy, (int)oc);
     CKL();
+    if (!c->split) {
+        vo = c->v[1];
+        gid_old = c->gid[1];
+    }
     if (c->split) {   // boundary-plane cell counts -> the neighbours' ghost planes
         const int npc = c->npc;
         k_plane_counts<<<nblk(2 * npc, 256), 256, 0, c->stream>>>(c->geo, c->ocount, c->send_cnt);
@@ -1005,18 +1051,16 @@ ljmd_status rebuild(ljmd_ctx* c) {
     c->n_slots = need;
     k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm);
     CKL();
-    const int on = c->oc_cur ^ 1;
-    double* vn = c->v[on];
-    const size_t oc = c->own_cap;
-    double4* xn = c->x[c->xc ^ 1];
+    // in place: the new layout goes into the current buffers (positions from xw, velocities
+    // and gids from the copies), so no buffer pointer changes at a rebuild
+    double* vn = c->v[0];
+    double4* xn = c->x[c->xc];
     TRY(dsl_before_sort(c, gid_old));
     k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
         c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, gid_old, c->xw, vo, vo + oc, vo + 2 * oc,
-        xn, c->xf, vn, vn + oc, vn + 2 * oc, c->gid[on], c->own_slot, c->ocell_of, c->slot_gid,
-        c->opt.rebuild_check ? c->xbuild : nullptr, c->xp[c->xc ^ 1], c->d_fl);
+        xn, c->xf, vn, vn + oc, vn + 2 * oc, c->gid[0], c->own_slot, c->ocell_of, c->slot_gid,
+        c->xbuild, c->xp[c->xc], c->d_fl);
     CKL();
-    c->oc_cur = on;
-    c->xc ^= 1;
     TRY(dsl_after_sort(c));
     if (c->split) {   // ghost planes: positions + gids of the neighbours' boundary planes
         k_plane_index<<<nblk((int64_t)2 * c->npc * 32, 256), 256, 0, c->stream>>>(c->geo, c->send_cnt,
@@ -1038,16 +1082,16 @@ ljmd_status rebuild(ljmd_ctx* c) {
     c->max_staged = c->h_fl->max_staged;
     c->n_gflat = c->h_fl->n_gflat;
     TRY(build_images(c));
-    if (16 * (size_t)(c->max_staged + 1) > kMaxStageSmem || c->max_staged > 65535)
+    if (build_smem(c) > kMaxStageSmem || force_smem(c) > kMaxStageSmem || c->max_staged > 65535)
         return set_err(c, LJMD_E_CAPACITY,
                        "a force tile needs %d staged particles (> %zu B of shared memory): density too high",
                        c->max_staged, kMaxStageSmem);
     TRY(launch_nlist(c));
     TRY(sync_flags(c));
     c->n_grecv = c->h_fl->n_grecv;
-    if (c->h_fl->overlap_gid != INT_MAX)
-        return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)", c->h_fl->overlap_gid,
-                       c->h_fl->overlap_gid_j);
+    if (c->h_fl->overlap_pair != ~0ull)
+        return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)",
+                       (int)(c->h_fl->overlap_pair >> 32), (int)(c->h_fl->overlap_pair & 0xffffffffu));
     if (c->h_fl->max_nbr > c->K) {
         int K = (c->h_fl->max_nbr * 5 / 4 + 8) / 8 * 8;
         TRY(alloc_list(c, K));
@@ -1074,6 +1118,48 @@ ljmd_status rebuild(ljmd_ctx* c) {
         CKL();
     }
 
+    return LJMD_OK;
+}
+
+// Validation mode: missed pairs of this step's positions (k_val_* in kernels.cuh), into row
+// vslot of vhist.  Single rank, full list (checked at init).
+ljmd_status validate_step(ljmd_ctx* c, int vslot) {
+    const Geo& g = c->geo;
+    const int ncell = g.nc[0] * g.nc[1] * g.nc[2];
+    if (!c->vcount) {
+        TRY(dalloc(c, &c->vcount, ncell));
+        TRY(dalloc(c, &c->vbegin, (size_t)ncell + 1));
+        TRY(dalloc(c, &c->vcell, c->own_cap));
+        TRY(dalloc(c, &c->vrank, c->own_cap));
+        TRY(dalloc(c, &c->vpos, c->own_cap));
+    }
+    const int n = c->n_own;
+    CK(cudaMemsetAsync(c->vcount, 0, sizeof(int) * (size_t)ncell, c->stream));
+    k_val_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, g, c->vcount, c->vcell, c->vrank);
+    CKL();
+    TRY(scan(c, c->vcount, ncell, c->vbegin));
+    k_val_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, c->vcell, c->vrank, c->vbegin,
+                                                       c->vpos);
+    CKL();
+    ValArgs a;
+    a.g = g;
+    a.x = c->x[c->xc];
+    a.own_slot = c->own_slot;
+    a.vcell = c->vcell;
+    a.vbegin = c->vbegin;
+    a.vpos = c->vpos;
+    a.nbr = reinterpret_cast<const unsigned short*>(c->use_rr ? c->nbr8b : c->nbr8);
+    a.ncount = c->ncount;
+    a.ocell_of = c->ocell_of;
+    a.tr = TileRows{c->tr_begin, c->tr_off, c->tr_len};
+    a.n_own = n;
+    a.n_pad = c->n_pad;
+    a.rc2 = c->rc * c->rc;
+    a.vhist = c->vhist;
+    a.vslot = vslot;
+    a.fl = c->d_fl;
+    k_val_count<<<nblk(n, 256), 256, 0, c->stream>>>(a);
+    CKL();
     return LJMD_OK;
 }
 
@@ -1181,12 +1267,39 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const 
     c->n_rebuilds = 0;
     c->rebuild_steps.clear();
     c->h_hist.clear();
+    c->h_val.clear();
+    c->last_build_step = -1;
+    CK(cudaMemsetAsync(c->d_st, 0, sizeof(DevStats), c->stream));
     TRY(rebuild(c));
     TRY(ensure_hist(c, 1));
     TRY(launch_force(c, true, kStore, false));
     TRY(finalize_energy(c, c->hist));
     TRY(allreduce(c, c->hist, 2, false));
     TRY(pull_hist(c, 1));
+    c->cur_pe = c->h_hist[0];
+    c->cur_ke = c->h_hist[1];
+    c->energy_current = true;
+    return LJMD_OK;
+}
+
+// PE, KE and e_i of the current state: reused when the last step of the previous
+// ljmd_step call (or the init sequence) sampled them, otherwise one Energy force pass
+ljmd_status energy_now(ljmd_ctx* c) {
+    if (c->energy_current) return LJMD_OK;
+    TRY(launch_force(c, true, kStore, false));
+    TRY(ensure_hist(c, 1));
+    double* tmp = c->hist + 2 * (c->hist_cap - 1);
+    TRY(finalize_energy(c, tmp));
+    TRY(allreduce(c, tmp, 2, false));
+    if (c->h_histm_cap < 1) {
+        CK(cudaHostAlloc(&c->h_histm, sizeof(double) * 2, cudaHostAllocMapped));
+        c->h_histm_cap = 1;
+    }
+    TRY(to_host(c, c->h_histm, tmp, sizeof(double) * 2));
+    CK(cudaStreamSynchronize(c->stream));
+    c->cur_pe = c->h_histm[0];
+    c->cur_ke = c->h_histm[1];
+    c->energy_current = true;
     return LJMD_OK;
 }
 
@@ -1306,6 +1419,10 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         delete c;
         return set_err(nullptr, LJMD_E_ARG, "ljmd_init: newton3 needs nranks = 1 (no reverse halo)");
     }
+    if (o.validate && (o.nranks > 1 || o.split_self || o.newton3)) {
+        delete c;
+        return set_err(nullptr, LJMD_E_ARG, "ljmd_init: validate needs nranks = 1 and the full list");
+    }
     auto fail = [&](ljmd_status s) {
         g_init_error = c->msg.empty() ? std::string("ljmd_init failed") : c->msg;
         ljmd_destroy(c);
@@ -1354,6 +1471,8 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     }
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
+        cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess ||
+        cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostAlloc(&c->h_fl, sizeof(DevFlags), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostAlloc(&c->h_slots, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
         set_err(c, LJMD_E_CUDA, "flag allocation failed");
@@ -1476,6 +1595,15 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
     TRY(ensure_hist(c, nsteps / std::max<int64_t>(ee, 1) + 2));
     int64_t nsamp = 0;
     const int64_t first_launch = c->force_launches;
+    const int64_t step0 = c->steps_done;
+    c->energy_current = false;
+    if (c->opt.validate) {
+        if (c->vhist_cap < nsteps) {
+            TRY(dalloc(c, &c->vhist, (size_t)2 * nsteps));
+            c->vhist_cap = nsteps;
+        }
+        CK(cudaMemsetAsync(c->vhist, 0, sizeof(int) * 2 * (size_t)nsteps, c->stream));
+    }
     const double delta2 = c->opt.delta * c->opt.delta;
     // Alg. alg:VelocityVerlet line 6 of the first step (uses the stored F)
     if (check) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
@@ -1486,11 +1614,11 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         if (check)
             k_kick_drift<true><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
                 c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc]);
+                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
         else
             k_kick_drift<false><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
                 c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc]);
+                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
         CKL();
     }
     for (int64_t s = 1; s <= nsteps; ++s) {
@@ -1531,7 +1659,9 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         const bool sample = ee > 0 && (c->steps_done % ee) == 0;
         const bool last = s == nsteps;
         if (check && !last) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
+        if (c->opt.validate) TRY(validate_step(c, (int)(s - 1)));
         TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last, halo_pending));
+        if (last) c->energy_current = sample && ee > 0;
         if (sample) {
             TRY(finalize_energy(c, c->hist + 2 * nsamp));
             TRY(allreduce(c, c->hist + 2 * nsamp, 2, false));
@@ -1540,8 +1670,24 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         if (!last) c->xc ^= 1;
     }
     TRY(pull_hist(c, nsamp));
+    if (c->energy_current) {
+        c->cur_pe = c->h_hist[c->h_hist.size() - 2];
+        c->cur_ke = c->h_hist[c->h_hist.size() - 1];
+    }
     TRY(collect_profile(c, first_launch));
     TRY(sync_flags(c));
+    if (c->opt.validate) {
+        if (c->h_fl->val_error)
+            return set_err(c, LJMD_E_STATE, "validation: a listed in-range pair was not found by the cell search");
+        std::vector<int> h((size_t)2 * nsteps);
+        CK(cudaMemcpyAsync(h.data(), c->vhist, sizeof(int) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int64_t k = 0; k < nsteps; ++k) {
+            c->h_val.push_back(step0 + k + 1);
+            c->h_val.push_back(h[2 * k]);
+            c->h_val.push_back(h[2 * k + 1]);
+        }
+    }
     return LJMD_OK;
 }
 
@@ -1592,25 +1738,15 @@ ljmd_status ljmd_get_positions(ljmd_ctx* c, double* out, int64_t wrapped) {
 ljmd_status ljmd_get_particle_energy(ljmd_ctx* c, double* out) {
     TRY(check_ctx(c));
     if (!out) return LJMD_E_ARG;
-    TRY(launch_force(c, true, kStore, false));
+    TRY(energy_now(c));
     return readback(c, c->e, 1, out);
 }
 
 ljmd_status ljmd_get_energy(ljmd_ctx* c, double* pe, double* ke) {
     TRY(check_ctx(c));
-    TRY(launch_force(c, true, kStore, false));
-    TRY(ensure_hist(c, 1));
-    double* tmp = c->hist + 2 * (c->hist_cap - 1);
-    TRY(finalize_energy(c, tmp));
-    TRY(allreduce(c, tmp, 2, false));
-    if (c->h_histm_cap < 1) {
-        CK(cudaHostAlloc(&c->h_histm, sizeof(double) * 2, cudaHostAllocMapped));
-        c->h_histm_cap = 1;
-    }
-    TRY(to_host(c, c->h_histm, tmp, sizeof(double) * 2));
-    CK(cudaStreamSynchronize(c->stream));
-    if (pe) *pe = c->h_histm[0];
-    if (ke) *ke = c->h_histm[1];
+    TRY(energy_now(c));
+    if (pe) *pe = c->cur_pe;
+    if (ke) *ke = c->cur_ke;
     return LJMD_OK;
 }
 
@@ -1684,6 +1820,27 @@ ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s) {
     s->force_ms = c->force_ms;
     s->energy_samples = (int64_t)c->h_hist.size() / 2;
     s->kernel_launches = c->kernel_launches;
+    TRY(to_host(c, c->h_st, c->d_st, sizeof(DevStats)));
+    CK(cudaStreamSynchronize(c->stream));
+    s->dangerous_builds = (int64_t)c->h_st->dangerous;
+    s->max_build_disp = std::sqrt(c->h_st->max_disp2);
+    const int64_t nv = (int64_t)c->h_val.size() / 3;
+    s->validated_steps = nv;
+    for (int64_t k = 0; k < nv; ++k) {
+        s->missed_particle_steps += c->h_val[3 * k + 1];
+        s->missed_pairs += c->h_val[3 * k + 2];
+        s->max_missed_particles = std::max(s->max_missed_particles, c->h_val[3 * k + 1]);
+    }
+    return LJMD_OK;
+}
+
+ljmd_status ljmd_get_validation(ljmd_ctx* c, int64_t* out, int64_t cap, int64_t* count) {
+    TRY(check_ctx(c));
+    if (!c->opt.validate) return set_err(c, LJMD_E_ARG, "ljmd_get_validation: validation mode is off");
+    const int64_t nv = (int64_t)c->h_val.size() / 3;
+    if (count) *count = nv;
+    for (int64_t k = 0; out && k < std::min(nv, cap); ++k)
+        for (int q = 0; q < 3; ++q) out[3 * k + q] = c->h_val[3 * k + q];
     return LJMD_OK;
 }
 
@@ -1695,7 +1852,11 @@ const char* ljmd_last_error(const ljmd_ctx* c) {
 void ljmd_destroy(ljmd_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    // a step that failed after queueing the halo exchange on aux_stream may still have NCCL
+    // work or copies in flight on it: drain both streams before the comm and buffers go
+    if (c->aux_stream) cudaStreamSynchronize(c->aux_stream);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     void* ptrs[] = {c->x[0], c->x[1], c->xf, c->slot_gid, c->v[0], c->v[1], c->gid[0], c->gid[1],
                     c->own_slot, c->ocell_of, c->F, c->e, c->xbuild, c->xw, c->cell_of, c->rank_in, c->perm,
                     c->ocount, c->obegin, c->ecount, c->ebegin, c->ecell_src, c->gc_dst, c->gc_src, c->gc_shift,
@@ -1717,6 +1878,10 @@ void ljmd_destroy(ljmd_ctx* c) {
     if (c->h_tot) cudaFreeHost(c->h_tot);
     delete c->tr;
     if (c->h_fl) cudaFreeHost(c->h_fl);
+    if (c->h_st) cudaFreeHost(c->h_st);
+    for (void* p : {(void*)c->d_st, (void*)c->vcount, (void*)c->vbegin, (void*)c->vcell, (void*)c->vrank,
+                    (void*)c->vpos, (void*)c->vhist})
+        if (p) cudaFree(p);
     if (c->h_histm) cudaFreeHost(c->h_histm);
     if (c->h_slots) cudaFreeHost(c->h_slots);
     for (auto e : c->ev) cudaEventDestroy(e);

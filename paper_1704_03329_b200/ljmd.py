@@ -27,6 +27,7 @@ STATUS = {0: "LJMD_OK", -1: "LJMD_E_ARG", -2: "LJMD_E_BOX", -3: "LJMD_E_NONFINIT
 EXPORTS = ("ljmd_default_options", "ljmd_init", "ljmd_set_state", "ljmd_step", "ljmd_get_forces",
            "ljmd_get_positions", "ljmd_get_velocities", "ljmd_get_particle_energy", "ljmd_get_energy",
            "ljmd_get_energy_history", "ljmd_get_neighbours", "ljmd_get_rebuild_steps", "ljmd_get_stats",
+           "ljmd_get_validation",
            "ljmd_last_error", "ljmd_destroy", "ljmd_version", "ljmd_plan_cells", "ljmd_plan_slab",
            "ljmd_measure_fp64_peak", "ljmd_nccl_unique_id", "ljmd_boa", "ljmd_cna", "ljmd_set_thermostat", "ljmd_set_profile",
            "ljmd_stage_state", "ljmd_get_positions_async", "ljmd_wait_transfers",
@@ -48,7 +49,8 @@ class Options(ctypes.Structure):
                 ("rank", ctypes.c_int64), ("nranks", ctypes.c_int64),
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int64), ("list_order", ctypes.c_int64),
-                ("split_self", ctypes.c_int64), ("newton3", ctypes.c_int64)]
+                ("split_self", ctypes.c_int64), ("newton3", ctypes.c_int64),
+                ("validate", ctypes.c_int64)]
 
 
 class Stats(ctypes.Structure):
@@ -58,7 +60,10 @@ class Stats(ctypes.Structure):
                 ("total_neighbours", ctypes.c_int64), ("n_cells", ctypes.c_int64 * 3),
                 ("regrows", ctypes.c_int64), ("force_launches", ctypes.c_int64),
                 ("force_ms", ctypes.c_double), ("energy_samples", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("dangerous_builds", ctypes.c_int64),
+                ("max_build_disp", ctypes.c_double), ("validated_steps", ctypes.c_int64),
+                ("missed_pairs", ctypes.c_int64), ("missed_particle_steps", ctypes.c_int64),
+                ("max_missed_particles", ctypes.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -98,6 +103,7 @@ def load(path: str = None):
         "ljmd_get_neighbours": ([vp, _I, _I, ctypes.c_int64], ctypes.c_int),
         "ljmd_get_rebuild_steps": ([vp, _I, ctypes.c_int64, _I], ctypes.c_int),
         "ljmd_get_stats": ([vp, ctypes.POINTER(Stats)], ctypes.c_int),
+        "ljmd_get_validation": ([vp, _I, ctypes.c_int64, _I], ctypes.c_int),
         "ljmd_last_error": ([vp], ctypes.c_char_p),
         "ljmd_destroy": ([vp], None),
         "ljmd_version": ([], ctypes.c_char_p),
@@ -122,6 +128,8 @@ def load(path: str = None):
         "ljmd_loop_free": ([vp, ctypes.c_int64], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
+        if not hasattr(lib, name) and "LJMD_LIB" in os.environ:
+            continue   # an older A/B build of the library (measurement runs only)
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
@@ -353,6 +361,15 @@ class LJMD:
         out = np.zeros(cnt.value, dtype=np.int64)
         self._ck(self._lib.ljmd_get_rebuild_steps(self._h, out.ctypes.data_as(_I), cnt.value,
                                                   ctypes.byref(cnt)))
+        return out
+
+    def validation(self):
+        """Validation mode: [k, 3] int64 rows (step, particles with a missed pair, missed
+        ordered pairs) for every validated step since init / set_state."""
+        cnt = ctypes.c_int64()
+        self._ck(self._lib.ljmd_get_validation(self._h, None, 0, ctypes.byref(cnt)))
+        out = np.zeros((cnt.value, 3), dtype=np.int64)
+        self._ck(self._lib.ljmd_get_validation(self._h, out.ctypes.data_as(_I), cnt.value, ctypes.byref(cnt)))
         return out
 
     def stats(self):
