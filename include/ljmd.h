@@ -94,6 +94,15 @@ typedef struct {
                                 keeps a list past the skin guarantee of
                                Eq. eqn:extended_cutoff when particles move
                                fast: this measures what that costs in missed interactions.  */
+    int64_t graphs;         /* 1 (default): on one rank (no newton3 / validate / profile /
+                               thermostat / DSL data), ljmd_step runs as a captured CUDA graph:
+                               the rebuild decision (fixed Ns or the displacement check) and the
+                               capacity checks are taken on the device, no host round trip per
+                               step or per rebuild; a capacity shortfall resumes on the eager
+                               path at that step.  0: eager launches (host decides each step). */
+    int64_t tight_caps;     /* testing: after init, shrink the slot, staging and list capacities
+                               to exactly what the initial state needs (the next larger rebuild
+                               then exercises the capacity checks); 0 (default)               */
 } ljmd_options;
 
 typedef struct {
@@ -121,6 +130,9 @@ typedef struct {
     int64_t missed_pairs;      /* ordered pairs with r < rc not in the list, summed over steps */
     int64_t missed_particle_steps;  /* (particle, step) with at least one missed pair          */
     int64_t max_missed_particles;   /* largest number of such particles in one step           */
+    int64_t graph_calls;       /* ljmd_step calls run as a captured graph                       */
+    int64_t graph_aborts;      /* of those, resumed eagerly after a device capacity check      */
+    int64_t graphs_cached;     /* captured step graphs currently instantiated                  */
 } ljmd_stats;
 
 /* Fill *o with the defaults listed above. */

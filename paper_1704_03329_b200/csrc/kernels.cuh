@@ -19,6 +19,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// 1: nranks > 1, the boundary force tiles wait in-kernel on a flag the halo stream releases
+// (one launch over every tile); hangs with NCCL on one GPU, so off
+#ifndef LJMD_HALO_GATE
+#define LJMD_HALO_GATE 0
+#endif
+
 namespace ljmd {
 
 struct DevFlags {
@@ -27,6 +33,8 @@ struct DevFlags {
     int nonfinite_gid;           // smallest gid with a non-finite coordinate (INT_MAX: none)
     int val_error;               // validation: a listed in-range pair the fresh search missed
     int rr_ovf;                  // list build: a bank-aware overflow run exceeded kRrRun
+    int halo_timeout;            // a boundary force tile waited too long for the halo
+    int pad2;
     int max_staged;              // largest tile staging count at the last build
     int migrate_gid;             // a particle that moved further than one cell plane (INT_MAX: none)
     int overflow;     // analysis capacity exceeded (ljmd_cna)
@@ -46,14 +54,71 @@ __global__ void k_copy_words(const unsigned* __restrict__ src, unsigned* dst, in
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
-__global__ void k_reset_flags(DevFlags* fl) {
+// keep_errors: the error fields (non-finite / migration gids, coincident pair, validation)
+// survive, so a failure in one rebuild of a captured step sequence is still seen when the
+// host reads the flags at the end of the call
+__global__ void k_reset_flags(DevFlags* fl, int keep_errors) {
     DevFlags f;
     memset(&f, 0, sizeof f);
-    f.migrate_gid = INT_MAX;
-    f.nonfinite_gid = INT_MAX;
-    f.overlap_pair = ~0ull;
+    f.migrate_gid = keep_errors ? fl->migrate_gid : INT_MAX;
+    f.nonfinite_gid = keep_errors ? fl->nonfinite_gid : INT_MAX;
+    f.overlap_pair = keep_errors ? fl->overlap_pair : ~0ull;
+    f.val_error = keep_errors ? fl->val_error : 0;
     *fl = f;
 }
+
+// ------------------------------------------------------------------------ graph-mode control
+// Step control of a captured step sequence (ljmd_step on one rank): the
+// rebuild decision of reading R7 is taken on the device and gates the rebuild through a
+// conditional graph node, so no step waits for the host.  Capacities are checked on the
+// device as well; a shortfall aborts the rest of the sequence (every later kernel of it
+// returns at once) and the host resumes at that step with regrown buffers.
+struct DevCtl {
+    int abort;        // 0 running; 1 slots short (nothing mutated); 2 staging / list width short
+                      // (new layout in place, list incomplete)
+    int abort_step;   // step of the call (1-based) whose rebuild aborted
+    int nreb;         // rebuilds in this call (steps in rstep[])
+    int nsamp;        // energy samples written in this call
+    int step;         // step of the last decision
+    int since;        // steps since the last rebuild (persists across calls; set by the host)
+};
+
+// One step's decision: since += 1; due = forced || since >= Ns || (check && 4 max|dx|^2 >
+// delta^2), the last from the previous step's epilogue (non-negative doubles compare as
+// their bit patterns); the maximum is cleared for this step's epilogue.
+// step_now: the step of the call (1-based) this decision belongs to
+__global__ void k_decide(DevCtl* ctl, DevFlags* fl, int ns, int check, int forced, double delta2, int* rstep,
+                         int step_now, cudaGraphConditionalHandle h) {
+    if (ctl->abort) {
+        cudaGraphSetConditional(h, 0u);
+        return;
+    }
+    ctl->step = step_now;
+    ctl->since += 1;
+    bool due = forced || ctl->since >= ns;
+    if (!due && check) due = 4.0 * __longlong_as_double((long long)fl->maxdisp2) > delta2;
+    fl->maxdisp2 = 0ull;
+    if (due) {
+        ctl->since = 0;
+        rstep[ctl->nreb++] = ctl->step;
+    }
+    cudaGraphSetConditional(h, due ? 1u : 0u);
+}
+
+__global__ void k_set_since(DevCtl* ctl, int since) { ctl->since = since; }
+
+// capacity checks inside a captured rebuild: stage 1 (before anything is permuted) the slot
+// count, stage 2 (after the tile tables) the staging size, stage 3 the list width
+__global__ void k_check_caps(DevCtl* ctl, const DevFlags* fl, const int* need_slots, int slot_cap, int stage_cap,
+                             int K, int stage, cudaGraphConditionalHandle h) {
+    bool ok = !ctl->abort;
+    if (ok && stage == 1 && *need_slots > slot_cap) { ctl->abort = 1; ok = false; }
+    if (ok && stage == 2 && fl->max_staged > stage_cap) { ctl->abort = 2; ok = false; }
+    if (ok && stage == 3 && fl->max_nbr > K) { ctl->abort = 2; ok = false; }
+    if (!ok && ctl->abort_step == 0) ctl->abort_step = ctl->step;
+    if (stage < 3) cudaGraphSetConditional(h, ok ? 1u : 0u);
+}
+
 __device__ __forceinline__ double4 ld256(const double4* p) {
     double4 r;
     asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -498,7 +563,8 @@ __global__ void __launch_bounds__(256) k_ghost_flat(int n, const int4* __restric
 // (nranks > 1) are listed apart (grecv) and refreshed after each exchange.
 struct Images {
     const int* off;    // [n_own + 1]; null: the kernel writes no images
-    const int2* e;     // {dst slot, shift code}
+    const int2* e;     // {dst slot, shift code}; code bit 7: a send-area entry (nranks > 1),
+                       // written as double4 only
 };
 
 __device__ __forceinline__ void write_images(const Images& im, int t, const Geo& g, double4* __restrict__ x,
@@ -511,8 +577,23 @@ __device__ __forceinline__ void write_images(const Images& im, int t, const Geo&
                                        __dadd_rn(p.y, (double)(((d.y >> 2) & 3) - 1) * g.L[1]),
                                        __dadd_rn(p.z, (double)(((d.y >> 4) & 3) - 1) * g.L[2]), 0.0);
         st256(x + d.x, q);
-        st_packed(xp, d.x, q);
+        if (!(d.y & 0x80)) st_packed(xp, d.x, q);
     }
+}
+
+// release of a step's halo to the gated boundary tiles of the force launch
+__global__ void k_set_flag(unsigned* flag, unsigned seq) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flag), "r"(seq) : "memory");
+}
+
+// ghost planes arrive as double4 (32-byte records: every slot is aligned for the transfer);
+// the force kernel stages packed positions, written here for the two planes
+__global__ void k_xp_from_x(int b0, int n0, int b1, int n1, const double4* __restrict__ x, double* __restrict__ xp) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n0 + n1) return;
+    const int sl = k < n0 ? b0 + k : b1 + (k - n0);
+    st_packed(xp, sl, ld256(x + sl));
 }
 
 __global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __restrict__ slot2t) {
@@ -522,11 +603,13 @@ __global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __res
 
 // FILL = false: count the images of each owned source (and move received-plane images to
 // grecv); FILL = true: place them (the counts return to zero)
+// n_dev != null: the ghost count is read on the device (captured rebuilds: grid over a cap)
 template <bool FILL>
 __global__ void k_img_build(int n, const int4* __restrict__ gflat, int n_slots, const int* __restrict__ slot2t,
                             int* __restrict__ cnt, const int* __restrict__ off, int2* __restrict__ img,
-                            int4* __restrict__ grecv, DevFlags* fl) {
+                            int4* __restrict__ grecv, DevFlags* fl, const int* n_dev) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n_dev) n = *n_dev;
     if (i >= n) return;
     const int4 e = gflat[i];
     if (e.y < n_slots) {
@@ -653,6 +736,53 @@ __global__ void k_pack(int n, const int* __restrict__ idx, const double4* __rest
     double4 p = ld256(x + s);
     p.w = (double)slot_gid[s];
     st256(out + k, p);
+}
+
+// ------------------------------------------------------------- direct-landing halo (nranks > 1)
+// The boundary planes travel every step in the RECEIVER's ghost-plane layout: the whole
+// extended z-plane (the owned plane plus its periodic x/y images, cells in (iy, ix) order,
+// particles in slot order) with the z shift of the periodic seam already added, so the
+// receive lands straight in the receiver's ghost slots (positions and packed positions) and
+// no unpack or image pass runs.  The sender's copy lives in a send area after the slot range
+// of the position buffers and is written by the kernels that move the particles (force
+// epilogue, opening kick-drift), through the same per-particle image lists as the periodic
+// images: one entry {send-area index, source slot, shift code} per boundary particle image.
+
+// counts per extended plane cell: side 0 = bottom owned plane (-> lower neighbour), 1 = top
+__global__ void k_plane_ext_counts(Geo g, const int* __restrict__ ecount, int* __restrict__ cnt) {
+    const int np = g.ex * g.ey;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= 2 * np) return;
+    const int side = k / np, c = k % np, ix = c % g.ex, iy = c / g.ex;
+    const int ox = (ix - 1 + g.nc[0]) % g.nc[0], oy = (iy - 1 + g.nc[1]) % g.nc[1];
+    const int iz = side == 0 ? 1 : g.nzl;
+    cnt[k] = ecount[(iz * g.ey + (oy + 1)) * g.ex + (ox + 1)];
+}
+
+// one warp per extended plane cell: image entries {base + offset, source slot, shift code}
+// appended to the ghost-image list (gflat) from which the per-particle image lists are built.
+// zs[side]: z shift of the plane as the receiver sees it (-1, 0, +1 in units of Lz).
+__global__ void k_send_map(Geo g, const int* __restrict__ ebegin, const int* __restrict__ ecount,
+                           const int* __restrict__ off, int base, int zs0, int zs1, int4* __restrict__ gflat,
+                           int cap, DevFlags* fl) {
+    const int np = g.ex * g.ey;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= 2 * np) return;
+    const int side = warp / np, c = warp % np, ix = c % g.ex, iy = c / g.ex;
+    const int ox = (ix - 1 + g.nc[0]) % g.nc[0], oy = (iy - 1 + g.nc[1]) % g.nc[1];
+    const int sx = ix == 0 ? -1 : (ix == g.nc[0] + 1 ? 1 : 0);
+    const int sy = iy == 0 ? -1 : (iy == g.nc[1] + 1 ? 1 : 0);
+    const int sz = side == 0 ? zs0 : zs1;
+    const int iz = side == 0 ? 1 : g.nzl;
+    const int ec = (iz * g.ey + (oy + 1)) * g.ex + (ox + 1);
+    const int sb = ebegin[ec], m = ecount[ec];
+    int at = 0;
+    if (lane == 0 && m) at = atomicAdd(&fl->n_gflat, m);
+    at = __shfl_sync(0xffffffffu, at, 0);
+    const int code = (sx + 1) | ((sy + 1) << 2) | ((sz + 1) << 4) | 0x80;   // bit 7: send area
+    for (int k = lane; k < m; k += 32)   // past cap: the host regrows and rebuilds again
+        if (at + k < cap) gflat[at + k] = make_int4(base + off[warp] + k, sb + k, code, 0);
 }
 
 // received plane particles: gid from the w component (at build)
@@ -1062,6 +1192,12 @@ struct ForceArgs {
     const double4* xbuild;   // displacement check (may be null)
     Images im;               // ghost images written with x(n+1) (kKKD)
     int tile_base;           // first tile of this launch
+    int seg0, gap;           // tiles seg0.. of the launch are shifted by gap (two ranges, one launch)
+    // gated halo (nranks > 1): one launch over every tile, interior tiles first; the two
+    // boundary tile layers (whose halos hold received planes) wait in-kernel for the halo
+    const unsigned* halo_flag;   // null: no gating
+    unsigned halo_seq;           // the value the flag reaches once this step's halo has landed
+    int nint, layer;             // interior tiles, tiles per z layer
     DevFlags* fl;
     int n_own, n_pad;
     double rc2, c12, nc6, a12, na6, a0;   // nc6 = -c6, na6 = -a6 (fold into DFMA operands)
@@ -1071,6 +1207,8 @@ struct ForceArgs {
     double nu_dt, sd;                     // collision probability per step, sqrt(T/m)
     unsigned long long seed;
     long long step;                       // 1-based index of the step this launch completes
+    const DevCtl* ctl;                    // captured steps: skip everything after an abort
+    int parts;                            // CTAs per tile (small systems: more CTAs than tiles)
 };
 
 // Philox4x32-10 (Salmon et al., SC'11): counter-based, so the draws of (gid, step) do not
@@ -1245,6 +1383,9 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
         if (kRing == 0) {   // block b+2 into L1 now, block b+1 into registers
             if (b + 2 < nblk) prefetch_l1(nb + (size_t)(b + 2) * stride);
             if (b + 1 < nblk) nxt = nb[(size_t)(b + 1) * stride];
+#if LJMD_LOADFENCE
+            __syncwarp(__activemask());   // keeps ptxas from sinking the load to the loop end
+#endif
         } else if (b > 0) {
             cp_wait<(kRing > 0 ? kRing - 1 : 0)>();   // the group of block b has landed
             cur = lds128(ring + (unsigned)((b % (kRing > 0 ? kRing : 1)) * kForceThreads * 16));
@@ -1342,11 +1483,40 @@ template <bool ENERGY, int MODE, bool CHECK>
 __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double sh[kForceThreads / 32];
-    const int tile = a.tile_base + blockIdx.x;   // a launch may cover a range of tiles
+    // a launch covers a range of tiles, a.parts CTAs per tile (each stages the whole tile
+    // halo and takes a share of its particles: small systems get enough CTAs for the chip)
+#if LJMD_FPARTS_OFF
+    const int part = 0;
+    const int ti = blockIdx.x;
+#else
+    const int part = blockIdx.x % a.parts;
+    const int ti = blockIdx.x / a.parts;
+#endif
+#if LJMD_SEG_OFF
+    int tile = a.tile_base + ti;
+    const bool gated = false;
+#else
+    int tile = a.tile_base + ti + (ti >= a.seg0 ? a.gap : 0);
+    const bool gated = a.halo_flag && ti >= a.nint;
+#endif
+    // gated order: interior tiles [L, T - L) first, then the lower layer [0, L), then the upper
+    // layer [T - L, T) -- whose launch index is its own tile index
+#if !LJMD_SEG_OFF
+    if (a.halo_flag) tile = ti < a.nint ? a.layer + ti : (ti - a.nint < a.layer ? ti - a.nint : ti);
+#endif
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // captured steps: skip everything after an aborted rebuild, before any table of it is
+    // read (the flag is written only by rebuild kernels, never by a force launch)
+    if (a.ctl && a.ctl->abort) return;
     const TileGeo T = tile_geo(a.g, tile);
-    const int t0 = a.obegin[a.tile_oc0[tile]];
-    const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
+    const int tt0 = a.obegin[a.tile_oc0[tile]];
+    const int mt = a.obegin[a.tile_oc0[tile + 1]] - tt0;
+    // shares in multiples of 16 particles: a particle's thread keeps its residue mod 16 (the
+    // bank-aware list order is relative to it)
+    const int per = ((mt + a.parts - 1) / a.parts + 15) & ~15;
+    const int qb = min(part * per, mt);
+    const int t0 = tt0 + qb;
+    const int m = min(qb + per, mt) - qb;
     const bool has = (int)threadIdx.x < m;
     FPart P;
     // halo rows of this tile: lane r holds (begin, offset, length) of row r -- tables of the
@@ -1383,6 +1553,28 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         ring_start(a, P, myring);   // the list is not written by the force kernel
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+#if LJMD_HALO_GATE
+    if (warp == 0 && gated) {   // boundary tile: wait until this step's halo has landed
+        if (lane == 0) {
+            unsigned v = 0u;
+            long long spins = 0;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.halo_flag) : "memory");
+                if ((int)(v - a.halo_seq) >= 0) break;
+                if (++spins > (1ll << 26)) {   // ~10 s: report instead of hanging the device
+                    atomicOr(&a.fl->halo_timeout, 1);
+                    break;
+                }
+                __nanosleep(128);
+            }
+            // the staging below reads the received planes through the async (TMA) proxy
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+    }
+#else
+    (void)gated;
 #endif
     if (warp == 0) {   // the copies go out as soon as the positions may be read
         unsigned sz = 0u;
@@ -1440,8 +1632,8 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         const double pe = block_sum<kForceThreads>(epart, sh);
         const double k2 = block_sum<kForceThreads>(ke, sh);
         if (threadIdx.x == 0) {
-            a.pe_part[tile] = pe;
-            a.ke_part[tile] = k2;
+            a.pe_part[tile * a.parts + part] = pe;
+            a.ke_part[tile * a.parts + part] = k2;
         }
     }
 }
@@ -1629,9 +1821,14 @@ __global__ void __launch_bounds__(256) k_val_count(ValArgs a) {
 }
 
 // fixed-order final reduction of the per-block partials -> out[0] = PE, out[1] = KE
+// ctl != null (captured steps): out is the history base, the sample index comes from ctl
 __global__ void k_finalize_energy(const double* __restrict__ pe_part, const double* __restrict__ ke_part,
-                                  int nb, double* __restrict__ out) {
+                                  int nb, double* __restrict__ out, DevCtl* ctl) {
     __shared__ double sh[32];
+    if (ctl) {
+        if (ctl->abort) return;
+        out += 2 * ctl->nsamp;
+    }
     double p = 0.0, k = 0.0;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) {
         p += pe_part[i];
@@ -1643,6 +1840,7 @@ __global__ void k_finalize_energy(const double* __restrict__ pe_part, const doub
     if (threadIdx.x == 0) {
         out[0] = ps;
         out[1] = ks;
+        if (ctl) ctl->nsamp += 1;
     }
 }
 

@@ -15,12 +15,16 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
 using namespace ljmd;
 
 static constexpr size_t kMaxStageSmem = 200 * 1024;   // dynamic smem cap for the tile staging
+#ifndef LJMD_STAGE_MARGIN
+#define LJMD_STAGE_MARGIN 8   // stage_cap = max_staged (1 + 1/MARGIN) + 16 when it grows
+#endif
 
 namespace {
 
@@ -131,6 +135,7 @@ struct ljmd_ctx {
     double* pe_part = nullptr;
     double* ke_part = nullptr;
     int n_fblocks = 0;
+    int fparts = 1;                   // force CTAs per tile
     double* hist = nullptr;   // [hist_cap][2]
     double* h_histm = nullptr;   // mapped page-locked readback of hist
     int64_t h_histm_cap = 0;
@@ -156,6 +161,25 @@ struct ljmd_ctx {
     // call was a sample step, or the init sequence): ljmd_get_energy need not recompute
     bool energy_current = false;
     double cur_pe = 0.0, cur_ke = 0.0;
+    // ---- graph mode (single rank): ljmd_step captured into CUDA graphs, rebuild decided and
+    // capacity-checked on the device
+    DevCtl* d_ctl = nullptr;
+    DevCtl* h_ctl = nullptr;          // mapped readback
+    int* d_rstep = nullptr;           // rebuild steps of the current call (1-based within it)
+    int* h_rstep = nullptr;           // mapped readback
+    int64_t rstep_cap = 0;
+    int stage_cap = 0;                // staged particles per tile the force/build launches are sized for
+    struct GraphEntry {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ex = nullptr;
+        int64_t launches = 0;         // kernels outside the conditional rebuild bodies
+    };
+    std::map<std::string, GraphEntry> graphs;
+    bool capturing = false;           // launches go into a graph being captured
+    cudaStream_t cap_stream[3] = {nullptr, nullptr, nullptr};   // capture of nested rebuild bodies
+    int64_t graph_calls = 0, graph_aborts = 0;
+    int64_t rebuild_kernels = 0;      // kernels of one captured rebuild (for the launch count)
+    int64_t call_nsamp = 0;           // energy samples of the current ljmd_step call
     int* h_slots = nullptr;        // pinned
     double* d_stage = nullptr;     // [3][own_cap] readback staging
     // overlapped host transfers (ljmd_stage_state / ljmd_get_positions_async)
@@ -199,6 +223,17 @@ struct ljmd_ctx {
     int* iota = nullptr;
     int* stay_t = nullptr;        // compaction order of the stayers (migrate)
     int* h_tot = nullptr;         // pinned: send/recv plane totals
+    // direct-landing halo (per step): send area after the slot range of x / xp, in the
+    // receiver's ghost-plane layout; receives land in the ghost planes
+    int send_extra = 0;           // entries of x / xp / gflat / img beyond slot_cap
+    int* pl_cnt = nullptr;        // [2 ex ey] extended-plane cell counts (bottom, top)
+    int* pl_off = nullptr;        // [2 ex ey + 1]
+    int* h_pl = nullptr;          // mapped: {send total, bottom part, lower ghost begin, lower
+                                  //          ghost end, upper ghost begin, upper ghost end}
+    int area[2] = {0, 0};         // send-area entries for the lower / upper neighbour
+    int gbeg[2] = {0, 0}, glen[2] = {0, 0};   // my lower / upper ghost plane: slots
+    unsigned* halo_flag = nullptr;    // gated boundary tiles: released per step by the halo stream
+    unsigned halo_seq = 0;
 };
 
 ljmd_status dsl_before_sort(ljmd_ctx* c, const int* gid_old);
@@ -249,8 +284,17 @@ ljmd_status set_err(ljmd_ctx* c, ljmd_status s, const char* fmt, ...) {
         if (s_ != LJMD_OK) return s_;   \
     } while (0)
 
+void drop_graphs(ljmd_ctx* c) {
+    for (auto& kv : c->graphs) {
+        if (kv.second.ex) cudaGraphExecDestroy(kv.second.ex);
+        if (kv.second.g) cudaGraphDestroy(kv.second.g);
+    }
+    c->graphs.clear();
+}
+
 template <class T>
 ljmd_status dalloc(ljmd_ctx* c, T** p, size_t n) {
+    if (c) drop_graphs(c);   // captured step graphs hold raw pointers
     if (*p) cudaFree(*p);
     *p = nullptr;
     if (n == 0) n = 1;
@@ -296,7 +340,7 @@ ljmd_status sync_flags(ljmd_ctx* c) {
 }
 
 ljmd_status reset_flags(ljmd_ctx* c) {
-    k_reset_flags<<<1, 1, 0, c->stream>>>(c->d_fl);
+    k_reset_flags<<<1, 1, 0, c->stream>>>(c->d_fl, 1);
     CKL();
     return LJMD_OK;
 }
@@ -449,7 +493,9 @@ ljmd_status alloc_owned(ljmd_ctx* c, int cap) {
     TRY(dalloc(c, &c->img_off, (size_t)cap + 1));
     TRY(dalloc(c, &c->d_stage, (size_t)3 * cap));
     TRY(dalloc(c, &c->xbuild, cap));   // dangerous-build test (and the safe policy's check)
-    c->n_fblocks = c->n_tiles;   // one force CTA per tile
+    // force CTAs per tile: enough CTAs for two per SM on small systems (C1: 14 tiles -> 8 parts)
+    c->fparts = c->newton3 ? 1 : std::max(1, std::min(8, (2 * 148 + c->n_tiles - 1) / c->n_tiles));
+    c->n_fblocks = c->n_tiles * c->fparts;
     TRY(dalloc(c, &c->pe_part, c->n_fblocks));
     TRY(dalloc(c, &c->ke_part, c->n_fblocks));
     if (c->newton3) {
@@ -462,7 +508,7 @@ ljmd_status alloc_owned(ljmd_ctx* c, int cap) {
 ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     double4* nx[2] = {nullptr, nullptr};
     for (int b = 0; b < 2; ++b) {
-        cudaError_t e = cudaMalloc(&nx[b], sizeof(double4) * (size_t)cap);
+        cudaError_t e = cudaMalloc(&nx[b], sizeof(double4) * ((size_t)cap + c->send_extra));
         if (e != cudaSuccess) {
             cudaGetLastError();
             if (nx[0]) cudaFree(nx[0]);
@@ -479,10 +525,11 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     }
     TRY(dalloc(c, &c->xf, cap));
     TRY(dalloc(c, &c->slot_gid, cap));
-    TRY(dalloc(c, &c->gflat, cap));
-    for (int b = 0; b < 2; ++b) TRY(dalloc(c, &c->xp[b], (size_t)3 * cap + 8));   // +8: bulk-copy overrun
+    TRY(dalloc(c, &c->gflat, (size_t)cap + c->send_extra));
+    for (int b = 0; b < 2; ++b)
+        TRY(dalloc(c, &c->xp[b], (size_t)3 * ((size_t)cap + c->send_extra) + 8));   // +8: bulk-copy overrun
     TRY(dalloc(c, &c->slot2t, cap));
-    TRY(dalloc(c, &c->img, cap));
+    TRY(dalloc(c, &c->img, (size_t)cap + c->send_extra));
     TRY(dalloc(c, &c->grecv, cap));
     if (c->newton3 || c->dsl_on) {
         TRY(dalloc(c, &c->slot_t, cap));
@@ -502,7 +549,7 @@ ljmd_status alloc_list(ljmd_ctx* c, int K) {
 
 // ------------------------------------------------------------------ kernels launchers
 // k_build_nlist dynamic shared memory: the staged fp32 halo
-inline size_t build_smem(const ljmd_ctx* c) { return 16 * (size_t)(c->max_staged + 1); }
+inline size_t build_smem(const ljmd_ctx* c) { return 16 * (size_t)(c->stage_cap + 1); }
 
 ljmd_status launch_nlist(ljmd_ctx* c) {
     NlistArgs a;
@@ -597,13 +644,22 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.sd = c->thermo_sd;
     a.seed = c->thermo_seed;
     a.step = c->steps_done;
+    a.ctl = c->capturing ? c->d_ctl : nullptr;
+    a.parts = c->fparts;
+    a.tile_base = 0;
+    a.seg0 = INT_MAX;
+    a.gap = 0;
+    a.halo_flag = nullptr;
+    a.halo_seq = 0;
+    a.nint = 0;
+    a.layer = 0;
     return a;
 }
 
 constexpr size_t kStageBytes = 24;   // packed {x, y, z} per staged particle
 // k_force dynamic shared memory: the staged halo (+ sentinel), then the list ring
 inline size_t force_smem(const ljmd_ctx* c) {
-    return (kStageBytes * (size_t)(c->max_staged + 1) + 15) / 16 * 16 + 16 * (size_t)kRing * kForceThreads;
+    return (kStageBytes * (size_t)(c->stage_cap + 1) + 15) / 16 * 16 + 16 * (size_t)kRing * kForceThreads;
 }
 
 template <bool E, int M, bool C>
@@ -611,7 +667,7 @@ void force_launch(ljmd_ctx* c, const ForceArgs& a, int n_launch, cudaStream_t st
     if (!st) st = c->stream;
 #if LJMD_PDL
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)n_launch);
+    cfg.gridDim = dim3((unsigned)(n_launch * c->fparts));
     cfg.blockDim = dim3(kForceThreads);
     cfg.dynamicSmemBytes = force_smem(c);
     cfg.stream = st;
@@ -624,7 +680,7 @@ void force_launch(ljmd_ctx* c, const ForceArgs& a, int n_launch, cudaStream_t st
     cfg.numAttrs = c->pdl_ok ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_force<E, M, C>, a);
 #else
-    k_force<E, M, C><<<n_launch, kForceThreads, force_smem(c), st>>>(a);
+    k_force<E, M, C><<<n_launch * c->fparts, kForceThreads, force_smem(c), st>>>(a);
 #endif
 }
 
@@ -739,9 +795,12 @@ ljmd_status launch_half(ljmd_ctx* c, bool energy, int mode, bool check, cudaEven
 }
 
 template <bool E, int M, bool C>
-void force_range(ljmd_ctx* c, ForceArgs a, int first, int count, cudaStream_t st = nullptr) {
+void force_range(ljmd_ctx* c, ForceArgs a, int first, int count, cudaStream_t st = nullptr, int seg0 = INT_MAX,
+                 int gap = 0) {
     if (count <= 0) return;
     a.tile_base = first;
+    a.seg0 = seg0;
+    a.gap = gap;
     force_launch<E, M, C>(c, a, count, st);
 }
 
@@ -756,10 +815,23 @@ void force_all(ljmd_ctx* c, const ForceArgs& a, bool halo_pending) {
         force_range<E, M, C>(c, a, 0, c->n_tiles);
         return;
     }
+#if LJMD_HALO_GATE
+    // one launch, interior tiles first; the boundary tiles wait in-kernel for the halo flag
+    // (no programmatic overlap: an early-started next launch must not hold the SMs the halo
+    // stream needs while boundary tiles wait)
+    ForceArgs g = a;
+    g.halo_flag = c->halo_flag;
+    g.halo_seq = c->halo_seq;
+    g.nint = c->n_tiles - 2 * layer;
+    g.layer = layer;
+    c->pdl_ok = false;
+    force_range<E, M, C>(c, g, 0, c->n_tiles);
+#else
     force_range<E, M, C>(c, a, layer, c->n_tiles - 2 * layer);
     cudaStreamWaitEvent(c->stream, c->ev_halo, 0);
-    force_range<E, M, C>(c, a, 0, layer);
-    force_range<E, M, C>(c, a, c->n_tiles - layer, layer);
+    // both boundary layers in one launch (one wave instead of two)
+    force_range<E, M, C>(c, a, 0, 2 * layer, nullptr, layer, c->n_tiles - 2 * layer);
+#endif
 }
 
 ljmd_status launch_force(ljmd_ctx* c, bool energy, int mode, bool check, bool halo_pending = false) {
@@ -858,6 +930,57 @@ ljmd_status halo_exchange(ljmd_ctx* c, cudaStream_t st = nullptr) {
                     e * c->n_recv[0], rx + c->n_recv[0], e * c->n_recv[1], st);
 }
 
+// Per step (nranks > 1): the send areas (written by the kernels that moved the particles)
+// go to the neighbours and land in their ghost planes, positions and packed positions; the
+// posting order pairs correctly also when both neighbours are one rank (p = 2).
+ljmd_status halo_direct(ljmd_ctx* c, cudaStream_t st = nullptr) {
+    // double4 records (32 B: every slot aligned for the transfer); the packed copy the force
+    // kernel stages is written for the two received planes right after
+    if (!st) st = c->stream;
+    double4* X = c->x[c->xc];
+    const size_t base = (size_t)c->slot_cap;
+    const size_t e4 = sizeof(double4);
+    const size_t a0 = (size_t)c->area[0], a1 = (size_t)c->area[1];
+    std::vector<Xfer> sends{{c->hi_rank, X + base + a0, e4 * a1}, {c->lo_rank, X + base, e4 * a0}};
+    std::vector<Xfer> recvs{{c->lo_rank, X + c->gbeg[0], e4 * c->glen[0]}, {c->hi_rank, X + c->gbeg[1], e4 * c->glen[1]}};
+    std::string err;
+    if (!c->tr->exchange(st, sends, recvs, err)) return set_err(c, LJMD_E_NCCL, "%s", err.c_str());
+    const int nr = c->glen[0] + c->glen[1];
+    if (nr > 0) {
+        k_xp_from_x<<<nblk(nr, 256), 256, 0, st>>>(c->gbeg[0], c->glen[0], c->gbeg[1], c->glen[1], X, c->xp[c->xc]);
+        CKL();
+    }
+    return LJMD_OK;
+}
+
+// At a rebuild (nranks > 1): the send map of the direct-landing halo, appended to the image
+// list gflat (so the kernels that move a boundary particle also write its send-area copies),
+// and the send / ghost-plane extents (read by the host at the rebuild's next synchronisation).
+ljmd_status send_map(ljmd_ctx* c) {
+    const Geo& g = c->geo;
+    const int np = g.ex * g.ey;
+    if (!c->pl_cnt) {
+        TRY(dalloc(c, &c->pl_cnt, 2 * (size_t)np));
+        TRY(dalloc(c, &c->pl_off, 2 * (size_t)np + 1));
+        CK(cudaHostAlloc(&c->h_pl, sizeof(int) * 8, cudaHostAllocMapped));
+    }
+    k_plane_ext_counts<<<nblk(2 * np, 256), 256, 0, c->stream>>>(g, c->ecount, c->pl_cnt);
+    CKL();
+    TRY(scan(c, c->pl_cnt, 2 * np, c->pl_off));
+    const int zs0 = g.z0 == 0 ? 1 : 0, zs1 = g.z0 + g.nzl == g.nc[2] ? -1 : 0;
+    k_send_map<<<nblk((int64_t)2 * np * 32, 256), 256, 0, c->stream>>>(g, c->ebegin, c->ecount, c->pl_off, c->slot_cap,
+                                                                       zs0, zs1, c->gflat,
+                                                                       c->slot_cap + c->send_extra, c->d_fl);
+    CKL();
+    TRY(to_host(c, c->h_pl + 0, c->pl_off + 2 * np, sizeof(int)));
+    TRY(to_host(c, c->h_pl + 1, c->pl_off + np, sizeof(int)));
+    TRY(to_host(c, c->h_pl + 2, c->ebegin, sizeof(int)));
+    TRY(to_host(c, c->h_pl + 3, c->ebegin + np, sizeof(int)));
+    TRY(to_host(c, c->h_pl + 4, c->ebegin + (size_t)(g.nzl + 1) * np, sizeof(int)));
+    TRY(to_host(c, c->h_pl + 5, c->ebegin + c->n_ecell, sizeof(int)));
+    return LJMD_OK;
+}
+
 ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
     GhostCells gc{c->gc_dst, c->gc_src, c->gc_shift, c->n_gcell};
     int blocks = nblk((int64_t)c->n_gcell * 32, 256);
@@ -873,34 +996,26 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
     return LJMD_OK;
 }
 
-// images of received halo planes, after each exchange (nranks > 1)
-ljmd_status refresh_recv(ljmd_ctx* c, cudaStream_t st = nullptr) {
-    if (c->n_grecv > 0) {
-        k_ghost_flat<<<nblk(c->n_grecv, 256), 256, 0, st ? st : c->stream>>>(c->n_grecv, c->grecv, c->geo,
-                                                                               c->x[c->xc], c->xp[c->xc]);
-        CKL();
-    }
-    return LJMD_OK;
-}
-
 // CSR of the ghost images of every owned particle (written by the kernels that move it) and
 // the list of received-plane images; from the build-time ghost list
 ljmd_status build_images(ljmd_ctx* c) {
-    if (c->newton3 || c->n_gflat == 0) {
+    if (c->newton3 || (!c->capturing && c->n_gflat == 0)) {
         CK(cudaMemsetAsync(c->img_off, 0, sizeof(int) * ((size_t)c->n_own + 1), c->stream));
         return LJMD_OK;
     }
     k_slot2t<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->own_slot, c->slot2t);
     CKL();
     CK(cudaMemsetAsync(c->img_cnt, 0, sizeof(int) * (size_t)c->n_own, c->stream));
-    k_img_build<false><<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->n_slots, c->slot2t,
-                                                                     c->img_cnt, c->img_off, c->img, c->grecv,
-                                                                     c->d_fl);
+    // captured: the ghost count is only known on the device (grid over the slot capacity)
+    const int ng = c->capturing ? c->slot_cap : c->n_gflat;
+    const int* ndev = c->capturing ? &c->d_fl->n_gflat : nullptr;
+    const int nsl = c->capturing ? INT_MAX : c->n_slots;   // single rank: every source is local
+    k_img_build<false><<<nblk(ng, 256), 256, 0, c->stream>>>(ng, c->gflat, nsl, c->slot2t, c->img_cnt, c->img_off,
+                                                             c->img, c->grecv, c->d_fl, ndev);
     CKL();
     TRY(scan(c, c->img_cnt, c->n_own, c->img_off));
-    k_img_build<true><<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->n_slots, c->slot2t,
-                                                                    c->img_cnt, c->img_off, c->img, c->grecv,
-                                                                    c->d_fl);
+    k_img_build<true><<<nblk(ng, 256), 256, 0, c->stream>>>(ng, c->gflat, nsl, c->slot2t, c->img_cnt, c->img_off,
+                                                            c->img, c->grecv, c->d_fl, ndev);
     CKL();
     return LJMD_OK;
 }
@@ -952,7 +1067,7 @@ ljmd_status migrate(ljmd_ctx* c) {
 
 // Cell binning (counting sort + gid order), ghost images and the Verlet list
 // (Sec. 3.4; IntegratorRange rebuild).
-ljmd_status rebuild(ljmd_ctx* c) {
+ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     // Bank-aware re-ordering costs about 1.4 force launches and saves about 13 % of each
     // launch it serves (C2: 225 us against 21 us per step), so it pays for lists that serve
     // >= kRrMinSteps steps: always under the paper's fixed Ns = 20; under the displacement-
@@ -962,7 +1077,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     // on every rank.
     constexpr double kRrMinSteps = 10.0;
     c->pdl_ok = false;   // the next force launch reads the new list: no programmatic overlap
-    if (c->last_build_step >= 0 && c->steps_done > c->last_build_step) {
+    if (danger && c->last_build_step >= 0 && c->steps_done > c->last_build_step) {
         // dangerous-build test on the last step the old list served (x(s-1) in the other
         // position buffer, old layout), before the binning overwrites it
         k_maxdisp<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->x[c->xc ^ 1], c->own_slot,
@@ -977,7 +1092,7 @@ ljmd_status rebuild(ljmd_ctx* c) {
     else if (c->interval_ema == 0.0)
         c->interval_ema = (double)c->opt.rebuild_every;
     c->last_build_step = c->steps_done;
-    c->use_rr = c->bank_order && c->interval_ema >= kRrMinSteps;
+    (void)kRrMinSteps;   // the list order is chosen per ljmd_step call (decide_list_order)
     TRY(reset_flags(c));
     CK(cudaMemsetAsync(c->ocount, 0, sizeof(int) * c->n_ocell, c->stream));
     // input of the binning: the current owned particles, or the post-migration compaction
@@ -1075,12 +1190,34 @@ ljmd_status rebuild(ljmd_ctx* c) {
         }
     }
     TRY(refresh_ghosts(c, true));
+    if (c->split) TRY(send_map(c));
     k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
         c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl);
     CKL();
     TRY(sync_flags(c));
     c->max_staged = c->h_fl->max_staged;
     c->n_gflat = c->h_fl->n_gflat;
+    if (c->split) {
+        const int* h = c->h_pl;
+        c->area[0] = h[1];
+        c->area[1] = h[0] - h[1];
+        c->gbeg[0] = h[2];
+        c->glen[0] = h[3] - h[2];
+        c->gbeg[1] = h[4];
+        c->glen[1] = h[5] - h[4];
+        // the send area (after slot_cap) and its image-list entries need room: regrow keeping
+        // the current positions (the rebuild is past every read of the old ones)
+        if (h[0] > c->send_extra || c->n_gflat > c->slot_cap + c->send_extra) {
+            c->send_extra = std::max(h[0], c->n_gflat - c->slot_cap) * 5 / 4 + 1024;
+            TRY(alloc_slots(c, c->slot_cap, true));
+            ++c->regrows;
+            return rebuild(c, false);   // the new layout is in place: bin it again with room
+        }
+    }
+    if (c->max_staged > c->stage_cap) {   // launches are sized for stage_cap (also in graphs)
+        c->stage_cap = c->max_staged + c->max_staged / LJMD_STAGE_MARGIN + 16;
+        drop_graphs(c);
+    }
     TRY(build_images(c));
     if (build_smem(c) > kMaxStageSmem || force_smem(c) > kMaxStageSmem || c->max_staged > 65535)
         return set_err(c, LJMD_E_CAPACITY,
@@ -1163,6 +1300,137 @@ ljmd_status validate_step(ljmd_ctx* c, int vslot) {
     return LJMD_OK;
 }
 
+
+// ---------------------------------------------------------------------- graph mode (one rank)
+// ljmd_step as a CUDA graph: the step sequence of a call is captured once per shape (steps,
+// buffer parity, schedule phase, list order) and replayed.  The rebuild is a conditional node
+// whose condition is set on the device (reading R7: fixed Ns, or the displacement check), and
+// its capacity checks are device-side too, so a call runs without a single host round trip;
+// the host reads the step control (rebuild steps, samples, abort) at the end of the call.  A
+// capacity shortfall aborts the rest of the sequence and the host resumes at that step on
+// the eager path with regrown buffers (same arithmetic, same results).
+bool graph_ok(const ljmd_ctx* c) {
+    return c->opt.graphs && !c->split && !c->newton3 && !c->opt.validate && !c->opt.profile && c->nu_dt == 0.0 &&
+           !c->dsl_on && c->stage_cap > 0;
+}
+
+// Launch `setter(handle)` on c->stream (being captured), then an IF node after it whose body is
+// captured from `fn` on `body` (c->stream points there while fn runs).
+template <class Setter, class Body>
+ljmd_status cond_if(ljmd_ctx* c, cudaStream_t body, Setter setter, Body fn) {
+    cudaStream_t st = c->stream;
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps;
+    size_t nd;
+    CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+    setter(h);
+    CKL();
+    CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+    cudaGraphNodeParams prm = {};
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h;
+    prm.conditional.type = cudaGraphCondTypeIf;
+    prm.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, deps, nd, &prm));
+    CK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    CK(cudaStreamBeginCaptureToGraph(body, prm.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    c->stream = body;
+    const ljmd_status r = fn();
+    c->stream = st;
+    cudaGraph_t tmp;
+    const cudaError_t e = cudaStreamEndCapture(body, &tmp);
+    if (r != LJMD_OK) return r;
+    if (e != cudaSuccess) return set_err(c, LJMD_E_CUDA, "capture of a conditional body: %s", cudaGetErrorString(e));
+    return LJMD_OK;
+}
+
+// The rebuild of one step inside a captured sequence (single rank): the eager rebuild's
+// kernels without its host synchronisations, capacities checked on the device in three
+// stages (slots before anything is permuted; staging after the tile tables; list width
+// after the build), each gating the rest through a nested conditional node.
+ljmd_status rebuild_captured(ljmd_ctx* c) {
+    const int n = c->n_own;
+    const size_t oc = c->own_cap;
+    k_maxdisp<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc ^ 1], c->own_slot, c->xbuild, &c->d_st->disp_bits);
+    CKL();
+    k_dangerous<<<1, 1, 0, c->stream>>>(c->d_st, c->opt.delta * c->opt.delta);
+    CKL();
+    TRY(reset_flags(c));
+    CK(cudaMemsetAsync(c->ocount, 0, sizeof(int) * c->n_ocell, c->stream));
+    k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, c->geo, c->xw, c->ocount, c->cell_of,
+                                                    c->rank_in, c->gid[0], c->d_fl, c->v[0], c->v[1], c->gid[1],
+                                                    (int)oc);
+    CKL();
+    TRY(scan(c, c->ocount, c->n_ocell, c->obegin));
+    k_ext_counts<<<nblk(c->n_ecell, 256), 256, 0, c->stream>>>(c->n_ecell, c->ocount, c->geo, c->ecell_src,
+                                                              c->recv_cnt, c->ecount);
+    CKL();
+    TRY(scan(c, c->ecount, c->n_ecell, c->ebegin));
+    DevCtl* ctl = c->d_ctl;
+    DevFlags* fl = c->d_fl;
+    const int* need = c->ebegin + c->n_ecell;
+    const int slot_cap = c->slot_cap, stage_cap = c->stage_cap, K = c->K;
+    return cond_if(
+        c, c->cap_stream[1],
+        [&](cudaGraphConditionalHandle h) {
+            k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 1, h);
+        },
+        [&]() -> ljmd_status {
+            k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm);
+            CKL();
+            double* vo = c->v[1];
+            k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
+                c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, c->gid[1], c->xw, vo, vo + oc,
+                vo + 2 * oc, c->x[c->xc], c->xf, c->v[0], c->v[0] + oc, c->v[0] + 2 * oc, c->gid[0], c->own_slot,
+                c->ocell_of, c->slot_gid, c->xbuild, c->xp[c->xc], c->d_fl);
+            CKL();
+            TRY(refresh_ghosts(c, true));
+            k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
+                c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl);
+            CKL();
+            return cond_if(
+                c, c->cap_stream[2],
+                [&](cudaGraphConditionalHandle h) {
+                    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 2, h);
+                },
+                [&]() -> ljmd_status {
+                    TRY(build_images(c));
+                    TRY(launch_nlist(c));
+                    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 3,
+                                                         cudaGraphConditionalHandle{});
+                    CKL();
+                    if (c->use_rr) {
+                        k_list_rr<<<nblk(n, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
+                            n, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0,
+                            c->nbr8b);
+                        CKL();
+                    }
+                    return LJMD_OK;
+                });
+        });
+}
+
+// The list order of the rebuilds of one ljmd_step call (eager and graph paths alike): the
+// bank-aware pass costs ~1.4 force launches and saves ~13 % of each launch it serves, so it is
+// used while the recent lists have served >= 10 steps (running estimate of the rebuild
+// interval, starting at Ns): always under the paper's fixed Ns = 20.  Deterministic, the same
+// on every rank.
+void decide_list_order(ljmd_ctx* c) {
+    if (c->interval_ema == 0.0) c->interval_ema = (double)c->opt.rebuild_every;
+    c->use_rr = c->bank_order && c->interval_ema >= 10.0;
+}
+
+// bookkeeping of one rebuild at MD step `step` (eager and graph paths)
+void note_rebuild(ljmd_ctx* c, int64_t step) {
+    ++c->n_rebuilds;
+    c->rebuild_steps.push_back(step);
+}
+
 ljmd_status ensure_hist(ljmd_ctx* c, int64_t need) {
     if (need <= c->hist_cap) return LJMD_OK;
     int64_t cap = std::max<int64_t>(need, 64);
@@ -1172,7 +1440,8 @@ ljmd_status ensure_hist(ljmd_ctx* c, int64_t need) {
 }
 
 ljmd_status finalize_energy(ljmd_ctx* c, double* dst) {
-    k_finalize_energy<<<1, 1024, 0, c->stream>>>(c->pe_part, c->ke_part, c->n_tiles, dst);
+    k_finalize_energy<<<1, 1024, 0, c->stream>>>(c->pe_part, c->ke_part, c->n_tiles * (c->newton3 ? 1 : c->fparts), dst,
+                                                 c->capturing ? c->d_ctl : nullptr);
     CKL();
     return LJMD_OK;
 }
@@ -1270,6 +1539,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const 
     c->h_val.clear();
     c->last_build_step = -1;
     CK(cudaMemsetAsync(c->d_st, 0, sizeof(DevStats), c->stream));
+    decide_list_order(c);
     TRY(rebuild(c));
     TRY(ensure_hist(c, 1));
     TRY(launch_force(c, true, kStore, false));
@@ -1360,6 +1630,8 @@ ljmd_status ljmd_default_options(ljmd_options* o) {
     o->list_order = 1;
     o->split_self = 0;
     o->newton3 = 0;
+    o->validate = 0;
+    o->graphs = 1;
     return LJMD_OK;
 }
 
@@ -1468,9 +1740,16 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
             set_err(c, LJMD_E_CUDA, "aux stream creation failed");
             return fail(LJMD_E_CUDA);
         }
+        if (cudaMalloc(&c->halo_flag, sizeof(unsigned)) != cudaSuccess ||
+            cudaMemset(c->halo_flag, 0, sizeof(unsigned)) != cudaSuccess) {
+            set_err(c, LJMD_E_CUDA, "halo flag allocation failed");
+            return fail(LJMD_E_CUDA);
+        }
     }
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
+        cudaMalloc(&c->d_ctl, sizeof(DevCtl)) != cudaSuccess ||
+        cudaHostAlloc(&c->h_ctl, sizeof(DevCtl), cudaHostAllocMapped) != cudaSuccess ||
         cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess ||
         cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostAlloc(&c->h_fl, sizeof(DevFlags), cudaHostAllocMapped) != cudaSuccess ||
@@ -1478,6 +1757,13 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         set_err(c, LJMD_E_CUDA, "flag allocation failed");
         return fail(LJMD_E_CUDA);
     }
+    k_reset_flags<<<1, 1, 0, c->stream>>>(c->d_fl, 0);
+    cudaMemsetAsync(c->d_ctl, 0, sizeof(DevCtl), c->stream);
+    for (int k = 0; k < 3; ++k)
+        if (cudaStreamCreateWithFlags(&c->cap_stream[k], cudaStreamNonBlocking) != cudaSuccess) {
+            set_err(c, LJMD_E_CUDA, "capture stream creation failed");
+            return fail(LJMD_E_CUDA);
+        }
     // owned capacity: the whole system on one rank; a slab's share + 25 % headroom otherwise
     const double share = (double)c->geo.nzl / (double)c->geo.nc[2];
     const int cap = c->nranks == 1 ? (int)n : (int)std::min<int64_t>(n, (int64_t)(n * share * 1.25) + 4096);
@@ -1498,6 +1784,11 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
             return fail(LJMD_E_CUDA);
         }
     }
+    if (c->split) {   // send areas: the two boundary planes with their x/y images, generous
+        const double per_plane = (double)cap / (double)c->geo.nzl;
+        const double img = (double)(c->geo.ex * c->geo.ey) / (double)(c->geo.nc[0] * c->geo.nc[1]);
+        c->send_extra = (int)std::min<double>(2.0 * per_plane * img * 1.5 + 4096, (double)INT_MAX / 4);
+    }
     const double ghost_ratio = (double)c->n_ecell / (double)c->n_ocell;
     int64_t scap = (int64_t)std::ceil(cap * ghost_ratio * 1.15) + 4096;
     if ((s = alloc_slots(c, (int)std::min<int64_t>(scap, INT_MAX / 2), false)) != LJMD_OK) return fail(s);
@@ -1507,6 +1798,14 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     int K = o.nbr_capacity > 0 ? ((int)o.nbr_capacity + 7) / 8 * 8 : ((int)std::ceil(expect * 1.4) + 16 + 7) / 8 * 8;
     if ((s = alloc_list(c, K)) != LJMD_OK) return fail(s);
     if ((s = load_state(c, pos, vel)) != LJMD_OK) return fail(s);
+    if (o.tight_caps) {
+        // testing: every capacity exactly what this state needs, so that a later rebuild inside
+        // a captured step sequence runs short and takes the abort / eager-resume path
+        c->stage_cap = c->max_staged;
+        if ((s = alloc_list(c, std::max(8, (c->max_nbr + 7) / 8 * 8))) != LJMD_OK ||
+            (s = alloc_slots(c, c->n_slots, false)) != LJMD_OK || (s = load_state(c, pos, vel)) != LJMD_OK)
+            return fail(s);
+    }
     *out = c;
     return LJMD_OK;
 }
@@ -1586,14 +1885,242 @@ ljmd_status ljmd_wait_transfers(ljmd_ctx* c) {
     return LJMD_OK;
 }
 
+ljmd_status kick_drift(ljmd_ctx* c) {
+    // Alg. alg:VelocityVerlet line 6 of the first step of a call (uses the stored F)
+    const bool check = c->opt.rebuild_check != 0;
+    if (check) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
+    double* v = c->v[c->oc_cur];
+    const size_t oc = c->own_cap;
+    const double h = 0.5 * c->dt / c->opt.mass;
+    if (check)
+        k_kick_drift<true><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
+            c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h, c->dt,
+            c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
+    else
+        k_kick_drift<false><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
+            c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h, c->dt,
+            c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
+    CKL();
+    return LJMD_OK;
+}
+
+// Steps s_first .. n of a call on the eager path (host decides each rebuild).  rebuilt_first:
+// step s_first's drift and rebuild are already done (resumption after a graph abort).
+ljmd_status step_eager(ljmd_ctx* c, int64_t s_first, int64_t nsteps, bool rebuilt_first) {
+    const bool check = c->opt.rebuild_check != 0;
+    const int64_t ee = c->opt.energy_every;
+    const double delta2 = c->opt.delta * c->opt.delta;
+    for (int64_t s = s_first; s <= nsteps; ++s) {
+        bool halo_pending = false;
+        if (!(rebuilt_first && s == s_first)) {
+            ++c->since;
+            ++c->steps_done;
+            bool due = c->since >= c->opt.rebuild_every;
+            if (!due && check) {
+                // global max displacement (non-negative doubles: max of the bit patterns)
+                TRY(allreduce(c, reinterpret_cast<double*>(&c->d_fl->maxdisp2), 1, true));
+                TRY(sync_flags(c));
+                double m2;
+                std::memcpy(&m2, &c->h_fl->maxdisp2, sizeof m2);
+                due = 4.0 * m2 > delta2;
+            }
+            if (due) {
+                TRY(rebuild(c));
+                c->since = 0;
+                note_rebuild(c, c->steps_done);
+            } else {
+                // ghost images of owned particles were written with the positions (force
+                // epilogue / kick-drift); received halo planes need theirs after the exchange
+                if (c->split && c->aux_stream) {
+                    // the halo travels on aux_stream while the interior tiles compute
+                    CK(cudaEventRecord(c->ev_ready, c->stream));
+                    CK(cudaStreamWaitEvent(c->aux_stream, c->ev_ready, 0));
+                    TRY(halo_direct(c, c->aux_stream));
+#if LJMD_HALO_GATE
+                    ++c->halo_seq;
+                    k_set_flag<<<1, 1, 0, c->aux_stream>>>(c->halo_flag, c->halo_seq);
+                    CKL();
+#endif
+                    CK(cudaEventRecord(c->ev_halo, c->aux_stream));
+                    halo_pending = true;
+                } else if (c->split) {
+                    TRY(halo_direct(c));
+                }
+                if (c->newton3) TRY(refresh_ghosts(c, false));
+            }
+        }
+        const bool sample = ee > 0 && (c->steps_done % ee) == 0;
+        const bool last = s == nsteps;
+        if (check && !last) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
+        if (c->opt.validate) TRY(validate_step(c, (int)(s - 1)));
+        TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last, halo_pending));
+        if (last) c->energy_current = sample && ee > 0;
+        if (sample) {
+            TRY(finalize_energy(c, c->hist + 2 * c->call_nsamp));
+            TRY(allreduce(c, c->hist + 2 * c->call_nsamp, 2, false));
+            ++c->call_nsamp;
+        }
+        if (!last) c->xc ^= 1;
+    }
+    return LJMD_OK;
+}
+
+// The step sequence of one call, captured (graph mode): kick-drift, then per step the
+// device decision + conditional rebuild (safe policy: every step; fixed policy: the
+// host-known due steps), the force with its fused velocity-Verlet epilogue, the samples.
+ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) {
+    const bool check = c->opt.rebuild_check != 0;
+    const int64_t ee = c->opt.energy_every;
+    const int ns = (int)c->opt.rebuild_every;
+    const double delta2 = c->opt.delta * c->opt.delta;
+    const int xc0 = c->xc;
+    const int64_t step0 = c->steps_done;
+    const int64_t k0 = c->kernel_launches;
+    int64_t body_k = 0, nconds = 0;
+    c->capturing = true;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    ljmd_status r = [&]() -> ljmd_status {
+        CK(cudaMemsetAsync(c->d_ctl, 0, offsetof(DevCtl, since), c->stream));   // since persists across calls
+        TRY(kick_drift(c));
+        int64_t sim_since = c->since;
+        for (int64_t s = 1; s <= nsteps; ++s) {
+            bool cond = check;
+            bool forced = false;
+            if (!check) {
+                ++sim_since;
+                if (sim_since >= ns) {
+                    sim_since = 0;
+                    cond = forced = true;
+                }
+            }
+            if (cond) {
+                const int64_t kb = c->kernel_launches;
+                TRY(cond_if(
+                    c, c->cap_stream[0],
+                    [&](cudaGraphConditionalHandle h) {
+                        k_decide<<<1, 1, 0, c->stream>>>(c->d_ctl, c->d_fl, ns, check ? 1 : 0, forced ? 1 : 0, delta2,
+                                                        c->d_rstep, (int)s, h);
+                    },
+                    [&]() { return rebuild_captured(c); }));
+                body_k = c->kernel_launches - kb - 1;
+                ++nconds;
+                c->pdl_ok = false;   // the force after the rebuild node reads the new list
+            }
+            const bool sample = ee > 0 && ((step0 + s) % ee) == 0;
+            const bool last = s == nsteps;
+            TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last, false));
+            if (sample) TRY(finalize_energy(c, c->hist));
+            if (!last) c->xc ^= 1;
+        }
+        return LJMD_OK;
+    }();
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    c->xc = xc0;
+    c->pdl_ok = false;
+    if (r != LJMD_OK) {
+        if (g) cudaGraphDestroy(g);
+        return r;
+    }
+    if (e != cudaSuccess) return set_err(c, LJMD_E_CUDA, "graph capture of ljmd_step: %s", cudaGetErrorString(e));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&ex, g, 0);
+    if (ei != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return set_err(c, LJMD_E_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(ei));
+    }
+    ge.g = g;
+    ge.ex = ex;
+    ge.launches = (c->kernel_launches - k0) - nconds * body_k;   // without the conditional bodies
+    c->rebuild_kernels = body_k;
+    c->kernel_launches = k0;   // counted per replay below
+    return LJMD_OK;
+}
+
+ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps) {
+    const bool check = c->opt.rebuild_check != 0;
+    const int64_t ee = c->opt.energy_every;
+    if (c->rstep_cap < nsteps) {
+        TRY(dalloc(c, &c->d_rstep, (size_t)nsteps));
+        if (c->h_rstep) cudaFreeHost(c->h_rstep);
+        c->h_rstep = nullptr;
+        CK(cudaHostAlloc(&c->h_rstep, sizeof(int) * (size_t)nsteps, cudaHostAllocMapped));
+        c->rstep_cap = nsteps;
+    }
+    char key[160];
+    snprintf(key, sizeof key, "n%lld x%d s%lld e%lld c%d r%d", (long long)nsteps, c->xc,
+             check ? -1LL : (long long)c->since, ee > 0 ? (long long)(c->steps_done % ee) : 0LL, check ? 1 : 0,
+             c->use_rr ? 1 : 0);
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        ljmd_ctx::GraphEntry ge;
+        TRY(capture_call(c, nsteps, ge));
+        it = c->graphs.emplace(key, ge).first;
+    }
+    const int64_t step0 = c->steps_done;
+    const int xc0 = c->xc;
+    int64_t sim_since = c->since;   // fixed policy: the host-known schedule
+    for (int64_t s = 1; s <= nsteps; ++s)
+        if (++sim_since >= c->opt.rebuild_every) sim_since = 0;
+    if (check) {
+        k_set_since<<<1, 1, 0, c->stream>>>(c->d_ctl, (int)c->since);
+        CKL();
+    }
+    CK(cudaGraphLaunch(it->second.ex, c->stream));
+    ++c->graph_calls;
+    TRY(to_host(c, c->h_ctl, c->d_ctl, sizeof(DevCtl)));
+    TRY(to_host(c, c->h_rstep, c->d_rstep, sizeof(int) * (size_t)nsteps));
+    TRY(to_host(c, c->h_slots, c->ebegin + c->n_ecell, sizeof(int)));
+    TRY(sync_flags(c));
+    const DevCtl ctl = *c->h_ctl;
+    c->kernel_launches += it->second.launches + (int64_t)ctl.nreb * c->rebuild_kernels;
+    for (int k = 0; k < ctl.nreb; ++k) {
+        const int64_t st = step0 + c->h_rstep[k];
+        if (c->last_build_step >= 0 && st > c->last_build_step)
+            c->interval_ema = 0.5 * c->interval_ema + 0.5 * (double)(st - c->last_build_step);
+        c->last_build_step = st;
+        note_rebuild(c, st);
+    }
+    c->call_nsamp = ctl.nsamp;
+    if (c->h_fl->nonfinite_gid != INT_MAX)
+        return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d", c->h_fl->nonfinite_gid);
+    if (c->h_fl->overlap_pair != ~0ull)
+        return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)",
+                       (int)(c->h_fl->overlap_pair >> 32), (int)(c->h_fl->overlap_pair & 0xffffffffu));
+    if (ctl.nreb > 0) {
+        c->n_slots = *c->h_slots;
+        c->max_staged = c->h_fl->max_staged;
+        c->n_gflat = c->h_fl->n_gflat;
+        c->max_nbr = c->h_fl->max_nbr;
+        c->total_nbr = c->h_fl->total_nbr;
+    }
+    if (!ctl.abort) {
+        c->steps_done = step0 + nsteps;
+        c->since = check ? ctl.since : sim_since;
+        c->xc = xc0 ^ (int)((nsteps - 1) & 1);
+        c->energy_current = ee > 0 && (c->steps_done % ee) == 0;
+        return LJMD_OK;
+    }
+    // a capacity ran short in the rebuild of step sa: steps 1 .. sa-1 are complete, step sa
+    // has drifted; resume there on the eager path (its rebuild regrows what is short)
+    const int64_t sa = ctl.abort_step;
+    ++c->graph_aborts;
+    c->steps_done = step0 + sa;
+    c->since = 0;
+    c->xc = xc0 ^ (int)((sa - 1) & 1);
+    CK(cudaMemsetAsync(c->d_ctl, 0, offsetof(DevCtl, since), c->stream));
+    TRY(rebuild(c, /*danger=*/false));   // the dangerous-build test of this rebuild already ran
+    return step_eager(c, sa, nsteps, true);
+}
+
 ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
     TRY(check_ctx(c));
     if (nsteps < 0) return set_err(c, LJMD_E_ARG, "ljmd_step: nsteps < 0");
     if (nsteps == 0) return LJMD_OK;
-    const bool check = c->opt.rebuild_check != 0;
     const int64_t ee = c->opt.energy_every;
     TRY(ensure_hist(c, nsteps / std::max<int64_t>(ee, 1) + 2));
-    int64_t nsamp = 0;
+    c->call_nsamp = 0;
     const int64_t first_launch = c->force_launches;
     const int64_t step0 = c->steps_done;
     c->energy_current = false;
@@ -1604,78 +2131,21 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         }
         CK(cudaMemsetAsync(c->vhist, 0, sizeof(int) * 2 * (size_t)nsteps, c->stream));
     }
-    const double delta2 = c->opt.delta * c->opt.delta;
-    // Alg. alg:VelocityVerlet line 6 of the first step (uses the stored F)
-    if (check) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
-    {
-        double* v = c->v[c->oc_cur];
-        const size_t oc = c->own_cap;
-        double h = 0.5 * c->dt / c->opt.mass;
-        if (check)
-            k_kick_drift<true><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
-                c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
-        else
-            k_kick_drift<false><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
-                c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h,
-                c->dt, c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
-        CKL();
+    decide_list_order(c);
+    if (graph_ok(c)) {
+        TRY(step_graph(c, nsteps));
+    } else {
+        TRY(kick_drift(c));
+        TRY(step_eager(c, 1, nsteps, false));
     }
-    for (int64_t s = 1; s <= nsteps; ++s) {
-        ++c->since;
-        ++c->steps_done;
-        bool due = c->since >= c->opt.rebuild_every;
-        bool halo_pending = false;
-        if (!due && check) {
-            // global max displacement (non-negative doubles: max of the bit patterns)
-            TRY(allreduce(c, reinterpret_cast<double*>(&c->d_fl->maxdisp2), 1, true));
-            TRY(sync_flags(c));
-            double m2;
-            std::memcpy(&m2, &c->h_fl->maxdisp2, sizeof m2);
-            due = 4.0 * m2 > delta2;
-        }
-        if (due) {
-            TRY(rebuild(c));
-            c->since = 0;
-            ++c->n_rebuilds;
-            c->rebuild_steps.push_back(c->steps_done);
-        } else {
-            // ghost images of owned particles were written with the positions (force
-            // epilogue / kick-drift); received halo planes need theirs after the exchange
-            if (c->split && c->aux_stream) {
-                // the halo travels on aux_stream while the interior tiles compute
-                CK(cudaEventRecord(c->ev_ready, c->stream));
-                CK(cudaStreamWaitEvent(c->aux_stream, c->ev_ready, 0));
-                TRY(halo_exchange(c, c->aux_stream));
-                TRY(refresh_recv(c, c->aux_stream));
-                CK(cudaEventRecord(c->ev_halo, c->aux_stream));
-                halo_pending = true;
-            } else if (c->split) {
-                TRY(halo_exchange(c));
-                TRY(refresh_recv(c));
-            }
-            if (c->newton3) TRY(refresh_ghosts(c, false));
-        }
-        const bool sample = ee > 0 && (c->steps_done % ee) == 0;
-        const bool last = s == nsteps;
-        if (check && !last) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
-        if (c->opt.validate) TRY(validate_step(c, (int)(s - 1)));
-        TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last, halo_pending));
-        if (last) c->energy_current = sample && ee > 0;
-        if (sample) {
-            TRY(finalize_energy(c, c->hist + 2 * nsamp));
-            TRY(allreduce(c, c->hist + 2 * nsamp, 2, false));
-            ++nsamp;
-        }
-        if (!last) c->xc ^= 1;
-    }
-    TRY(pull_hist(c, nsamp));
+    TRY(pull_hist(c, c->call_nsamp));
     if (c->energy_current) {
         c->cur_pe = c->h_hist[c->h_hist.size() - 2];
         c->cur_ke = c->h_hist[c->h_hist.size() - 1];
     }
     TRY(collect_profile(c, first_launch));
     TRY(sync_flags(c));
+    if (c->h_fl->halo_timeout) return set_err(c, LJMD_E_NCCL, "a boundary force tile timed out waiting for the halo");
     if (c->opt.validate) {
         if (c->h_fl->val_error)
             return set_err(c, LJMD_E_STATE, "validation: a listed in-range pair was not found by the cell search");
@@ -1824,6 +2294,9 @@ ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s) {
     CK(cudaStreamSynchronize(c->stream));
     s->dangerous_builds = (int64_t)c->h_st->dangerous;
     s->max_build_disp = std::sqrt(c->h_st->max_disp2);
+    s->graph_calls = c->graph_calls;
+    s->graph_aborts = c->graph_aborts;
+    s->graphs_cached = (int64_t)c->graphs.size();
     const int64_t nv = (int64_t)c->h_val.size() / 3;
     s->validated_steps = nv;
     for (int64_t k = 0; k < nv; ++k) {
@@ -1879,6 +2352,13 @@ void ljmd_destroy(ljmd_ctx* c) {
     delete c->tr;
     if (c->h_fl) cudaFreeHost(c->h_fl);
     if (c->h_st) cudaFreeHost(c->h_st);
+    drop_graphs(c);
+    if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    if (c->h_rstep) cudaFreeHost(c->h_rstep);
+    for (void* p : {(void*)c->d_ctl, (void*)c->d_rstep, (void*)c->halo_flag})
+        if (p) cudaFree(p);
+    for (cudaStream_t st : c->cap_stream)
+        if (st) cudaStreamDestroy(st);
     for (void* p : {(void*)c->d_st, (void*)c->vcount, (void*)c->vbegin, (void*)c->vcell, (void*)c->vrank,
                     (void*)c->vpos, (void*)c->vhist})
         if (p) cudaFree(p);

@@ -50,7 +50,7 @@ class Options(ctypes.Structure):
                 ("nccl_id", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("profile", ctypes.c_int64), ("list_order", ctypes.c_int64),
                 ("split_self", ctypes.c_int64), ("newton3", ctypes.c_int64),
-                ("validate", ctypes.c_int64)]
+                ("validate", ctypes.c_int64), ("graphs", ctypes.c_int64), ("tight_caps", ctypes.c_int64)]
 
 
 class Stats(ctypes.Structure):
@@ -63,7 +63,8 @@ class Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64), ("dangerous_builds", ctypes.c_int64),
                 ("max_build_disp", ctypes.c_double), ("validated_steps", ctypes.c_int64),
                 ("missed_pairs", ctypes.c_int64), ("missed_particle_steps", ctypes.c_int64),
-                ("max_missed_particles", ctypes.c_int64)]
+                ("max_missed_particles", ctypes.c_int64), ("graph_calls", ctypes.c_int64),
+                ("graph_aborts", ctypes.c_int64), ("graphs_cached", ctypes.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}

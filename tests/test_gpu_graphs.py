@@ -1,0 +1,79 @@
+"""GPU: ljmd_step as a captured CUDA graph (device-side rebuild decision and capacity checks,
+DESIGN.md §10) against the eager path, which takes the same decisions on the host: the
+same kernels in the same order on the same data, so the trajectories agree bit for bit."""
+import numpy as np
+import pytest
+
+import ljinputs as li
+from conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_1704_03329_b200 import ljmd
+    ljmd.load()
+    return ljmd
+
+
+def state(cells=8, sigma_d=0.05, t0=1.44):
+    pos, box = li.fcc(cells, cells, cells)
+    return li.perturb(pos, sigma_d), li.velocities(len(pos), t0), box
+
+
+def run(eng, pos, vel, box, calls, **kw):
+    with eng.LJMD(pos, vel, box, **kw) as ctx:
+        for n in calls:
+            ctx.step(n)
+        out = dict(x=ctx.positions(), v=ctx.velocities(), F=ctx.forces(), e=ctx.energy_history(),
+                   reb=ctx.rebuild_steps(), st=ctx.stats())
+    return out
+
+
+def same(a, b):
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["v"], b["v"]) and np.array_equal(a["F"], b["F"])
+    assert np.array_equal(a["e"][0], b["e"][0]) and np.array_equal(a["e"][1], b["e"][1])
+    assert a["reb"].tolist() == b["reb"].tolist()
+
+
+@pytest.mark.parametrize("check", [0, 1])
+def test_graph_equals_eager(eng, check):
+    """Both rebuild policies, calls of several lengths (graphs captured per shape and
+    replayed): positions, velocities, forces, the energy history and the rebuild steps are
+    bitwise those of the eager path."""
+    pos, vel, box = state()
+    calls = [20, 20, 7, 13, 20, 1, 19]
+    g = run(eng, pos, vel, box, calls, rebuild_check=check, graphs=1)
+    e = run(eng, pos, vel, box, calls, rebuild_check=check, graphs=0)
+    same(g, e)
+    assert g["st"]["graph_calls"] == len(calls) and e["st"]["graph_calls"] == 0
+    assert g["st"]["dangerous_builds"] == e["st"]["dangerous_builds"]
+    assert len(g["reb"]) >= (2 if check == 0 else 4)
+
+
+def test_graph_capacity_abort_resumes(eng):
+    """Capacities shrunk to the initial state's needs (tight_caps): the first rebuild inside
+    a captured sequence that needs more (slots, staging or list width) aborts on the device;
+    the host resumes eagerly at that step with regrown buffers.  The trajectory is the eager
+    one bit for bit."""
+    pos, vel, box = state(sigma_d=0.0, t0=2.0)   # perfect FCC melting: the layout grows
+    calls = [20, 20, 20]
+    g = run(eng, pos, vel, box, calls, graphs=1, tight_caps=1)
+    e = run(eng, pos, vel, box, calls, graphs=0)
+    same(g, e)
+    assert g["st"]["graph_aborts"] >= 1 and g["st"]["regrows"] >= 1
+
+
+def test_graph_parity_with_oracle(eng, orc):
+    """A 40-step graph-mode run (two captured calls, one rebuild each) against the oracle's
+    trajectory with the same schedule: energies within the 100-step bar."""
+    pos, vel, box = state(cells=10)
+    with eng.LJMD(pos, vel, box, graphs=1) as ctx:
+        ctx.step(20)
+        ctx.step(20)
+        pe, ke = ctx.energy_history()
+        assert ctx.stats()["graph_calls"] == 2
+    r = orc.run(pos, vel, box, 40)
+    np.testing.assert_allclose(pe, r.pe, rtol=1e-8)
+    np.testing.assert_allclose(ke, r.ke, rtol=1e-8)

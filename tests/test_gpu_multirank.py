@@ -94,6 +94,25 @@ def test_decomposition_bitwise(nranks):
     assert sum(o["st"]["n_owned"] for o in per) == len(pos)
 
 
+@pytest.mark.parametrize("nranks,check", [(2, 0), (3, 0), (2, 1)])
+def test_decomposition_overlapped_halo_bitwise(nranks, check):
+    """Slabs thick enough for the overlapped halo path (>= 3 tile layers per rank: 6 x 6 x 24
+    FCC cells -> 14 z planes): the boundary planes travel on the second stream in the
+    receiver's ghost-plane layout while the interior tiles compute, the two boundary tile
+    layers run as one launch after it.  45 steps (two rebuilds with migration; also under
+    the displacement-checked policy) equal p = 1 bit for bit."""
+    pos, box = li.fcc(6, 6, 24)
+    pos = li.perturb(pos, 0.05)
+    vel = li.velocities(len(pos), 1.44)
+    ref = single(pos, vel, box, 45, list_order=0, rebuild_check=check)
+    got, per = run_ranks(nranks, pos, vel, box, 45, list_order=0, rebuild_check=check)
+    assert np.array_equal(got["X"], ref["X"])
+    assert np.array_equal(got["V"], ref["V"])
+    assert np.array_equal(got["F"], ref["F"])
+    for o in per:
+        assert o["rs"].tolist() == ref["rs"].tolist()
+
+
 def test_decomposition_default_order():
     """With the (default) bank-aware neighbour order the per-particle summation order
     depends on the tiling, so p = 2 agrees with p = 1 to rounding, not bitwise."""

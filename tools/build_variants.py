@@ -1,4 +1,4 @@
-"""Build A/B variants of libljmd.so with -D tuning macros: python scratch/build_variants.py 'v0:' 'v1:-DX=1' ..."""
+"""Build A/B variants of libljmd.so with -D tuning macros: python tools/build_variants.py 'v0:' 'v1:-DX=1' ..."""
 import os, subprocess, sys
 from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -1,5 +1,5 @@
 """Per-kernel GPU time (CUPTI via torch.profiler) of ljmd_step on C2 for the library in LJMD_LIB.
-usage: LJMD_LIB=... python scratch/kprof.py [cycles]"""
+usage: LJMD_LIB=... python tools/kprof.py [cycles]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -13,6 +13,7 @@ s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 split = int(os.environ.get("LJMD_SPLIT_SELF", "0"))
 opts = ljmd.default_options(device=0, stream=s.cuda_stream, rebuild_check=cfg.rebuild_check,
+                            graphs=int(os.environ.get("LJMD_GRAPHS", "1")),
                             list_order=int(os.environ.get("LJMD_LIST_ORDER", "1")), split_self=split)
 if split:
     import ctypes
