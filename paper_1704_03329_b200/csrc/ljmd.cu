@@ -1309,9 +1309,22 @@ ljmd_status validate_step(ljmd_ctx* c, int vslot) {
 // the host reads the step control (rebuild steps, samples, abort) at the end of the call.  A
 // capacity shortfall aborts the rest of the sequence and the host resumes at that step on
 // the eager path with regrown buffers (same arithmetic, same results).
+// Profilers and sanitizers cannot see the kernels of a graph with conditional nodes (ncu:
+// "not supported for profiling"), so under a CUDA injection tool (ncu, nsys,
+// compute-sanitizer set CUDA_INJECTION64_PATH) -- or with LJMD_GRAPHS=0 -- the same kernels
+// run on the eager path instead.
+bool graphs_allowed() {
+    static const bool ok = [] {
+        const char* inj = getenv("CUDA_INJECTION64_PATH");
+        const char* env = getenv("LJMD_GRAPHS");
+        return !(inj && *inj) && !(env && env[0] == '0');
+    }();
+    return ok;
+}
+
 bool graph_ok(const ljmd_ctx* c) {
-    return c->opt.graphs && !c->split && !c->newton3 && !c->opt.validate && !c->opt.profile && c->nu_dt == 0.0 &&
-           !c->dsl_on && c->stage_cap > 0;
+    return c->opt.graphs && graphs_allowed() && !c->split && !c->newton3 && !c->opt.validate && !c->opt.profile &&
+           c->nu_dt == 0.0 && !c->dsl_on && c->stage_cap > 0;
 }
 
 // Launch `setter(handle)` on c->stream (being captured), then an IF node after it whose body is
