@@ -872,6 +872,7 @@ struct NlistArgs {
     float thr_hi;        // r2f >= thr_hi  =>  r^2 >= rbar_c^2 for sure
     DevFlags* fl;
     const int* slot_gid;
+    int stage_cap;       // staged records per tile the dynamic shared memory is sized for
 };
 
 // One CTA per force tile (the same halo rows and local numbering as k_force).
@@ -890,9 +891,19 @@ struct NlistArgs {
 #define LJMD_BUILD_THREADS 480
 #endif
 constexpr int kBuildThreads = LJMD_BUILD_THREADS;
-#ifndef LJMD_BUILD_MINB
-#define LJMD_BUILD_MINB 4
+// Flattened candidate loop (round 2): each thread walks the concatenation of its non-empty
+// x-windows (one loop, the window switch predicated) instead of one loop per stencil row, so a
+// warp runs max_lanes(sum of windows) iterations instead of sum_rows(max_lanes(window)): the
+// lanes idle only at the end of the warp's longest list (55 % of lanes active before).  The
+// windows wait in shared memory (9 words per thread), the next candidate's position is loaded
+// one iteration ahead.  Same candidates, same order, same decisions: the list is unchanged.
+#ifndef LJMD_BUILD_FLAT
+#define LJMD_BUILD_FLAT 0
 #endif
+#ifndef LJMD_BUILD_MINB
+#define LJMD_BUILD_MINB (LJMD_BUILD_FLAT ? 3 : 4)
+#endif
+constexpr int kBuildWinWords = LJMD_BUILD_FLAT ? 9 * LJMD_BUILD_THREADS : 0;   // per-thread windows
 constexpr int kTileCells = kTX * kTY * kTZ;
 constexpr int kSegW = kTX + 3;            // cell boundaries per halo row (ext x = 0 .. tx + 2)
 constexpr int kSub = 16;                  // x sub-bins per cell for the window lookup
@@ -918,6 +929,8 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
     const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
     const int ncell = T.tx * T.ty * T.tz;
     float4* sF = reinterpret_cast<float4*>(smem);
+    unsigned* sWin = reinterpret_cast<unsigned*>(smem + 16 * ((size_t)a.stage_cap + 1));
+    (void)sWin;
     // (1) staging of the halo rows (fp32 mirror, 16 B per particle)
     for (int r = warp; r < T.R; r += kBuildThreads / 32) {
         const int b0 = a.tr.begin[tile * kRowsMax + r];
@@ -978,6 +991,78 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
         uint4* outb = a.nbr8 + t;
         unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
         int k = 0;
+#if LJMD_BUILD_FLAT
+        // accepted entries shift into four registers and leave as one 16-byte store per 8
+        auto emit = [&](int jl) {
+            w0 = __funnelshift_r(w0, w1, 16);
+            w1 = __funnelshift_r(w1, w2, 16);
+            w2 = __funnelshift_r(w2, w3, 16);
+            w3 = __funnelshift_r(w3, (unsigned)jl, 16);
+            if ((k & 7) == 7) {
+                if (k < K) *outb = make_uint4(w0, w1, w2, w3);
+                outb += stride;
+            }
+            ++k;
+        };
+        // (a) the x-windows of the non-empty stencil rows, in stencil order
+        int nr = 0, tot = 0;
+        unsigned long long sid = 0ull;   // stencil row rz * 3 + ry of window j, 4 bits each
+        for (int rz = 0; rz < 3; ++rz) {
+            const float ddz = rz == 0 ? fi.z - zlo : (rz == 2 ? zhi - fi.z : 0.f);
+            const float dz2 = fmaxf(ddz - slop, 0.f) * fmaxf(ddz - slop, 0.f);
+            for (int ry = 0; ry < 3; ++ry) {
+                const float ddy = ry == 0 ? fi.y - ylo : (ry == 2 ? yhi - fi.y : 0.f);
+                const float dyz2 = fmaf(fmaxf(ddy - slop, 0.f), fmaxf(ddy - slop, 0.f), dz2);
+                if (dyz2 >= thr_hi) continue;
+                const float xw = sqrtf(thr_hi - dyz2) + slop;
+                const int R = (lz + rz) * (T.ty + 2) + (ly + ry);
+                const float xl = fi.x - xw, xh = fi.x + xw;
+                const int g0 = kSub * lx, g1 = kSub * (lx + 3);
+                int gl = (int)floorf((xl - x0f) * inv_wsub) - 1;
+                int gh = (int)floorf((xh - x0f) * inv_wsub) + 2;
+                gl = min(max(gl, g0), g1);
+                gh = min(max(gh, g0), g1);
+                const int cl = min(gl / kSub, lx + 2), ch = min(gh / kSub, lx + 2);
+                const int lo = S.sub[R][cl][gl - kSub * cl];
+                const int hi = S.sub[R][ch][gh - kSub * ch];
+                if (hi > lo) {
+                    sWin[nr * kBuildThreads + threadIdx.x] = (unsigned)lo | ((unsigned)hi << 16);
+                    sid |= (unsigned long long)(rz * 3 + ry) << (4 * nr);
+                    ++nr;
+                    tot += hi - lo;
+                }
+            }
+        }
+        // (b) one loop over the concatenated windows (the own index is skipped: R4 self
+        // exclusion); candidate it + 1 is read while candidate it is decided
+        int j = 0;
+        unsigned wv = nr ? sWin[threadIdx.x] : 0u;
+        int jl = (int)(wv & 0xffffu), jend = (int)(wv >> 16);
+        float4 fj = sF[jl];
+        for (int it = 0; it < tot; ++it) {
+            const int jc = jl, jrow = j;
+            const float4 fc = fj;
+            if (++jl == jend) {
+                ++j;
+                wv = j < nr ? sWin[j * kBuildThreads + threadIdx.x] : 0u;
+                jl = (int)(wv & 0xffffu);
+                jend = (int)(wv >> 16);
+            }
+            fj = sF[jl];
+            const float fx = fi.x - fc.x, fy = fi.y - fc.y, fz = fi.z - fc.z;
+            const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+            if (r2f >= thr_hi || jc == li) continue;
+            bool take = r2f < thr_lo;
+            if (!take) {   // rare: decide in fp64 on the canonical r^2 (the oracle's test)
+                const int sr = (int)(sid >> (4 * jrow)) & 15;
+                const int R = (lz + sr / 3) * (T.ty + 2) + (ly + sr % 3);
+                const double4 xi = a.x[li + S.delta[R0]];
+                const double4 xj = a.x[jc + S.delta[R]];
+                take = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z) < a.rn2;
+            }
+            if (take) emit(jc);
+        }
+#else
         for (int rz = 0; rz < 3; ++rz) {
             const float ddz = rz == 0 ? fi.z - zlo : (rz == 2 ? zhi - fi.z : 0.f);
             const float dz2 = fmaxf(ddz - slop, 0.f) * fmaxf(ddz - slop, 0.f);
@@ -1026,6 +1111,7 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
                 }
             }
         }
+#endif
         if ((k & 7) && k < K) {   // pad the last block with the tile's sentinel index
             const unsigned sen = (unsigned)a.tr.off[tile * (kRowsMax + 1) + T.R];
             for (int e = k & 7; e < 8; ++e) {
@@ -1064,9 +1150,111 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
 // the cyclic search for the next available residue is one shift and one find-first-set
 // (225 us per C2 rebuild against 300 us with count and head arrays in shared memory).  A particle with a fuller
 // residue keeps the build order.
+// Round 2 (LJMD_RR_LEAN): the per-residue fill and take counters live as bytes in the
+// thread's shared-memory record instead of 64-bit nibble registers (whose variable 64-bit
+// shifts made the pass issue-bound: ~70 instructions per list entry, 232 us per C2 rebuild);
+// the same buckets, the same greedy walk, the same output.
+#ifndef LJMD_RR_LEAN
+#define LJMD_RR_LEAN 1
+#endif
 constexpr int kRrThreads = 128;
 constexpr int kRrCap = 8;                        // per-residue capacity (mean ~4.6)
 constexpr int kRrOvf = 16;                       // entries beyond a full bucket, emitted last
+#if LJMD_RR_LEAN
+// per thread: buckets u16[16][kRrCap], overflow u16[kRrOvf], fill counts u8[16], taken u8[16];
+// odd word stride (no bank aliasing between the threads' records)
+constexpr int kRrStrideW = (16 * kRrCap + kRrOvf) / 2 + 8 + 1;
+constexpr size_t kRrSmem = sizeof(unsigned) * (size_t)kRrThreads * kRrStrideW;
+
+__global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, int K, Geo g,
+                                                       const uint4* __restrict__ in,
+                                                       const int* __restrict__ ncount,
+                                                       const int* __restrict__ ocell_of,
+                                                       const int* __restrict__ obegin,
+                                                       const int* __restrict__ tile_oc0,
+                                                       uint4* __restrict__ out) {
+    extern __shared__ unsigned rr_smem[];
+    const int tid = threadIdx.x;
+    const int t = blockIdx.x * kRrThreads + tid;
+    unsigned* rec = rr_smem + (size_t)tid * kRrStrideW;
+    unsigned short* bkt = reinterpret_cast<unsigned short*>(rec);
+    unsigned short* ovf = bkt + 16 * kRrCap;
+    constexpr int kCw = (16 * kRrCap + kRrOvf) / 2;   // first counter word
+    unsigned char* C = reinterpret_cast<unsigned char*>(rec + kCw);
+    unsigned char* U = C + 16;
+    if (t >= n_own) return;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) rec[kCw + w] = 0u;
+    const int n = min(ncount[t], K);
+    const int nb = (n + 7) >> 3;
+    const size_t stride = (size_t)n_pad;
+    int cx, cy, cz;
+    lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
+    const int tile = tile_of_cell(g, cx, cy, cz);
+    const int off = (t - obegin[tile_oc0[tile]]) & 15;
+    int novf = 0;
+    bool overflow = false;
+    unsigned short pad = 0;
+    uint4 vn = nb > 0 ? in[t] : make_uint4(0u, 0u, 0u, 0u);
+    for (int b = 0; b < nb; ++b) {
+        const uint4 v = vn;
+        if (b + 1 < nb) vn = in[(size_t)(b + 1) * stride + t];   // next block in flight
+        const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const unsigned short l = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
+            if (b * 8 + e < n) {
+                const int r = l & 15;
+                const int c = C[r];
+                if (c < kRrCap) {
+                    bkt[r * kRrCap + c] = l;
+                    C[r] = (unsigned char)(c + 1);
+                } else if (novf < kRrOvf) {
+                    ovf[novf++] = l;
+                } else {
+                    overflow = true;
+                }
+            } else {
+                pad = l;   // the tile's sentinel
+            }
+        }
+    }
+    if (overflow) {
+        for (int b = 0; b < nb; ++b) out[(size_t)b * stride + t] = in[(size_t)b * stride + t];
+        return;
+    }
+    unsigned avail = 0u;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+        if (C[r]) avail |= 1u << r;
+    const int nin = n - novf;
+    unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;   // 8 pending entries, shifted in from the top
+    uint4* o = out + t;
+    unsigned av2 = avail | (avail << 16);   // bit r and r + 16: a rotation is one shift
+    int tgt = off;                          // (off + k) mod 16
+    for (int k = 0; k < nb * 8; ++k) {
+        unsigned l = pad;
+        if (k < nin) {
+            const int rr = (tgt + __ffs(av2 >> tgt) - 1) & 15;
+            tgt = (tgt + 1) & 15;
+            const int u = U[rr];
+            l = bkt[rr * kRrCap + u];
+            U[rr] = (unsigned char)(u + 1);
+            if (u + 1 == (int)C[rr]) av2 &= ~(0x10001u << rr);
+        } else if (k < n) {
+            l = ovf[k - nin];
+        }
+        w0 = __funnelshift_r(w0, w1, 16);
+        w1 = __funnelshift_r(w1, w2, 16);
+        w2 = __funnelshift_r(w2, w3, 16);
+        w3 = __funnelshift_r(w3, l, 16);
+        if ((k & 7) == 7) {
+            *o = make_uint4(w0, w1, w2, w3);
+            o += stride;
+        }
+    }
+}
+#else
 constexpr int kRrStrideW = (16 * kRrCap + kRrOvf) / 2 + 1;   // words per thread (odd: no bank aliasing)
 constexpr size_t kRrSmem = sizeof(unsigned) * (size_t)kRrThreads * kRrStrideW;
 
@@ -1156,6 +1344,8 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
         }
     }
 }
+
+#endif
 
 // --------------------------------------------------------------------------- force
 // LJ force over the full (both-orders) list, written only to i: no atomics.
@@ -1336,6 +1526,9 @@ constexpr int kRing = LJMD_RING;
 #ifndef LJMD_INT_CUT
 #define LJMD_INT_CUT 0
 #endif
+#ifndef LJMD_HICUT
+#define LJMD_HICUT 0
+#endif
 
 __device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
@@ -1377,6 +1570,9 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
 #if LJMD_INT_CUT
     const long long rc2b = __double_as_longlong(a.rc2);
 #endif
+#if LJMD_HICUT
+    const int rchi = __double2hiint(a.rc2);
+#endif
     for (int b = 0; b < nblk; ++b) {
         // a short block is padded with the sentinel, so every entry is evaluated unpredicated
         uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
@@ -1391,18 +1587,33 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
             cur = lds128(ring + (unsigned)((b % (kRing > 0 ? kRing : 1)) * kForceThreads * 16));
         }
         const unsigned w4[4] = {cur.x, cur.y, cur.z, cur.w};
+        unsigned nearm = 0u;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const unsigned l = (e & 1) ? (w4[e >> 1] >> 16) : (w4[e >> 1] & 0xffffu);
             const double* pj = reinterpret_cast<const double*>(sPb + 24u * l);
             const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
+#if LJMD_HICUT
+            // r^2 in FMA form (3 FP64 instructions instead of 5) and the cutoff on the high
+            // word of its bit pattern (ALU): a candidate whose high word differs from rc^2's
+            // by more than 1 is more than 2^32 ulps away, so the canonical r^2 (a few ulps off)
+            // takes the same decision; the rare rest re-decides on the canonical r^2 (R9)
+            // takes the same decision; the rare rest (|r - rc| < ~1e-6) is left out here and
+            // re-decided on the canonical r^2 after the block (R9)
+            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            const int dh = __double2hiint(r2) - rchi + 1;
+            const bool in = dh < 0;
+            nearm |= (unsigned)((unsigned)dh <= 2u) << e;
+#else
             const double r2 = r2_canon(dx, dy, dz);          // the oracle's r^2
+#endif
             const double ir2 = rcp64(r2);
             const double ir4 = ir2 * ir2;
             const double ir6 = ir4 * ir2;
             const double ir8 = ir4 * ir4;
             double gg = ir8 * fma(a.c12, ir6, a.nc6);
-#if LJMD_INT_CUT
+#if LJMD_HICUT
+#elif LJMD_INT_CUT
             const bool in = __double_as_longlong(r2) < rc2b;
 #else
             const bool in = r2 < a.rc2;
@@ -1416,6 +1627,26 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
                 u += in ? v : 0.0;
             }
         }
+#if LJMD_HICUT
+        // candidates within 2^32 ulps of rc^2: the canonical decision, one by one (almost never)
+        while (__builtin_expect(nearm != 0u, 0)) {
+            const int e = __ffs(nearm) - 1;
+            nearm &= nearm - 1u;
+            const unsigned wsel = (e & 4) ? ((e & 2) ? cur.w : cur.z) : ((e & 2) ? cur.y : cur.x);
+            const unsigned l = (wsel >> (16 * (e & 1))) & 0xffffu;
+            const double* pj = reinterpret_cast<const double*>(sPb + 24u * l);
+            const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
+            if (!(r2_canon(dx, dy, dz) < a.rc2)) continue;
+            const double ir2 = rcp64(fma(dz, dz, fma(dy, dy, dx * dx)));
+            const double ir4 = ir2 * ir2;
+            const double ir6 = ir4 * ir2;
+            const double gg = (ir4 * ir4) * fma(a.c12, ir6, a.nc6);
+            fx = fma(gg, dx, fx);
+            fy = fma(gg, dy, fy);
+            fz = fma(gg, dz, fz);
+            if (ENERGY) u += fma(fma(a.a12, ir6, a.na6), ir6, a.a0);
+        }
+#endif
         // block b + kRing into the slot of block b (just consumed): blocks b + 1 .. b + kRing - 1
         // stay in flight; block j >= 1 is commit group j - 1 of this particle
         if (kRing == 0) {

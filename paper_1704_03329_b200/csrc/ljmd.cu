@@ -549,7 +549,8 @@ ljmd_status alloc_list(ljmd_ctx* c, int K) {
 
 // ------------------------------------------------------------------ kernels launchers
 // k_build_nlist dynamic shared memory: the staged fp32 halo
-inline size_t build_smem(const ljmd_ctx* c) { return 16 * (size_t)(c->stage_cap + 1); }
+// (+ the per-thread x-windows of the flattened candidate loop)
+inline size_t build_smem(const ljmd_ctx* c) { return 16 * (size_t)(c->stage_cap + 1) + 4 * (size_t)kBuildWinWords; }
 
 ljmd_status launch_nlist(ljmd_ctx* c) {
     NlistArgs a;
@@ -591,6 +592,7 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     // fp32 pruning margin: position conversion (2^-24 X twice), face conversion, sqrt/fma
     // roundings -- 16 x the coordinate ulp plus an absolute floor
     a.slop_f = (float)(16.0 * std::ldexp(X, -23) + 1e-5);
+    a.stage_cap = c->stage_cap;
     k_build_nlist<<<c->n_tiles, kBuildThreads, build_smem(c), c->stream>>>(a);
     CKL();
     return LJMD_OK;
@@ -1310,14 +1312,21 @@ ljmd_status validate_step(ljmd_ctx* c, int vslot) {
 // capacity shortfall aborts the rest of the sequence and the host resumes at that step on
 // the eager path with regrown buffers (same arithmetic, same results).
 // Profilers and sanitizers cannot see the kernels of a graph with conditional nodes (ncu:
-// "not supported for profiling"), so under a CUDA injection tool (ncu, nsys,
-// compute-sanitizer set CUDA_INJECTION64_PATH) -- or with LJMD_GRAPHS=0 -- the same kernels
+// "not supported for profiling"), so under a CUDA injection tool (ncu, compute-sanitizer:
+// detected by the environment they give the target) -- or with LJMD_GRAPHS=0 -- the same kernels
 // run on the eager path instead.
 bool graphs_allowed() {
     static const bool ok = [] {
-        const char* inj = getenv("CUDA_INJECTION64_PATH");
+        // ncu sets NV_NSIGHT_INJECTION_TRANSPORT_TYPE, compute-sanitizer
+        // NV_SANITIZER_INJECTION_TRANSPORT_TYPE (measured on the B200 box; neither exports
+        // CUDA_INJECTION64_PATH to the target)
+        for (const char* v : {"CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                              "NV_SANITIZER_INJECTION_TRANSPORT_TYPE"}) {
+            const char* e = getenv(v);
+            if (e && *e) return false;
+        }
         const char* env = getenv("LJMD_GRAPHS");
-        return !(inj && *inj) && !(env && env[0] == '0');
+        return !(env && env[0] == '0');
     }();
     return ok;
 }
