@@ -243,7 +243,19 @@ def main():
 
     dist = None
     id_buf = None
-    if world > 1:
+    one_device = os.environ.get("LJMD_BENCH_DEVICE") is not None
+    if world > 1 and one_device:
+        # every rank on ONE GPU (NCCL refuses two ranks per device): gloo for the host-side
+        # plumbing and the engine's host-staged multi-process transport (LJMDSHM); the same
+        # rank logic, barriers and max-over-ranks timing as the NCCL run, for testing it
+        import ctypes
+        import uuid
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        key = [uuid.uuid4().hex if rank == 0 else None]
+        dist.broadcast_object_list(key, 0)
+        id_buf = ctypes.create_string_buffer(ljmd.shm_group_id(key[0]), 128)
+    elif world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         # the engine's own NCCL communicator: rank 0 creates the id, torch broadcasts it
@@ -262,7 +274,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if one_device else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -531,7 +543,8 @@ def main():
                    "l2": "working set > L2 (16-bit list %.0f MB + positions %.0f MB + v, F %.0f MB)" % (
                        2 * cand / 1e6, 56 * (n + st1["n_ghost"]) / 1e6, 48 * n / 1e6)},
         "gpu_launches": int(st1["kernel_launches"] - st0["kernel_launches"]),
-        "transport": "nccl" if (world > 1 or args.split_self) else "none",
+        "transport": ("shm (all ranks on one GPU)" if one_device and world > 1 else "nccl")
+        if (world > 1 or args.split_self) else "none",
         "roofline": {"bound": "alu",
                      "kernel": "k_force_half (fp64 LJ pair loop)" if args.newton3 else "k_force (fp64 LJ pair loop)", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,

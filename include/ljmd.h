@@ -306,7 +306,9 @@ ljmd_status ljmd_loop_free(ljmd_ctx* c, int64_t loop);
  * bytes (e.g. with torch.distributed) into ljmd_options.nccl_id on every rank.  An id
  * that starts with "LJMDLOCAL" instead selects the in-process loopback transport (several
  * contexts of one process exchanging through device copies; used by the tests to run the
- * multi-rank path on one GPU). */
+ * multi-rank path on one GPU), and one that starts with "LJMDSHM:<key>" the host-staged
+ * multi-PROCESS transport (ranks in separate processes on one GPU, transfers staged through
+ * files under /dev/shm; correctness path for the multi-process flow, synchronous). */
 ljmd_status ljmd_nccl_unique_id(void* out128);
 
 /* Measurement utility (bench.py roofline denominator): FP64 FMA throughput of the

@@ -873,6 +873,7 @@ struct NlistArgs {
     DevFlags* fl;
     const int* slot_gid;
     int stage_cap;       // staged records per tile the dynamic shared memory is sized for
+    int parts;           // CTAs per tile (small systems)
 };
 
 // One CTA per force tile (the same halo rows and local numbering as k_force).
@@ -920,7 +921,9 @@ struct BuildSmem {
 __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(NlistArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ BuildSmem S;
-    const int tile = blockIdx.x;
+    // a.parts CTAs per tile on small systems (each stages the whole halo, takes a share of
+    // the particles): enough CTAs for the chip where tiles are few
+    const int tile = blockIdx.x / a.parts, part = blockIdx.x % a.parts;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Geo& g = a.g;
     const TileGeo T = tile_geo(g, tile);
@@ -977,7 +980,9 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
     const int K = a.K;
     unsigned long long kk = 0ull;
     int kmax = 0;
-    for (int q = threadIdx.x; q < m; q += kBuildThreads) {
+    const int per = (m + a.parts - 1) / a.parts;
+    const int q_end = min(m, (part + 1) * per);
+    for (int q = part * per + (int)threadIdx.x; q < q_end; q += kBuildThreads) {
         int ci = 0;
         while (ci + 1 < ncell && S.cell_t0[ci + 1] <= q) ++ci;
         const int lx = ci % T.tx, ly = (ci / T.tx) % T.ty, lz = ci / (T.tx * T.ty);

@@ -593,7 +593,8 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     // roundings -- 16 x the coordinate ulp plus an absolute floor
     a.slop_f = (float)(16.0 * std::ldexp(X, -23) + 1e-5);
     a.stage_cap = c->stage_cap;
-    k_build_nlist<<<c->n_tiles, kBuildThreads, build_smem(c), c->stream>>>(a);
+    a.parts = c->fparts;   // the force kernel's CTAs per tile (1 on large systems)
+    k_build_nlist<<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
     CKL();
     return LJMD_OK;
 }

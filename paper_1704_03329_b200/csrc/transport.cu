@@ -4,8 +4,15 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cctype>
 #include <cstring>
+#include <thread>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -207,6 +214,122 @@ private:
     cudaEvent_t ready_ = nullptr, done_ = nullptr;
 };
 
+
+// ------------------------------------------------------------------------------- host-staged files
+// Several PROCESSES on one GPU (NCCL refuses two ranks on one device): every transfer is
+// staged through host memory as a file in a directory under /dev/shm shared by the ranks,
+// named (call sequence, src, dst, index) and unlinked by its reader; an all-reduce is an
+// all-to-all of the vectors reduced in rank order on every rank (deterministic, equal
+// everywhere).  Synchronous on the host: a correctness path for the multi-process flow
+// (bench.py under torchrun with LJMD_BENCH_DEVICE), not a fast one.
+class ShmTransport : public Transport {
+public:
+    ShmTransport(std::string dir, int rank, int nranks) : dir_(std::move(dir)), rank_(rank), n_(nranks) {
+        mkdir(dir_.c_str(), 0700);
+    }
+    ~ShmTransport() override { rmdir(dir_.c_str()); }   // the last rank out removes it
+    bool exchange(cudaStream_t stream, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                  std::string& err) override {
+        const long long seq = ++seq_;
+        if (cudaStreamSynchronize(stream) != cudaSuccess) return fail(err, "stream sync");
+        std::map<int, int> ks;
+        for (const Xfer& x : sends)
+            if (!post(stream, 'x', seq, rank_, x.peer, ks[x.peer]++, x.ptr, x.bytes, err)) return false;
+        std::map<int, int> kr;
+        for (const Xfer& x : recvs)
+            if (!take(stream, 'x', seq, x.peer, rank_, kr[x.peer]++, x.ptr, x.bytes, err)) return false;
+        return true;
+    }
+    bool allreduce(cudaStream_t stream, double* dbuf, int n, bool max, std::string& err) override {
+        const long long seq = ++seq_;
+        std::vector<double> mine(n), acc, other(n);
+        if (cudaMemcpyAsync(mine.data(), dbuf, sizeof(double) * n, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+            cudaStreamSynchronize(stream) != cudaSuccess)
+            return fail(err, "allreduce D2H");
+        for (int q = 0; q < n_; ++q)
+            if (q != rank_ && !write_file(name('r', seq, rank_, q, 0), mine.data(), sizeof(double) * n, err))
+                return false;
+        for (int q = 0; q < n_; ++q) {   // rank order: every rank sums in the same order
+            const double* v = mine.data();
+            if (q != rank_) {
+                if (!read_file(name('r', seq, q, rank_, 0), other.data(), sizeof(double) * n, err)) return false;
+                v = other.data();
+            }
+            if (q == 0) acc.assign(v, v + n);
+            else
+                for (int i = 0; i < n; ++i) acc[i] = max ? std::max(acc[i], v[i]) : acc[i] + v[i];
+        }
+        if (cudaMemcpyAsync(dbuf, acc.data(), sizeof(double) * n, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+            cudaStreamSynchronize(stream) != cudaSuccess)
+            return fail(err, "allreduce H2D");
+        return true;
+    }
+    const char* name() const override { return "shm"; }
+
+private:
+    static bool fail(std::string& err, const char* what) {
+        err = std::string("shm transport: ") + what + " failed";
+        return false;
+    }
+    std::string name(char ch, long long seq, int src, int dst, int k) const {
+        char b[96];
+        std::snprintf(b, sizeof b, "/%c%lld_%d_%d_%d", ch, seq, src, dst, k);
+        return dir_ + b;
+    }
+    bool write_file(const std::string& path, const void* p, size_t bytes, std::string& err) {
+        const std::string tmp = path + ".tmp";
+        FILE* f = std::fopen(tmp.c_str(), "wb");
+        if (!f || (bytes && std::fwrite(p, 1, bytes, f) != bytes) || std::fclose(f) != 0 ||
+            std::rename(tmp.c_str(), path.c_str()) != 0) {
+            err = "shm transport: cannot write " + path;
+            return false;
+        }
+        return true;
+    }
+    bool read_file(const std::string& path, void* p, size_t bytes, std::string& err) {
+        const auto t0 = std::chrono::steady_clock::now();
+        struct stat st;
+        while (stat(path.c_str(), &st) != 0) {   // the writer renames a complete file into place
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) {
+                err = "shm transport: timed out waiting for " + path;
+                return false;
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+        if ((size_t)st.st_size != bytes) {
+            err = "shm transport: size mismatch on " + path;
+            return false;
+        }
+        FILE* f = std::fopen(path.c_str(), "rb");
+        const bool ok = f && (!bytes || std::fread(p, 1, bytes, f) == bytes);
+        if (f) std::fclose(f);
+        std::remove(path.c_str());
+        if (!ok) err = "shm transport: cannot read " + path;
+        return ok;
+    }
+    bool post(cudaStream_t stream, char ch, long long seq, int src, int dst, int k, const void* dptr, size_t bytes,
+              std::string& err) {
+        buf_.resize(bytes);
+        if (bytes && (cudaMemcpyAsync(buf_.data(), dptr, bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+                      cudaStreamSynchronize(stream) != cudaSuccess))
+            return fail(err, "D2H");
+        return write_file(name(ch, seq, src, dst, k), buf_.data(), bytes, err);
+    }
+    bool take(cudaStream_t stream, char ch, long long seq, int src, int dst, int k, void* dptr, size_t bytes,
+              std::string& err) {
+        buf_.resize(bytes);
+        if (!read_file(name(ch, seq, src, dst, k), buf_.data(), bytes, err)) return false;
+        if (bytes && (cudaMemcpyAsync(dptr, buf_.data(), bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+                      cudaStreamSynchronize(stream) != cudaSuccess))
+            return fail(err, "H2D");
+        return true;
+    }
+    std::string dir_;
+    int rank_, n_;
+    long long seq_ = 0;
+    std::vector<unsigned char> buf_;
+};
+
 }  // namespace
 
 Transport* make_transport(const void* nccl_id, int rank, int nranks, int device, std::string& err) {
@@ -240,6 +363,14 @@ Transport* make_transport(const void* nccl_id, int rank, int nranks, int device,
             ++g->members;
         }
         return new LocalTransport(g, key, rank);
+    }
+    if (std::strncmp(id, "LJMDSHM:", 8) == 0) {   // processes on one device (tests, bench debug)
+        std::string key(id + 8, strnlen(id + 8, 120));
+        for (char& ch : key)
+            if (!std::isalnum((unsigned char)ch)) ch = '_';
+        struct stat st;
+        const std::string root = stat("/dev/shm", &st) == 0 ? "/dev/shm" : "/tmp";
+        return new ShmTransport(root + "/ljmd_" + key, rank, nranks);
     }
     NcclApi& api = nccl_api(err);
     if (!api.ok) return nullptr;

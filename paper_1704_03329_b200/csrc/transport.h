@@ -8,6 +8,9 @@
 //                      exchanging through a process-wide registry with D2D copies and CUDA
 //                      events.  Used to run the multi-rank device path on a single B200 in the
 //                      tests; selected by an id starting with "LJMDLOCAL".
+//   * ShmTransport   : several PROCESSES on one GPU (NCCL refuses two ranks per device):
+//                      transfers staged through host files under /dev/shm; selected by an id
+//                      "LJMDSHM:<key>".  Tests and bench.py's one-GPU multi-process run.
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>

@@ -202,6 +202,15 @@ def local_group_id(key: str) -> bytes:
     return b + b"\0" * (128 - len(b))
 
 
+def shm_group_id(key: str) -> bytes:
+    """Id of a host-staged multi-PROCESS group on one GPU (NCCL refuses two ranks per device):
+    every rank passes the same key."""
+    b = ("LJMDSHM:" + key).encode()
+    if len(b) > 127:
+        raise ValueError("key too long")
+    return b + b"\0" * (128 - len(b))
+
+
 def version() -> str:
     return load().ljmd_version().decode()
 
