@@ -932,8 +932,9 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
     const int m = a.obegin[a.tile_oc0[tile + 1]] - t0;
     const int ncell = T.tx * T.ty * T.tz;
     float4* sF = reinterpret_cast<float4*>(smem);
+#if LJMD_BUILD_FLAT
     unsigned* sWin = reinterpret_cast<unsigned*>(smem + 16 * ((size_t)a.stage_cap + 1));
-    (void)sWin;
+#endif
     // (1) staging of the halo rows (fp32 mirror, 16 B per particle)
     for (int r = warp; r < T.R; r += kBuildThreads / 32) {
         const int b0 = a.tr.begin[tile * kRowsMax + r];
@@ -1393,6 +1394,11 @@ struct ForceArgs {
     const unsigned* halo_flag;   // null: no gating
     unsigned halo_seq;           // the value the flag reaches once this step's halo has landed
     int nint, layer;             // interior tiles, tiles per z layer
+    // boundary-first launch (nranks > 1): the two boundary tile layers go first (launch
+    // indices [0, 2 layer)), each of their CTAs adds 1 to *bdone when its epilogue (which
+    // writes the outgoing halo) is done, so the next halo exchange starts during the interior
+    int bfirst;
+    unsigned* bdone;
     DevFlags* fl;
     int n_own, n_pad;
     double rc2, c12, nc6, a12, na6, a0;   // nc6 = -c6, na6 = -a6 (fold into DFMA operands)
@@ -1592,7 +1598,9 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
             cur = lds128(ring + (unsigned)((b % (kRing > 0 ? kRing : 1)) * kForceThreads * 16));
         }
         const unsigned w4[4] = {cur.x, cur.y, cur.z, cur.w};
+#if LJMD_HICUT == 1
         unsigned nearm = 0u;
+#endif
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const unsigned l = (e & 1) ? (w4[e >> 1] >> 16) : (w4[e >> 1] & 0xffffu);
@@ -1607,8 +1615,13 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
             // re-decided on the canonical r^2 after the block (R9)
             const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
             const int dh = __double2hiint(r2) - rchi + 1;
+#if LJMD_HICUT == 2   // predicated: the canonical test where the high words are within 1
+            bool in = dh < 0;
+            if ((unsigned)dh <= 2u) in = r2_canon(dx, dy, dz) < a.rc2;
+#else
             const bool in = dh < 0;
             nearm |= (unsigned)((unsigned)dh <= 2u) << e;
+#endif
 #else
             const double r2 = r2_canon(dx, dy, dz);          // the oracle's r^2
 #endif
@@ -1632,7 +1645,7 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
                 u += in ? v : 0.0;
             }
         }
-#if LJMD_HICUT
+#if LJMD_HICUT == 1
         // candidates within 2^32 ulps of rc^2: the canonical decision, one by one (almost never)
         while (__builtin_expect(nearm != 0u, 0)) {
             const int e = __ffs(nearm) - 1;
@@ -1739,6 +1752,8 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     // layer [T - L, T) -- whose launch index is its own tile index
 #if !LJMD_SEG_OFF
     if (a.halo_flag) tile = ti < a.nint ? a.layer + ti : (ti - a.nint < a.layer ? ti - a.nint : ti);
+    // boundary-first order: lower layer [0, L), upper layer [T - L, T), then the interior
+    if (a.bfirst) tile = ti < a.layer ? ti : (ti < 2 * a.layer ? a.nint + ti : ti - a.layer);
 #endif
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // captured steps: skip everything after an aborted rebuild, before any table of it is
@@ -1872,6 +1887,13 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
             a.ke_part[tile * a.parts + part] = k2;
         }
     }
+#if !LJMD_SEG_OFF
+    if (a.bfirst && ti < 2 * a.layer) {   // this CTA's outgoing halo copies are written
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(a.bdone, 1u);
+    }
+#endif
 }
 
 // opening half of a step() call: v += h F ; x += dt v  (in place, owned slots)

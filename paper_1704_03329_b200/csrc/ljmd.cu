@@ -6,6 +6,7 @@
 #include "dsl.h"
 #include "transport.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -234,6 +235,12 @@ struct ljmd_ctx {
     int gbeg[2] = {0, 0}, glen[2] = {0, 0};   // my lower / upper ghost plane: slots
     unsigned* halo_flag = nullptr;    // gated boundary tiles: released per step by the halo stream
     unsigned halo_seq = 0;
+    // boundary-first force launches (nranks > 1): the boundary CTAs count themselves done in
+    // *bdone; the next step's halo exchange waits for that count on aux_stream (a stream
+    // memory wait) and overlaps the interior tiles of the same launch
+    unsigned* bdone = nullptr;
+    unsigned bdone_issued = 0;        // the count every boundary CTA issued so far reaches
+    bool halo_queued = false;         // the next step's halo is in flight on aux_stream (ev_halo)
 };
 
 ljmd_status dsl_before_sort(ljmd_ctx* c, const int* gid_old);
@@ -654,6 +661,8 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.gap = 0;
     a.halo_flag = nullptr;
     a.halo_seq = 0;
+    a.bfirst = 0;
+    a.bdone = nullptr;
     a.nint = 0;
     a.layer = 0;
     return a;
@@ -814,6 +823,19 @@ void force_range(ljmd_ctx* c, ForceArgs a, int first, int count, cudaStream_t st
 template <bool E, int M, bool C>
 void force_all(ljmd_ctx* c, const ForceArgs& a, bool halo_pending) {
     const int layer = c->geo.ntx * c->geo.nty;
+    if (c->bdone) {
+        // nranks > 1 (aux stream): one launch, boundary tile layers first; their completion
+        // count lets the next halo exchange start while the interior tiles compute
+        if (halo_pending) cudaStreamWaitEvent(c->stream, c->ev_halo, 0);
+        ForceArgs g = a;
+        g.bfirst = 1;
+        g.bdone = c->bdone;
+        g.nint = c->n_tiles - 2 * layer;
+        g.layer = layer;
+        c->bdone_issued += (unsigned)(2 * layer * c->fparts);
+        force_range<E, M, C>(c, g, 0, c->n_tiles);
+        return;
+    }
     if (!halo_pending) {
         force_range<E, M, C>(c, a, 0, c->n_tiles);
         return;
@@ -899,6 +921,25 @@ ljmd_status collect_profile(ljmd_ctx* c, int64_t first_launch) {
     return LJMD_OK;
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point (no link against libcuda)
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32Fn stream_wait_value() {
+    static const WaitValue32Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (WaitValue32Fn) nullptr;
+        return reinterpret_cast<WaitValue32Fn>(p);
+    }();
+    return fn;
+}
+
+int getenv_int(const char* k, int d) {
+    const char* v = getenv(k);
+    return v && *v ? atoi(v) : d;
+}
+
 // Grouped exchange with the z neighbours, in the fixed order that also pairs correctly for
 // nranks = 2 (both neighbours are the same rank): send (up, down), receive (from below,
 // from above).  hi/lo payloads: what goes to the upper / lower neighbour.
@@ -936,11 +977,12 @@ ljmd_status halo_exchange(ljmd_ctx* c, cudaStream_t st = nullptr) {
 // Per step (nranks > 1): the send areas (written by the kernels that moved the particles)
 // go to the neighbours and land in their ghost planes, positions and packed positions; the
 // posting order pairs correctly also when both neighbours are one rank (p = 2).
-ljmd_status halo_direct(ljmd_ctx* c, cudaStream_t st = nullptr) {
+ljmd_status halo_direct(ljmd_ctx* c, cudaStream_t st = nullptr, int buf = -1) {
     // double4 records (32 B: every slot aligned for the transfer); the packed copy the force
     // kernel stages is written for the two received planes right after
     if (!st) st = c->stream;
-    double4* X = c->x[c->xc];
+    if (buf < 0) buf = c->xc;
+    double4* X = c->x[buf];
     const size_t base = (size_t)c->slot_cap;
     const size_t e4 = sizeof(double4);
     const size_t a0 = (size_t)c->area[0], a1 = (size_t)c->area[1];
@@ -950,7 +992,7 @@ ljmd_status halo_direct(ljmd_ctx* c, cudaStream_t st = nullptr) {
     if (!c->tr->exchange(st, sends, recvs, err)) return set_err(c, LJMD_E_NCCL, "%s", err.c_str());
     const int nr = c->glen[0] + c->glen[1];
     if (nr > 0) {
-        k_xp_from_x<<<nblk(nr, 256), 256, 0, st>>>(c->gbeg[0], c->glen[0], c->gbeg[1], c->glen[1], X, c->xp[c->xc]);
+        k_xp_from_x<<<nblk(nr, 256), 256, 0, st>>>(c->gbeg[0], c->glen[0], c->gbeg[1], c->glen[1], X, c->xp[buf]);
         CKL();
     }
     return LJMD_OK;
@@ -1768,6 +1810,15 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
             set_err(c, LJMD_E_CUDA, "halo flag allocation failed");
             return fail(LJMD_E_CUDA);
         }
+        // boundary-first launches with the halo started from a stream memory wait (when the
+        // driver offers cuStreamWaitValue32; else the interior / boundary split launches)
+        if (stream_wait_value() && getenv_int("LJMD_BFIRST", 1)) {
+            if (cudaMalloc(&c->bdone, sizeof(unsigned)) != cudaSuccess ||
+                cudaMemset(c->bdone, 0, sizeof(unsigned)) != cudaSuccess) {
+                set_err(c, LJMD_E_CUDA, "halo counter allocation failed");
+                return fail(LJMD_E_CUDA);
+            }
+        }
     }
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
@@ -1948,13 +1999,20 @@ ljmd_status step_eager(ljmd_ctx* c, int64_t s_first, int64_t nsteps, bool rebuil
                 due = 4.0 * m2 > delta2;
             }
             if (due) {
+                if (c->halo_queued) {   // the rebuild re-exchanges: let the queued halo land first
+                    CK(cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+                    c->halo_queued = false;
+                }
                 TRY(rebuild(c));
                 c->since = 0;
                 note_rebuild(c, c->steps_done);
             } else {
                 // ghost images of owned particles were written with the positions (force
                 // epilogue / kick-drift); received halo planes need theirs after the exchange
-                if (c->split && c->aux_stream) {
+                if (c->halo_queued) {   // started by the previous launch's boundary tiles
+                    c->halo_queued = false;
+                    halo_pending = true;
+                } else if (c->split && c->aux_stream) {
                     // the halo travels on aux_stream while the interior tiles compute
                     CK(cudaEventRecord(c->ev_ready, c->stream));
                     CK(cudaStreamWaitEvent(c->aux_stream, c->ev_ready, 0));
@@ -1984,6 +2042,17 @@ ljmd_status step_eager(ljmd_ctx* c, int64_t s_first, int64_t nsteps, bool rebuil
             ++c->call_nsamp;
         }
         if (!last) c->xc ^= 1;
+        // the next step's halo: x(n+1) of the boundary planes is in the send areas once the
+        // boundary CTAs of this launch have counted themselves done -- exchanged on aux_stream
+        // while the interior tiles compute (not before a known rebuild, which re-exchanges)
+        if (!last && c->bdone && !(!check && c->since + 1 >= c->opt.rebuild_every)) {
+            if (stream_wait_value()(reinterpret_cast<CUstream>(c->aux_stream), reinterpret_cast<CUdeviceptr>(c->bdone),
+                                    c->bdone_issued, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return set_err(c, LJMD_E_CUDA, "cuStreamWaitValue32 failed");
+            TRY(halo_direct(c, c->aux_stream, c->xc));
+            CK(cudaEventRecord(c->ev_halo, c->aux_stream));
+            c->halo_queued = true;
+        }
     }
     return LJMD_OK;
 }
@@ -2404,6 +2473,7 @@ void ljmd_destroy(ljmd_ctx* c) {
     }
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    if (c->bdone) cudaFree(c->bdone);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -4,8 +4,9 @@ and the totals, from `ncu -i --page source --print-source sass --csv`."""
 import csv, io, subprocess, sys
 rep, kre = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kre}", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+extra = sys.argv[4:]   # e.g. --launch-skip 2 --launch-count 1
+raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kre}", "--print-source", "sass",
+                      *extra], capture_output=True, text=True).stdout
 lines = raw.splitlines()
 hdr_i = [i for i, l in enumerate(lines) if l.startswith('"Address"')][0]
 rows = list(csv.reader(io.StringIO("\n".join(lines[hdr_i:]))))
