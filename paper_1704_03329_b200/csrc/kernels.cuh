@@ -1537,9 +1537,6 @@ constexpr int kRing = LJMD_RING;
 #ifndef LJMD_INT_CUT
 #define LJMD_INT_CUT 0
 #endif
-#ifndef LJMD_HICUT
-#define LJMD_HICUT 0
-#endif
 
 __device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
@@ -1581,9 +1578,6 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
 #if LJMD_INT_CUT
     const long long rc2b = __double_as_longlong(a.rc2);
 #endif
-#if LJMD_HICUT
-    const int rchi = __double2hiint(a.rc2);
-#endif
     for (int b = 0; b < nblk; ++b) {
         // a short block is padded with the sentinel, so every entry is evaluated unpredicated
         uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
@@ -1598,40 +1592,18 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
             cur = lds128(ring + (unsigned)((b % (kRing > 0 ? kRing : 1)) * kForceThreads * 16));
         }
         const unsigned w4[4] = {cur.x, cur.y, cur.z, cur.w};
-#if LJMD_HICUT == 1
-        unsigned nearm = 0u;
-#endif
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const unsigned l = (e & 1) ? (w4[e >> 1] >> 16) : (w4[e >> 1] & 0xffffu);
             const double* pj = reinterpret_cast<const double*>(sPb + 24u * l);
             const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
-#if LJMD_HICUT
-            // r^2 in FMA form (3 FP64 instructions instead of 5) and the cutoff on the high
-            // word of its bit pattern (ALU): a candidate whose high word differs from rc^2's
-            // by more than 1 is more than 2^32 ulps away, so the canonical r^2 (a few ulps off)
-            // takes the same decision; the rare rest re-decides on the canonical r^2 (R9)
-            // takes the same decision; the rare rest (|r - rc| < ~1e-6) is left out here and
-            // re-decided on the canonical r^2 after the block (R9)
-            const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-            const int dh = __double2hiint(r2) - rchi + 1;
-#if LJMD_HICUT == 2   // predicated: the canonical test where the high words are within 1
-            bool in = dh < 0;
-            if ((unsigned)dh <= 2u) in = r2_canon(dx, dy, dz) < a.rc2;
-#else
-            const bool in = dh < 0;
-            nearm |= (unsigned)((unsigned)dh <= 2u) << e;
-#endif
-#else
             const double r2 = r2_canon(dx, dy, dz);          // the oracle's r^2
-#endif
             const double ir2 = rcp64(r2);
             const double ir4 = ir2 * ir2;
             const double ir6 = ir4 * ir2;
             const double ir8 = ir4 * ir4;
             double gg = ir8 * fma(a.c12, ir6, a.nc6);
-#if LJMD_HICUT
-#elif LJMD_INT_CUT
+#if LJMD_INT_CUT
             const bool in = __double_as_longlong(r2) < rc2b;
 #else
             const bool in = r2 < a.rc2;
@@ -1645,26 +1617,7 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
                 u += in ? v : 0.0;
             }
         }
-#if LJMD_HICUT == 1
-        // candidates within 2^32 ulps of rc^2: the canonical decision, one by one (almost never)
-        while (__builtin_expect(nearm != 0u, 0)) {
-            const int e = __ffs(nearm) - 1;
-            nearm &= nearm - 1u;
-            const unsigned wsel = (e & 4) ? ((e & 2) ? cur.w : cur.z) : ((e & 2) ? cur.y : cur.x);
-            const unsigned l = (wsel >> (16 * (e & 1))) & 0xffffu;
-            const double* pj = reinterpret_cast<const double*>(sPb + 24u * l);
-            const double dx = xi.x - pj[0], dy = xi.y - pj[1], dz = xi.z - pj[2];
-            if (!(r2_canon(dx, dy, dz) < a.rc2)) continue;
-            const double ir2 = rcp64(fma(dz, dz, fma(dy, dy, dx * dx)));
-            const double ir4 = ir2 * ir2;
-            const double ir6 = ir4 * ir2;
-            const double gg = (ir4 * ir4) * fma(a.c12, ir6, a.nc6);
-            fx = fma(gg, dx, fx);
-            fy = fma(gg, dy, fy);
-            fz = fma(gg, dz, fz);
-            if (ENERGY) u += fma(fma(a.a12, ir6, a.na6), ir6, a.a0);
-        }
-#endif
+
         // block b + kRing into the slot of block b (just consumed): blocks b + 1 .. b + kRing - 1
         // stay in flight; block j >= 1 is commit group j - 1 of this particle
         if (kRing == 0) {
