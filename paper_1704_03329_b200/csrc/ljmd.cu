@@ -162,6 +162,10 @@ struct ljmd_ctx {
     // call was a sample step, or the init sequence): ljmd_get_energy need not recompute
     bool energy_current = false;
     double cur_pe = 0.0, cur_ke = 0.0;
+    // the init sequence's PE/KE travel to mapped memory without a host wait; read at the next
+    // synchronisation (end of ljmd_step) or on demand (settle_init)
+    double* h_init = nullptr;
+    bool init_pending = false, init_current = false;
     // ---- graph mode (single rank): ljmd_step captured into CUDA graphs, rebuild decided and
     // capacity-checked on the device
     DevCtl* d_ctl = nullptr;
@@ -1591,10 +1595,16 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const 
         const int b = dpos_in == c->stg[0] ? 0 : 1;
         CK(cudaEventRecord(c->stg_used[b], c->stream));
     }
-    TRY(sync_flags(c));
-    if (c->h_fl->nonfinite_gid != INT_MAX)
-        return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
-                       c->h_fl->nonfinite_gid);
+    // one rank: the non-finite flag (kept by reset_flags) is read at the rebuild's first
+    // synchronisation (k_wrap_bin bins a non-finite particle harmlessly); several ranks
+    // check before the migration
+    if (c->split) {
+        TRY(sync_flags(c));
+        if (c->h_fl->nonfinite_gid != INT_MAX)
+            return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
+                           c->h_fl->nonfinite_gid);
+    }
+    c->init_pending = false;
     c->n_own = (int)n;
     c->since = 0;
     c->steps_done = 0;
@@ -1610,16 +1620,32 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const 
     TRY(launch_force(c, true, kStore, false));
     TRY(finalize_energy(c, c->hist));
     TRY(allreduce(c, c->hist, 2, false));
-    TRY(pull_hist(c, 1));
-    c->cur_pe = c->h_hist[0];
-    c->cur_ke = c->h_hist[1];
+    if (!c->h_init) CK(cudaHostAlloc(&c->h_init, sizeof(double) * 2, cudaHostAllocMapped));
+    TRY(to_host(c, c->h_init, c->hist, sizeof(double) * 2));   // no host wait (settle_init)
+    c->init_pending = true;
+    c->init_current = true;
     c->energy_current = true;
+    return LJMD_OK;
+}
+
+// The init sequence's energies: first entry of the history; the current PE/KE while no step
+// has run since.  Waits for the stream (callers are at a synchronisation point anyway).
+ljmd_status settle_init(ljmd_ctx* c) {
+    if (!c->init_pending) return LJMD_OK;
+    CK(cudaStreamSynchronize(c->stream));
+    c->h_hist.insert(c->h_hist.begin(), c->h_init, c->h_init + 2);
+    if (c->init_current) {
+        c->cur_pe = c->h_init[0];
+        c->cur_ke = c->h_init[1];
+    }
+    c->init_pending = false;
     return LJMD_OK;
 }
 
 // PE, KE and e_i of the current state: reused when the last step of the previous
 // ljmd_step call (or the init sequence) sampled them, otherwise one Energy force pass
 ljmd_status energy_now(ljmd_ctx* c) {
+    TRY(settle_init(c));
     if (c->energy_current) return LJMD_OK;
     TRY(launch_force(c, true, kStore, false));
     TRY(ensure_hist(c, 1));
@@ -2216,6 +2242,7 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
     const int64_t first_launch = c->force_launches;
     const int64_t step0 = c->steps_done;
     c->energy_current = false;
+    c->init_current = false;
     if (c->opt.validate) {
         if (c->vhist_cap < nsteps) {
             TRY(dalloc(c, &c->vhist, (size_t)2 * nsteps));
@@ -2230,6 +2257,7 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         TRY(kick_drift(c));
         TRY(step_eager(c, 1, nsteps, false));
     }
+    TRY(settle_init(c));
     TRY(pull_hist(c, c->call_nsamp));
     if (c->energy_current) {
         c->cur_pe = c->h_hist[c->h_hist.size() - 2];
@@ -2314,6 +2342,7 @@ ljmd_status ljmd_get_energy(ljmd_ctx* c, double* pe, double* ke) {
 
 ljmd_status ljmd_get_energy_history(ljmd_ctx* c, double* pe, double* ke, int64_t cap, int64_t* count) {
     TRY(check_ctx(c));
+    TRY(settle_init(c));
     int64_t avail = (int64_t)c->h_hist.size() / 2;
     if (count) *count = avail;
     for (int64_t i = 0; i < std::min(cap, avail); ++i) {
@@ -2380,6 +2409,7 @@ ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s) {
     s->regrows = c->regrows;
     s->force_launches = c->force_launches;
     s->force_ms = c->force_ms;
+    TRY(settle_init(c));
     s->energy_samples = (int64_t)c->h_hist.size() / 2;
     s->kernel_launches = c->kernel_launches;
     TRY(to_host(c, c->h_st, c->d_st, sizeof(DevStats)));
@@ -2455,6 +2485,7 @@ void ljmd_destroy(ljmd_ctx* c) {
                     (void*)c->vpos, (void*)c->vhist})
         if (p) cudaFree(p);
     if (c->h_histm) cudaFreeHost(c->h_histm);
+    if (c->h_init) cudaFreeHost(c->h_init);
     if (c->h_slots) cudaFreeHost(c->h_slots);
     for (auto e : c->ev) cudaEventDestroy(e);
     if (c->copy_stream) {
