@@ -874,6 +874,7 @@ struct NlistArgs {
     const int* slot_gid;
     int stage_cap;       // staged records per tile the dynamic shared memory is sized for
     int parts;           // CTAs per tile (small systems)
+    int* own_li;         // out: each owned particle's index in its tile's staged halo
 };
 
 // One CTA per force tile (the same halo rows and local numbering as k_force).
@@ -989,6 +990,7 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
         const int lx = ci % T.tx, ly = (ci / T.tx) % T.ty, lz = ci / (T.tx * T.ty);
         const int R0 = (lz + 1) * (T.ty + 2) + (ly + 1);
         const int li = S.seg[R0][lx + 1] + (q - S.cell_t0[ci]);   // own local index
+        a.own_li[t0 + q] = li;
         const float4 fi = sF[li];
         const int cy = T.y0 + ly, cz = T.z0 + lz;
         const float ylo = a.ylo_f[cy], yhi = a.ylo_f[cy + 1];
@@ -1375,6 +1377,7 @@ struct ForceArgs {
     const double* xp;        // packed {x, y, z} per slot (24 B) of the current positions
     double* xp_next;         // kKKD: packed x(n+1)
     const int* own_slot;
+    const int* own_li;       // owned particle -> its index in the tile's staged halo
     const uint4* nbr;        // blocks of 8 16-bit local indices: nbr[b * n_pad + t]
     const int* ncount;
     const int* obegin;
@@ -1410,6 +1413,12 @@ struct ForceArgs {
     long long step;                       // 1-based index of the step this launch completes
     const DevCtl* ctl;                    // captured steps: skip everything after an abort
     int parts;                            // CTAs per tile (small systems: more CTAs than tiles)
+    // persistent variant (k_force_p): the launch's work units (tiles x parts) are handed out
+    // by a device counter; the last CTA out resets it for the next launch
+    int* pctr;
+    unsigned* pdone;
+    int n_units;
+    int pbuf_bytes;                       // bytes per staging buffer (16-byte multiple)
 };
 
 // Philox4x32-10 (Salmon et al., SC'11): counter-based, so the draws of (gid, step) do not
@@ -1471,6 +1480,14 @@ constexpr int kForceThreads = LJMD_FORCE_THREADS;
 // L2 prefetch of the epilogue's velocities right after the PDL wait (-0.5 us per launch)
 #ifndef LJMD_VPREF2
 #define LJMD_VPREF2 1
+#endif
+// halo copies issued by warp 0 right after the PDL wait, ahead of the per-particle loads; x_i
+// read from the staged halo (own_li, written by the list build)
+#ifndef LJMD_EARLY_TMA
+#define LJMD_EARLY_TMA 1
+#endif
+#if LJMD_EARLY_TMA && LJMD_HALO_GATE
+#error "LJMD_HALO_GATE gates the halo copies, which LJMD_EARLY_TMA issues first"
 #endif
 
 template <int NT>
@@ -1564,10 +1581,25 @@ __device__ __forceinline__ void ring_start(const ForceArgs& a, const FPart& P, u
     }
 }
 
+// Phase timers of the force kernel (measurement build only, LJMD_PHASES=1): per CTA the
+// globaltimer at entry, after the halo staging, the first and last warp's loop end, the
+// last warp's epilogue end, the CTA's end, and the SM id -- tools/phases.py.
+#ifndef LJMD_PHASES
+#define LJMD_PHASES 0
+#endif
+#if LJMD_PHASES
+__device__ unsigned long long ljmd_phase_buf[16384 * 10];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <bool ENERGY, int MODE, bool CHECK>
 __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& P, const char* sPb,
                                                double& epart, double& ke, unsigned long long& dbits,
-                                               unsigned ring) {
+                                               unsigned ring, unsigned long long* ph = nullptr) {
     const int t = P.t;
     const double4 xi = P.xi;
     const uint4* nb = a.nbr + t;
@@ -1629,6 +1661,18 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
             cp_commit();
         }
     }
+#if LJMD_PHASES
+    if (ph) {   // this warp's loop end (lanes reconverge here)
+        __syncwarp(__activemask());
+        if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) {
+            const unsigned long long now = gtimer();
+            atomicMin(&ph[2], now);
+            atomicMax(&ph[3], now);
+        }
+    }
+#else
+    (void)ph;
+#endif
     if ((MODE & 3) == kStore) {
         a.fx[t] = fx; a.fy[t] = fy; a.fz[t] = fz;
         if (ENERGY) {
@@ -1673,6 +1717,29 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
     }
 }
 
+// One TMA bulk copy per halo row of the tile (warp 0; lane r copies row r), completion on
+// the mbarrier with the total byte count (expect_tx by lane 0).
+__device__ __forceinline__ void issue_halo(const ForceArgs& a, const TileGeo& T, int rb, int ro, int rl,
+                                           double* sP, unsigned mb, int lane) {
+        unsigned sz = 0u;
+        unsigned long long src = 0ull;
+        unsigned dst = 0u;
+        if (lane < T.R) {
+            const unsigned d = (unsigned)(rb & 1) * 8u;
+            src = reinterpret_cast<unsigned long long>(a.xp + 3 * (size_t)rb) - d;
+            dst = (unsigned)__cvta_generic_to_shared(sP + 3 * ro) - d;
+            sz = (24u * (unsigned)rl + d + 15u) & ~15u;
+        }
+        unsigned tot = sz;
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(tot) : "memory");
+        __syncwarp();
+        if (sz)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         :: "r"(dst), "l"(src), "r"(sz), "r"(mb) : "memory");
+}
+
 // One CTA per tile.  (1) Each thread issues the global loads of its particle (slot, count,
 // first index block, position); (2) warp 0 copies the tile's halo rows -- x, y, z of every
 // particle any of its particles can list -- into shared memory with one TMA bulk copy per
@@ -1685,6 +1752,18 @@ template <bool ENERGY, int MODE, bool CHECK>
 __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double sh[kForceThreads / 32];
+#if LJMD_PHASES
+    __shared__ unsigned long long ph[8];
+    if (threadIdx.x == 0) {
+        ph[0] = gtimer();
+        ph[2] = ~0ull;
+        ph[3] = 0ull;
+        ph[4] = 0ull;
+    }
+    unsigned long long* php = ph;
+#else
+    unsigned long long* php = nullptr;
+#endif
     // a launch covers a range of tiles, a.parts CTAs per tile (each stages the whole tile
     // halo and takes a share of its particles: small systems get enough CTAs for the chip)
 #if LJMD_FPARTS_OFF
@@ -1709,6 +1788,15 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     if (a.bfirst) tile = ti < a.layer ? ti : (ti < 2 * a.layer ? a.nint + ti : ti - a.layer);
 #endif
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // one bulk copy per halo row (TMA engine), issued by warp 0, completion on an mbarrier
+    __shared__ __align__(8) unsigned long long mbar;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+#if LJMD_EARLY_TMA
+    if (threadIdx.x == 0) {   // at entry, before any load: the fence then waits for nothing
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+#endif
     // captured steps: skip everything after an aborted rebuild, before any table of it is
     // read (the flag is written only by rebuild kernels, never by a force launch)
     if (a.ctl && a.ctl->abort) return;
@@ -1733,12 +1821,11 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     // list ring after the staging buffer (16-byte aligned)
     const unsigned ring = ((unsigned)__cvta_generic_to_shared(smem) + 24u * (unsigned)(total + 1) + 15u) & ~15u;
     const unsigned myring = ring + 16u * threadIdx.x;
-    // one bulk copy per halo row (TMA engine), issued by warp 0, completion on an mbarrier
-    __shared__ __align__(8) unsigned long long mbar;
-    const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
     if (threadIdx.x == 0) {
+#if !LJMD_EARLY_TMA
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#endif
         sP[3 * total] = 1e30;   // sentinel (list padding): far away, contributes exactly 0
         sP[3 * total + 1] = 1e30;
         sP[3 * total + 2] = 1e30;
@@ -1748,12 +1835,36 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
     // one frees, loading the list indices (not written by this kernel) before it waits for
     // the positions and velocities
     asm volatile("griddepcontrol.launch_dependents;");
+#if LJMD_EARLY_TMA
+    // the halo copies first: they need only the row tables, so warp 0 waits for the previous
+    // launch and issues them before any per-particle load (measured: the per-particle load
+    // chain -- tile tables, slot / count / first list block -- held the copies back ~4 us)
+    if (warp == 0) {
+#if LJMD_PHASES
+        if (lane == 0) ph[6] = gtimer() + 0ull * (unsigned long long)(rb + rl + ro);   // row tables in
+#endif
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+#if LJMD_PHASES
+        if (lane == 0) ph[7] = gtimer();   // the previous launch is complete
+#endif
+        issue_halo(a, T, rb, ro, rl, sP, mb, lane);
+#if LJMD_PHASES
+        if (lane == 0) ph[5] = gtimer();   // the copies are issued
+#endif
+    }
+#endif
+    int li = 0;
     if (has) {
         const int t = t0 + threadIdx.x;
         P.t = t;
         P.si = a.own_slot[t];
         P.cnt = a.ncount[t];
+#if LJMD_EARLY_TMA
+        P.nb0 = a.nbr[t];       // unconditional (a count of 0 never reads it)
+        li = a.own_li[t];       // x_i from the staged halo (no dependent global load)
+#else
         P.nb0 = P.cnt > 0 ? a.nbr[t] : make_uint4(0u, 0u, 0u, 0u);
+#endif
         ring_start(a, P, myring);   // the list is not written by the force kernel
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1780,26 +1891,10 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
 #else
     (void)gated;
 #endif
-    if (warp == 0) {   // the copies go out as soon as the positions may be read
-        unsigned sz = 0u;
-        unsigned long long src = 0ull;
-        unsigned dst = 0u;
-        if (lane < T.R) {
-            const unsigned d = (unsigned)(rb & 1) * 8u;
-            src = reinterpret_cast<unsigned long long>(a.xp + 3 * (size_t)rb) - d;
-            dst = (unsigned)__cvta_generic_to_shared(sP + 3 * ro) - d;
-            sz = (24u * (unsigned)rl + d + 15u) & ~15u;
-        }
-        unsigned tot = sz;
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(tot) : "memory");
-        __syncwarp();
-        if (sz)
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         :: "r"(dst), "l"(src), "r"(sz), "r"(mb) : "memory");
-    }
-#if LJMD_PDL
+#if !(LJMD_PDL && LJMD_EARLY_TMA)
+    if (warp == 0) issue_halo(a, T, rb, ro, rl, sP, mb, lane);   // as soon as positions may be read
+#endif
+#if LJMD_PDL && !LJMD_EARLY_TMA
     if (has) P.xi = ld256(a.x + P.si);
 #if LJMD_VPREF2
     if (has && (MODE & 3) != kStore) {   // the epilogue's velocities, into L2 ahead of time
@@ -1808,7 +1903,7 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(a.vz + P.t) : "memory");
     }
 #endif
-#else
+#elif !LJMD_PDL
     if (has) {
         P = fpart_load(a, t0 + threadIdx.x);
         ring_start(a, P, myring);
@@ -1821,16 +1916,29 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
             asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
                          : "=r"(done) : "r"(mb) : "memory");
     }
+#if LJMD_PHASES
+    if (threadIdx.x == 0) ph[1] = gtimer();
+#endif
+#if LJMD_PDL && LJMD_EARLY_TMA
+    if (has) {   // the owned particle's staged position (the same value as x[si])
+        const double* q = sP + 3 * li;
+        P.xi = make_double4(q[0], q[1], q[2], 0.0);
+    }
+#endif
 
     const char* sPb = reinterpret_cast<const char*>(sP);
     double epart = 0.0, ke = 0.0;
     unsigned long long dbits = 0ull;
-    if (has) force_particle<ENERGY, MODE, CHECK>(a, P, sPb, epart, ke, dbits, myring);
+    if (has) force_particle<ENERGY, MODE, CHECK>(a, P, sPb, epart, ke, dbits, myring, php);
     for (int q = threadIdx.x + kForceThreads; q < m; q += kForceThreads) {   // dense tiles only
         const FPart Q = fpart_load(a, t0 + q);
         ring_start(a, Q, myring);
-        force_particle<ENERGY, MODE, CHECK>(a, Q, sPb, epart, ke, dbits, myring);
+        force_particle<ENERGY, MODE, CHECK>(a, Q, sPb, epart, ke, dbits, myring, php);
     }
+#if LJMD_PHASES
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) atomicMax(&ph[4], gtimer());
+#endif
     if (CHECK) block_atomic_max(dbits, &a.fl->maxdisp2);
     if (ENERGY) {
         const double pe = block_sum<kForceThreads>(epart, sh);
@@ -1840,6 +1948,18 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
             a.ke_part[tile * a.parts + part] = k2;
         }
     }
+#if LJMD_PHASES
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < 16384) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        unsigned long long* o = ljmd_phase_buf + 10 * (size_t)blockIdx.x;
+        o[8] = ph[6] - ph[0];
+        o[9] = ph[7] - ph[0];
+        o[0] = ph[0]; o[1] = ph[1]; o[2] = ph[2]; o[3] = ph[3]; o[4] = ph[4]; o[5] = gtimer();
+        o[6] = smid | ((unsigned long long)total << 32); o[7] = (unsigned long long)m | ((ph[5] - ph[0]) << 32);
+    }
+#endif
 #if !LJMD_SEG_OFF
     if (a.bfirst && ti < 2 * a.layer) {   // this CTA's outgoing halo copies are written
         __threadfence();
@@ -1847,6 +1967,219 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         if (threadIdx.x == 0) atomicAdd(a.bdone, 1u);
     }
 #endif
+}
+
+
+// ------------------------------------------------------------------ persistent force kernel
+// One CTA per SM (LJMD_PERSIST): a producer warp and two compute groups of kForceThreads
+// threads over kPBuf staging buffers.  The producer takes work units (tile, part) from a
+// device counter in the launch's order, loads the tile's halo-row table and issues its
+// bulk copies into the next free buffer (mbarrier `full`, the slot's tile / particle range
+// beside it); group g computes slots g, g + 2, ... exactly as k_force does one tile, then
+// releases the buffer (mbarrier `empty`).  The staging of a tile thus overlaps the other
+// group's and its own previous tile's pair loop instead of preceding every CTA's (the phase
+// timers of k_force: 23-30 % of a CTA's life before its halo landed).  Per-tile results are
+// the ones of k_force (same particle -> thread map, same reduction trees).
+#ifndef LJMD_PERSIST
+#define LJMD_PERSIST 0
+#endif
+constexpr int kPGroups = 2;
+constexpr int kPBuf = 3;
+constexpr int kPWarps = kPGroups * (kForceThreads / 32) + 1;   // + the producer warp
+constexpr int kPThreads = 32 * kPWarps;
+
+struct PSlot {
+    int tile, part, t0, m, total, boundary, seq;   // seq: the slot number this fill serves
+};
+
+__device__ __forceinline__ void mbar_wait(unsigned mb, unsigned parity) {
+    unsigned done = 0u;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned mb) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mb) : "memory");
+}
+template <bool ENERGY, int MODE, bool CHECK>
+__global__ void __launch_bounds__(kPThreads, 1) k_force_p(ForceArgs a) {
+    static_assert(kRing == 0, "persistent kernel: register list prefetch only");
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) unsigned long long full[kPBuf], empty[kPBuf];
+    __shared__ PSlot slot[kPBuf];
+    __shared__ unsigned long long smax[kPWarps];
+    __shared__ unsigned sdone[kPBuf];                          // warps done with a slot
+    __shared__ double psum[kPBuf][2][kForceThreads / 32];      // per-warp PE / KE partials
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kPBuf; ++k) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((unsigned)__cvta_generic_to_shared(&full[k])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((unsigned)__cvta_generic_to_shared(&empty[k])) : "memory");
+            sdone[k] = 0u;
+            slot[k].seq = -1;
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (a.ctl && a.ctl->abort) return;   // captured steps after an aborted rebuild
+    asm volatile("griddepcontrol.launch_dependents;");
+    unsigned long long dbits = 0ull;
+    if (warp == kPWarps - 1) {
+        // ---- producer: work units -> staged buffers.  Pipelined: the unit, its tile range
+        // and row table for slot s are fetched while the buffer of slot s - kPBuf is still
+        // in use; once it is released only the slot record and the copies remain.
+        asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous launch's positions
+        int ended = 0;
+        auto fetch = [&](int& tile, int& part, int& t0, int& m, int& rb, int& ro, int& rl, int& total, int& bnd,
+                         TileGeo& T) -> bool {
+            int ti = 0;
+            if (lane == 0) ti = atomicAdd(a.pctr, 1);
+            ti = __shfl_sync(0xffffffffu, ti, 0);
+            if (ti >= a.n_units) return false;
+            part = ti % a.parts;
+            ti /= a.parts;
+            tile = a.tile_base + ti + (ti >= a.seg0 ? a.gap : 0);
+            if (a.bfirst) tile = ti < a.layer ? ti : (ti < 2 * a.layer ? a.nint + ti : ti - a.layer);
+            bnd = (a.bfirst && ti < 2 * a.layer) ? 1 : 0;
+            T = tile_geo(a.g, tile);
+            const int tt0 = a.obegin[a.tile_oc0[tile]];
+            const int mt = a.obegin[a.tile_oc0[tile + 1]] - tt0;
+            const int per = ((mt + a.parts - 1) / a.parts + 15) & ~15;
+            const int qb = min(part * per, mt);
+            t0 = tt0 + qb;
+            m = min(qb + per, mt) - qb;
+            rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
+            ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
+            rl = lane < T.R ? a.tr.len[tile * kRowsMax + lane] : 0;
+            total = __shfl_sync(0xffffffffu, ro, T.R);
+            return true;
+        };
+        int tile = 0, part = 0, t0 = 0, m = 0, rb = 0, ro = 0, rl = 0, total = 0, bnd = 0;
+        TileGeo T;
+        bool have = fetch(tile, part, t0, m, rb, ro, rl, total, bnd, T);
+        for (int s = 0; ended < kPGroups; ++s) {
+            const int b = s % kPBuf;
+            if (s >= kPBuf) mbar_wait((unsigned)__cvta_generic_to_shared(&empty[b]), (unsigned)((s / kPBuf - 1) & 1));
+            const unsigned fb = (unsigned)__cvta_generic_to_shared(&full[b]);
+            if (!have) {   // no work left: this slot tells its group to stop
+                if (lane == 0) {
+                    slot[b].tile = -1;
+                    *reinterpret_cast<volatile int*>(&slot[b].seq) = s;
+                    mbar_arrive(fb);
+                }
+                ++ended;
+                continue;
+            }
+            double* sP = reinterpret_cast<double*>(smem + (size_t)b * a.pbuf_bytes);
+            if (lane == 0) {
+                slot[b] = PSlot{tile, part, t0, m, total, bnd, s};
+                sP[3 * total] = 1e30;   // sentinel (list padding)
+                sP[3 * total + 1] = 1e30;
+                sP[3 * total + 2] = 1e30;
+            }
+            issue_halo(a, T, rb, ro, rl, sP, fb, lane);   // lane 0's expect_tx releases the slot
+            have = fetch(tile, part, t0, m, rb, ro, rl, total, bnd, T);   // the next slot's unit
+        }
+    } else {
+        // ---- compute group g: slots g, g + kPGroups, ...
+        const int g = warp / (kForceThreads / 32);
+        const int gtid = threadIdx.x - g * kForceThreads;
+        const int gwarp = gtid >> 5;
+        for (int s = g;; s += kPGroups) {
+            const int b = s % kPBuf;
+            // warps of a group run independently, so a fast one may reach a use of buffer b
+            // two fills ahead of the one in flight, whose parity matches an older completed
+            // phase: it confirms the fill's slot number and waits again if it was early
+            for (;;) {
+                mbar_wait((unsigned)__cvta_generic_to_shared(&full[b]), (unsigned)((s / kPBuf) & 1));
+                if (*reinterpret_cast<volatile int*>(&slot[b].seq) == s) break;
+                while (*reinterpret_cast<volatile int*>(&slot[b].seq) != s) __nanosleep(64);
+            }
+            const PSlot S = slot[b];
+            if (S.tile < 0) break;
+            const char* sPb = reinterpret_cast<const char*>(smem + (size_t)b * a.pbuf_bytes);
+            double epart = 0.0, ke = 0.0;
+            if (gtid < S.m) {
+                FPart P;
+                P.t = S.t0 + gtid;
+                P.si = a.own_slot[P.t];
+                P.cnt = a.ncount[P.t];
+                P.nb0 = a.nbr[P.t];
+                const double* q = reinterpret_cast<const double*>(sPb) + 3 * a.own_li[P.t];
+                P.xi = make_double4(q[0], q[1], q[2], 0.0);
+                ring_start(a, P, 0u);
+                force_particle<ENERGY, MODE, CHECK>(a, P, sPb, epart, ke, dbits, 0u);
+            }
+            for (int q = gtid + kForceThreads; q < S.m; q += kForceThreads) {   // dense tiles only
+                const FPart Q = fpart_load(a, S.t0 + q);
+                ring_start(a, Q, 0u);
+                force_particle<ENERGY, MODE, CHECK>(a, Q, sPb, epart, ke, dbits, 0u);
+            }
+            // no group barrier: each warp moves on to its next slot; the last warp of the
+            // group done with this slot reduces the energies, counts a boundary tile and
+            // releases the buffer
+            if (ENERGY) {
+                double e1 = epart, k1 = ke;
+                for (int o = 16; o > 0; o >>= 1) {
+                    e1 += __shfl_down_sync(0xffffffffu, e1, o);
+                    k1 += __shfl_down_sync(0xffffffffu, k1, o);
+                }
+                if (lane == 0) {
+                    psum[b][0][gwarp] = e1;
+                    psum[b][1][gwarp] = k1;
+                }
+            }
+            unsigned last = 0u;
+            if (lane == 0) {
+                if (S.boundary) __threadfence();   // this warp's outgoing halo copies
+                __threadfence_block();
+                last = atomicAdd(&sdone[b], 1u) == (unsigned)(kForceThreads / 32 - 1);
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                __threadfence_block();
+                if (ENERGY) {   // block_sum's second stage over the group's warp partials
+                    double r = lane < kForceThreads / 32 ? psum[b][0][lane] : 0.0;
+                    double r2 = lane < kForceThreads / 32 ? psum[b][1][lane] : 0.0;
+                    for (int o = 16; o > 0; o >>= 1) {
+                        r += __shfl_down_sync(0xffffffffu, r, o);
+                        r2 += __shfl_down_sync(0xffffffffu, r2, o);
+                    }
+                    if (lane == 0) {
+                        a.pe_part[S.tile * a.parts + S.part] = r;
+                        a.ke_part[S.tile * a.parts + S.part] = r2;
+                    }
+                }
+                if (lane == 0) {
+                    if (S.boundary) atomicAdd(a.bdone, 1u);
+                    sdone[b] = 0u;
+                    mbar_arrive((unsigned)__cvta_generic_to_shared(&empty[b]));
+                }
+            }
+        }
+    }
+    if (CHECK) {   // the CTA's maximum displacement, one atomic per CTA
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_down_sync(0xffffffffu, dbits, o);
+            dbits = ob > dbits ? ob : dbits;
+        }
+        if (lane == 0) smax[warp] = dbits;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (CHECK) {
+            unsigned long long v = 0ull;
+            for (int w = 0; w < kPWarps; ++w) v = smax[w] > v ? smax[w] : v;
+            if (v) atomicMax(&a.fl->maxdisp2, v);
+        }
+        // the last CTA out resets the work counter for the next launch (which touches it only
+        // after its griddepcontrol.wait, i.e. after this grid has completed)
+        __threadfence();
+        if (atomicAdd(a.pdone, 1u) == gridDim.x - 1) {
+            *a.pctr = 0;
+            *a.pdone = 0u;
+        }
+    }
 }
 
 // opening half of a step() call: v += h F ; x += dt v  (in place, owned slots)
