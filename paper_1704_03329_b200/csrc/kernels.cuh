@@ -1413,12 +1413,6 @@ struct ForceArgs {
     long long step;                       // 1-based index of the step this launch completes
     const DevCtl* ctl;                    // captured steps: skip everything after an abort
     int parts;                            // CTAs per tile (small systems: more CTAs than tiles)
-    // persistent variant (k_force_p): the launch's work units (tiles x parts) are handed out
-    // by a device counter; the last CTA out resets it for the next launch
-    int* pctr;
-    unsigned* pdone;
-    int n_units;
-    int pbuf_bytes;                       // bytes per staging buffer (16-byte multiple)
 };
 
 // Philox4x32-10 (Salmon et al., SC'11): counter-based, so the draws of (gid, step) do not
@@ -1969,218 +1963,6 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
 #endif
 }
 
-
-// ------------------------------------------------------------------ persistent force kernel
-// One CTA per SM (LJMD_PERSIST): a producer warp and two compute groups of kForceThreads
-// threads over kPBuf staging buffers.  The producer takes work units (tile, part) from a
-// device counter in the launch's order, loads the tile's halo-row table and issues its
-// bulk copies into the next free buffer (mbarrier `full`, the slot's tile / particle range
-// beside it); group g computes slots g, g + 2, ... exactly as k_force does one tile, then
-// releases the buffer (mbarrier `empty`).  The staging of a tile thus overlaps the other
-// group's and its own previous tile's pair loop instead of preceding every CTA's (the phase
-// timers of k_force: 23-30 % of a CTA's life before its halo landed).  Per-tile results are
-// the ones of k_force (same particle -> thread map, same reduction trees).
-#ifndef LJMD_PERSIST
-#define LJMD_PERSIST 0
-#endif
-constexpr int kPGroups = 2;
-constexpr int kPBuf = 3;
-constexpr int kPWarps = kPGroups * (kForceThreads / 32) + 1;   // + the producer warp
-constexpr int kPThreads = 32 * kPWarps;
-
-struct PSlot {
-    int tile, part, t0, m, total, boundary, seq;   // seq: the slot number this fill serves
-};
-
-__device__ __forceinline__ void mbar_wait(unsigned mb, unsigned parity) {
-    unsigned done = 0u;
-    while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(mb), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned mb) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(mb) : "memory");
-}
-template <bool ENERGY, int MODE, bool CHECK>
-__global__ void __launch_bounds__(kPThreads, 1) k_force_p(ForceArgs a) {
-    static_assert(kRing == 0, "persistent kernel: register list prefetch only");
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(8) unsigned long long full[kPBuf], empty[kPBuf];
-    __shared__ PSlot slot[kPBuf];
-    __shared__ unsigned long long smax[kPWarps];
-    __shared__ unsigned sdone[kPBuf];                          // warps done with a slot
-    __shared__ double psum[kPBuf][2][kForceThreads / 32];      // per-warp PE / KE partials
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < kPBuf; ++k) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((unsigned)__cvta_generic_to_shared(&full[k])) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((unsigned)__cvta_generic_to_shared(&empty[k])) : "memory");
-            sdone[k] = 0u;
-            slot[k].seq = -1;
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (a.ctl && a.ctl->abort) return;   // captured steps after an aborted rebuild
-    asm volatile("griddepcontrol.launch_dependents;");
-    unsigned long long dbits = 0ull;
-    if (warp == kPWarps - 1) {
-        // ---- producer: work units -> staged buffers.  Pipelined: the unit, its tile range
-        // and row table for slot s are fetched while the buffer of slot s - kPBuf is still
-        // in use; once it is released only the slot record and the copies remain.
-        asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous launch's positions
-        int ended = 0;
-        auto fetch = [&](int& tile, int& part, int& t0, int& m, int& rb, int& ro, int& rl, int& total, int& bnd,
-                         TileGeo& T) -> bool {
-            int ti = 0;
-            if (lane == 0) ti = atomicAdd(a.pctr, 1);
-            ti = __shfl_sync(0xffffffffu, ti, 0);
-            if (ti >= a.n_units) return false;
-            part = ti % a.parts;
-            ti /= a.parts;
-            tile = a.tile_base + ti + (ti >= a.seg0 ? a.gap : 0);
-            if (a.bfirst) tile = ti < a.layer ? ti : (ti < 2 * a.layer ? a.nint + ti : ti - a.layer);
-            bnd = (a.bfirst && ti < 2 * a.layer) ? 1 : 0;
-            T = tile_geo(a.g, tile);
-            const int tt0 = a.obegin[a.tile_oc0[tile]];
-            const int mt = a.obegin[a.tile_oc0[tile + 1]] - tt0;
-            const int per = ((mt + a.parts - 1) / a.parts + 15) & ~15;
-            const int qb = min(part * per, mt);
-            t0 = tt0 + qb;
-            m = min(qb + per, mt) - qb;
-            rb = lane < T.R ? a.tr.begin[tile * kRowsMax + lane] : 0;
-            ro = lane <= T.R ? a.tr.off[tile * (kRowsMax + 1) + lane] : 0;
-            rl = lane < T.R ? a.tr.len[tile * kRowsMax + lane] : 0;
-            total = __shfl_sync(0xffffffffu, ro, T.R);
-            return true;
-        };
-        int tile = 0, part = 0, t0 = 0, m = 0, rb = 0, ro = 0, rl = 0, total = 0, bnd = 0;
-        TileGeo T;
-        bool have = fetch(tile, part, t0, m, rb, ro, rl, total, bnd, T);
-        for (int s = 0; ended < kPGroups; ++s) {
-            const int b = s % kPBuf;
-            if (s >= kPBuf) mbar_wait((unsigned)__cvta_generic_to_shared(&empty[b]), (unsigned)((s / kPBuf - 1) & 1));
-            const unsigned fb = (unsigned)__cvta_generic_to_shared(&full[b]);
-            if (!have) {   // no work left: this slot tells its group to stop
-                if (lane == 0) {
-                    slot[b].tile = -1;
-                    *reinterpret_cast<volatile int*>(&slot[b].seq) = s;
-                    mbar_arrive(fb);
-                }
-                ++ended;
-                continue;
-            }
-            double* sP = reinterpret_cast<double*>(smem + (size_t)b * a.pbuf_bytes);
-            if (lane == 0) {
-                slot[b] = PSlot{tile, part, t0, m, total, bnd, s};
-                sP[3 * total] = 1e30;   // sentinel (list padding)
-                sP[3 * total + 1] = 1e30;
-                sP[3 * total + 2] = 1e30;
-            }
-            issue_halo(a, T, rb, ro, rl, sP, fb, lane);   // lane 0's expect_tx releases the slot
-            have = fetch(tile, part, t0, m, rb, ro, rl, total, bnd, T);   // the next slot's unit
-        }
-    } else {
-        // ---- compute group g: slots g, g + kPGroups, ...
-        const int g = warp / (kForceThreads / 32);
-        const int gtid = threadIdx.x - g * kForceThreads;
-        const int gwarp = gtid >> 5;
-        for (int s = g;; s += kPGroups) {
-            const int b = s % kPBuf;
-            // warps of a group run independently, so a fast one may reach a use of buffer b
-            // two fills ahead of the one in flight, whose parity matches an older completed
-            // phase: it confirms the fill's slot number and waits again if it was early
-            for (;;) {
-                mbar_wait((unsigned)__cvta_generic_to_shared(&full[b]), (unsigned)((s / kPBuf) & 1));
-                if (*reinterpret_cast<volatile int*>(&slot[b].seq) == s) break;
-                while (*reinterpret_cast<volatile int*>(&slot[b].seq) != s) __nanosleep(64);
-            }
-            const PSlot S = slot[b];
-            if (S.tile < 0) break;
-            const char* sPb = reinterpret_cast<const char*>(smem + (size_t)b * a.pbuf_bytes);
-            double epart = 0.0, ke = 0.0;
-            if (gtid < S.m) {
-                FPart P;
-                P.t = S.t0 + gtid;
-                P.si = a.own_slot[P.t];
-                P.cnt = a.ncount[P.t];
-                P.nb0 = a.nbr[P.t];
-                const double* q = reinterpret_cast<const double*>(sPb) + 3 * a.own_li[P.t];
-                P.xi = make_double4(q[0], q[1], q[2], 0.0);
-                ring_start(a, P, 0u);
-                force_particle<ENERGY, MODE, CHECK>(a, P, sPb, epart, ke, dbits, 0u);
-            }
-            for (int q = gtid + kForceThreads; q < S.m; q += kForceThreads) {   // dense tiles only
-                const FPart Q = fpart_load(a, S.t0 + q);
-                ring_start(a, Q, 0u);
-                force_particle<ENERGY, MODE, CHECK>(a, Q, sPb, epart, ke, dbits, 0u);
-            }
-            // no group barrier: each warp moves on to its next slot; the last warp of the
-            // group done with this slot reduces the energies, counts a boundary tile and
-            // releases the buffer
-            if (ENERGY) {
-                double e1 = epart, k1 = ke;
-                for (int o = 16; o > 0; o >>= 1) {
-                    e1 += __shfl_down_sync(0xffffffffu, e1, o);
-                    k1 += __shfl_down_sync(0xffffffffu, k1, o);
-                }
-                if (lane == 0) {
-                    psum[b][0][gwarp] = e1;
-                    psum[b][1][gwarp] = k1;
-                }
-            }
-            unsigned last = 0u;
-            if (lane == 0) {
-                if (S.boundary) __threadfence();   // this warp's outgoing halo copies
-                __threadfence_block();
-                last = atomicAdd(&sdone[b], 1u) == (unsigned)(kForceThreads / 32 - 1);
-            }
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-                __threadfence_block();
-                if (ENERGY) {   // block_sum's second stage over the group's warp partials
-                    double r = lane < kForceThreads / 32 ? psum[b][0][lane] : 0.0;
-                    double r2 = lane < kForceThreads / 32 ? psum[b][1][lane] : 0.0;
-                    for (int o = 16; o > 0; o >>= 1) {
-                        r += __shfl_down_sync(0xffffffffu, r, o);
-                        r2 += __shfl_down_sync(0xffffffffu, r2, o);
-                    }
-                    if (lane == 0) {
-                        a.pe_part[S.tile * a.parts + S.part] = r;
-                        a.ke_part[S.tile * a.parts + S.part] = r2;
-                    }
-                }
-                if (lane == 0) {
-                    if (S.boundary) atomicAdd(a.bdone, 1u);
-                    sdone[b] = 0u;
-                    mbar_arrive((unsigned)__cvta_generic_to_shared(&empty[b]));
-                }
-            }
-        }
-    }
-    if (CHECK) {   // the CTA's maximum displacement, one atomic per CTA
-        for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long ob = __shfl_down_sync(0xffffffffu, dbits, o);
-            dbits = ob > dbits ? ob : dbits;
-        }
-        if (lane == 0) smax[warp] = dbits;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (CHECK) {
-            unsigned long long v = 0ull;
-            for (int w = 0; w < kPWarps; ++w) v = smax[w] > v ? smax[w] : v;
-            if (v) atomicMax(&a.fl->maxdisp2, v);
-        }
-        // the last CTA out resets the work counter for the next launch (which touches it only
-        // after its griddepcontrol.wait, i.e. after this grid has completed)
-        __threadfence();
-        if (atomicAdd(a.pdone, 1u) == gridDim.x - 1) {
-            *a.pctr = 0;
-            *a.pdone = 0u;
-        }
-    }
-}
 
 // opening half of a step() call: v += h F ; x += dt v  (in place, owned slots)
 // The pre-drift position is also written to the other buffer's owned slot (xprev), so that

@@ -138,10 +138,6 @@ struct ljmd_ctx {
     double* ke_part = nullptr;
     int n_fblocks = 0;
     int fparts = 1;                   // force CTAs per tile
-    // persistent force kernel (k_force_p): one CTA per SM, work units from a device counter
-    int n_sm = 0;
-    int* pctr = nullptr;
-    unsigned* pdone = nullptr;
     double* hist = nullptr;   // [hist_cap][2]
     double* h_histm = nullptr;   // mapped page-locked readback of hist
     int64_t h_histm_cap = 0;
@@ -675,29 +671,12 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.halo_seq = 0;
     a.bfirst = 0;
     a.bdone = nullptr;
-    a.pctr = nullptr;
-    a.pdone = nullptr;
-    a.n_units = 0;
-    a.pbuf_bytes = 0;
     a.nint = 0;
     a.layer = 0;
     return a;
 }
 
 constexpr size_t kStageBytes = 24;   // packed {x, y, z} per staged particle
-constexpr size_t kMaxPSmem = 225 * 1024;   // dynamic smem of k_force_p (kPBuf staging buffers)
-
-// bytes of one persistent-kernel staging buffer (the halo + sentinel, 16-byte multiple)
-inline size_t pbuf_bytes(const ljmd_ctx* c) { return (kStageBytes * (size_t)(c->stage_cap + 1) + 15) / 16 * 16; }
-// the persistent kernel serves launches of large systems (one part per tile) whose staging
-// buffers fit three times in shared memory
-inline bool persist_ok(const ljmd_ctx* c) {
-    static const bool env = [] {
-        const char* e = getenv("LJMD_PERSIST");
-        return !(e && e[0] == '0');
-    }();
-    return LJMD_PERSIST && env && c->pctr && c->fparts == 1 && !c->newton3 && kPBuf * pbuf_bytes(c) <= kMaxPSmem;
-}
 // k_force dynamic shared memory: the staged halo (+ sentinel), then the list ring
 inline size_t force_smem(const ljmd_ctx* c) {
     return (kStageBytes * (size_t)(c->stage_cap + 1) + 15) / 16 * 16 + 16 * (size_t)kRing * kForceThreads;
@@ -706,25 +685,6 @@ inline size_t force_smem(const ljmd_ctx* c) {
 template <bool E, int M, bool C>
 void force_launch(ljmd_ctx* c, const ForceArgs& a, int n_launch, cudaStream_t st = nullptr) {
     if (!st) st = c->stream;
-    if (persist_ok(c) && !a.halo_flag) {
-        ForceArgs p = a;
-        p.pctr = c->pctr;
-        p.pdone = c->pdone;
-        p.n_units = n_launch * c->fparts;
-        p.pbuf_bytes = (int)pbuf_bytes(c);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)std::max(1, std::min(c->n_sm, p.n_units)));
-        cfg.blockDim = dim3(kPThreads);
-        cfg.dynamicSmemBytes = (size_t)kPBuf * pbuf_bytes(c);
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = c->pdl_ok ? 1 : 0;
-        cudaLaunchKernelEx(&cfg, k_force_p<E, M, C>, p);
-        return;
-    }
 #if LJMD_PDL
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(n_launch * c->fparts));
@@ -746,11 +706,8 @@ void force_launch(ljmd_ctx* c, const ForceArgs& a, int n_launch, cudaStream_t st
 
 template <bool E, int M, bool C>
 cudaError_t force_attr() {
-    cudaError_t e = cudaFuncSetAttribute(k_force<E, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kMaxStageSmem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_force_p<E, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxPSmem);
-    return e;
+    return cudaFuncSetAttribute(k_force<E, M, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kMaxStageSmem);
 }
 
 ljmd_status set_force_attrs(ljmd_ctx* c) {
@@ -1894,13 +1851,6 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         }
     }
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
-    if (cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess ||
-        cudaMalloc(&c->pctr, sizeof(int)) != cudaSuccess || cudaMemset(c->pctr, 0, sizeof(int)) != cudaSuccess ||
-        cudaMalloc(&c->pdone, sizeof(unsigned)) != cudaSuccess ||
-        cudaMemset(c->pdone, 0, sizeof(unsigned)) != cudaSuccess) {
-        set_err(c, LJMD_E_CUDA, "persistent-kernel counters");
-        return fail(LJMD_E_CUDA);
-    }
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
         cudaMalloc(&c->d_ctl, sizeof(DevCtl)) != cudaSuccess ||
         cudaHostAlloc(&c->h_ctl, sizeof(DevCtl), cudaHostAllocMapped) != cudaSuccess ||
@@ -2567,8 +2517,6 @@ void ljmd_destroy(ljmd_ctx* c) {
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     if (c->bdone) cudaFree(c->bdone);
-    if (c->pctr) cudaFree(c->pctr);
-    if (c->pdone) cudaFree(c->pdone);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
