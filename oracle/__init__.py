@@ -161,13 +161,14 @@ def cell_dims(box, rn):
     return nc
 
 
-def neighbours(pos, box, rn, method="brute"):
-    """O3 (brute) / O4 (cells): CSR (offsets[n+1], nbr[...]) with each NB(i) ascending."""
+def neighbours(pos, box, rn, method="brute", omp=False):
+    """O3 (brute) / O4 (cells): CSR (offsets[n+1], nbr[...]) with each NB(i) ascending.
+    omp: the OpenMP build of the same source (rows in parallel, identical results)."""
     p = _f64(pos, (-1, 3))
     b = _f64(box)
     n = p.shape[0]
     off = np.zeros(n + 1, dtype=np.int64)
-    f = _load().orc_neigh_brute if method == "brute" else _load().orc_neigh_cells
+    f = _load(omp).orc_neigh_brute if method == "brute" else _load(omp).orc_neigh_cells
     tot = f(n, _dp(p), _dp(b), float(rn), _ip(off), None)
     if tot < 0:
         raise ValueError("box too small: fewer than 3 cells of width >= rbar_c")
@@ -185,8 +186,9 @@ class Forces:
     pe: float
 
 
-def forces(pos, box, lj: LJ = LJ(), nlist=None):
-    """O5: per-particle forces, energies e_i = 1/2 sum_j V, tolerance scales S_i, A_i."""
+def forces(pos, box, lj: LJ = LJ(), nlist=None, omp=False):
+    """O5: per-particle forces, energies e_i = 1/2 sum_j V, tolerance scales S_i, A_i.
+    omp: the OpenMP build of the same source (rows in parallel, identical results)."""
     p = _f64(pos, (-1, 3))
     b = _f64(box)
     n = p.shape[0]
@@ -197,7 +199,7 @@ def forces(pos, box, lj: LJ = LJ(), nlist=None):
     c = lj.c()
     off, nbr = (None, None) if nlist is None else (np.ascontiguousarray(nlist[0], dtype=np.int64),
                                                    np.ascontiguousarray(nlist[1], dtype=np.int64))
-    pe = _load().orc_forces(n, _dp(p), _dp(b), ctypes.byref(c), _ip(off), _ip(nbr),
+    pe = _load(omp).orc_forces(n, _dp(p), _dp(b), ctypes.byref(c), _ip(off), _ip(nbr),
                             _dp(F), _dp(e), _dp(S), _dp(A))
     return Forces(F, e, S, A, pe)
 

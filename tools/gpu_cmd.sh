@@ -1,3 +1,4 @@
 OUT=gpurun_out
-timeout 300 python -m pytest tests/test_gpu_parity.py -x -q > $OUT/gt31.log 2>&1; echo "rc=$?" >> $OUT/gt31.log
-timeout 600 bash tools/abenv.sh LJMD_PERSIST 0 1 0 1 > $OUT/ab31.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/gt33.log 2>&1; echo "rc=$?" >> $OUT/gt33.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke33.log 2>&1
+timeout 1200 bash tools/bench_all.sh > $OUT/bench_all33.log 2>&1

@@ -15,6 +15,14 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-fi
 ncu --set full --import-source on --clock-control none \
     -k regex:"k_force|k_build_nlist|k_list_rr|k_wrap_bin|k_cell_sort|k_kick_drift|k_maxdisp|k_ghost_refresh|k_scatter|k_tile_rows|k_img_build|k_finalize" \
     -s 12 -c 24 -o $OUT/r2_full python tools/build_drive.py 1 > $OUT/r2_full.log 2>&1
-# 3. sanitizers over both rebuild policies, graphs and eager paths, the analyses, a dilute box
+python profiles/extract_r2.py $OUT/r2_full.ncu-rep $OUT/r2_force_kernels_summary.json --traffic $OUT/force_traffic.json \
+    > $OUT/r2_full_extract.log 2>&1 && rm -f $OUT/r2_full.ncu-rep   # gpurun copies back <= 64 MiB
+# 3. the binning / list / integration kernels of one rebuild cycle
+ncu --set full --import-source on --clock-control none \
+    -k regex:"k_build_nlist|k_list_rr|k_wrap_bin|k_cell_sort|k_kick_drift|k_maxdisp|k_ghost_refresh|k_scatter|k_tile_rows|k_img_build" \
+    -c 14 -o $OUT/r2_aux python tools/build_drive.py 1 > $OUT/r2_aux.log 2>&1
+python profiles/extract_r2.py $OUT/r2_aux.ncu-rep $OUT/r2_aux_kernels_summary.json > $OUT/r2_aux_extract.log 2>&1 \
+    && rm -f $OUT/r2_aux.ncu-rep
+# 4. sanitizers over both rebuild policies, graphs and eager paths, the analyses, a dilute box
 compute-sanitizer --tool memcheck --leak-check full python tools/sanitize_drive.py > $OUT/r2_memcheck.log 2>&1
-compute-sanitizer --tool racecheck python tools/sanitize_drive.py > $OUT/r2_racecheck.log 2>&1
+compute-sanitizer --tool racecheck python tools/sanitize_drive.py 2>&1 | tail -c 20000 > $OUT/r2_racecheck.log
