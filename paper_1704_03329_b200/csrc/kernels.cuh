@@ -1203,27 +1203,33 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
     int novf = 0;
     bool overflow = false;
     unsigned short pad = 0;
+    // filing, branch-free per entry: a bucket slot while the residue has room, else the
+    // next overflow slot (clamped; a full overflow area makes the particle keep build order)
+    auto file = [&](unsigned short l) {
+        const int r = l & 15;
+        const int c = C[r];
+        const bool ok = c < kRrCap;
+        unsigned short* dst = ok ? bkt + r * kRrCap + c : ovf + min(novf, kRrOvf - 1);
+        *dst = l;
+        C[r] = (unsigned char)(c + (ok ? 1 : 0));
+        overflow |= !ok && novf >= kRrOvf;
+        novf += ok ? 0 : 1;
+    };
+    const int nfull = n >> 3;
     uint4 vn = nb > 0 ? in[t] : make_uint4(0u, 0u, 0u, 0u);
     for (int b = 0; b < nb; ++b) {
         const uint4 v = vn;
         if (b + 1 < nb) vn = in[(size_t)(b + 1) * stride + t];   // next block in flight
         const unsigned w[4] = {v.x, v.y, v.z, v.w};
+        if (b < nfull) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const unsigned short l = (unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu));
-            if (b * 8 + e < n) {
-                const int r = l & 15;
-                const int c = C[r];
-                if (c < kRrCap) {
-                    bkt[r * kRrCap + c] = l;
-                    C[r] = (unsigned char)(c + 1);
-                } else if (novf < kRrOvf) {
-                    ovf[novf++] = l;
-                } else {
-                    overflow = true;
-                }
-            } else {
-                pad = l;   // the tile's sentinel
+            for (int e = 0; e < 8; ++e)
+                file((unsigned short)((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffffu)));
+        } else {   // the last, padded block
+            for (int e = 0; e < 8; ++e) {
+                const unsigned short l = (unsigned short)((w[e >> 1] >> (16 * (e & 1))) & 0xffffu);
+                if (b * 8 + e < n) file(l);
+                else pad = l;   // the tile's sentinel
             }
         }
     }
@@ -1238,20 +1244,8 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
     const int nin = n - novf;
     unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;   // 8 pending entries, shifted in from the top
     uint4* o = out + t;
-    unsigned av2 = avail | (avail << 16);   // bit r and r + 16: a rotation is one shift
-    int tgt = off;                          // (off + k) mod 16
-    for (int k = 0; k < nb * 8; ++k) {
-        unsigned l = pad;
-        if (k < nin) {
-            const int rr = (tgt + __ffs(av2 >> tgt) - 1) & 15;
-            tgt = (tgt + 1) & 15;
-            const int u = U[rr];
-            l = bkt[rr * kRrCap + u];
-            U[rr] = (unsigned char)(u + 1);
-            if (u + 1 == (int)C[rr]) av2 &= ~(0x10001u << rr);
-        } else if (k < n) {
-            l = ovf[k - nin];
-        }
+    int k = 0;
+    auto emit = [&](unsigned l) {
         w0 = __funnelshift_r(w0, w1, 16);
         w1 = __funnelshift_r(w1, w2, 16);
         w2 = __funnelshift_r(w2, w3, 16);
@@ -1260,7 +1254,21 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
             *o = make_uint4(w0, w1, w2, w3);
             o += stride;
         }
+        ++k;
+    };
+    unsigned av2 = avail | (avail << 16);   // bit r and r + 16: a rotation is one shift
+    int tgt = off;                          // (off + k) mod 16
+    for (int q = 0; q < nin; ++q) {         // the greedy walk over the residues
+        const int rr = (tgt + __ffs(av2 >> tgt) - 1) & 15;
+        tgt = (tgt + 1) & 15;
+        const int u = U[rr];
+        const unsigned l = bkt[rr * kRrCap + u];
+        U[rr] = (unsigned char)(u + 1);
+        av2 &= u + 1 == (int)C[rr] ? ~(0x10001u << rr) : 0xffffffffu;
+        emit(l);
     }
+    for (int q = 0; q < novf; ++q) emit(ovf[q]);   // overflow entries, build order
+    while (k < nb * 8) emit(pad);                  // the last block's sentinel padding
 }
 #else
 constexpr int kRrStrideW = (16 * kRrCap + kRrOvf) / 2 + 1;   // words per thread (odd: no bank aliasing)
@@ -1790,6 +1798,7 @@ __global__ void __launch_bounds__(kForceThreads, LJMD_FORCE_MINB) k_force(ForceA
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (warp == 0) __syncwarp();   // the lanes that issue the copies see the initialised barrier
 #endif
     // captured steps: skip everything after an aborted rebuild, before any table of it is
     // read (the flag is written only by rebuild kernels, never by a force launch)
