@@ -375,3 +375,23 @@ def test_full_size_exhaustive_c2(eng, orc):
     o2, n2 = orc.neighbours(xw, box, RN, "cells", omp=True)
     assert np.array_equal(np.asarray(off, dtype=np.int64), o2)
     assert np.array_equal(_sorted_rows(off, nbr), _sorted_rows(o2, n2))
+
+
+def test_trajectory_energies_100_steps_c2(eng, orc):
+    """The 100-step trajectory bar at the bench size: C2 (N = 1,048,576, fixed Ns = 20, five
+    device rebuilds), sampled PE/KE/E within 1e-8 relative of the oracle's run with the same
+    schedule (the OpenMP build of the same source: identical results, minutes -> seconds)."""
+    c = li.CONFIGS["C2"]
+    pos, vel, box = c.build()
+    with eng.LJMD(pos, vel, box) as ctx:
+        ctx.step(100)
+        pe, ke = ctx.energy_history()
+        rs = ctx.rebuild_steps()
+    orc.threads(0)
+    r = orc.run(pos, vel, box, 100, lj=lj_of(0.25), mode="list", omp=True)
+    assert rs.tolist() == r.rebuild_steps.tolist() == [20, 40, 60, 80, 100]
+    assert len(pe) == len(r.pe) == 11
+    scale = np.abs(r.pe) + np.abs(r.ke)
+    assert np.all(np.abs(pe - r.pe) <= 1e-8 * scale)
+    assert np.all(np.abs(ke - r.ke) <= 1e-8 * scale)
+    assert np.all(np.abs((pe + ke) - (r.pe + r.ke)) <= 1e-8 * np.abs(r.pe + r.ke))
