@@ -919,6 +919,12 @@ struct BuildSmem {
     unsigned short sub[kRowsMax][kTX + 2][kSub + 1];
 };
 
+// SMALL (small systems, a.parts > 1 CTAs per tile, each with a few dozen particles): a WARP per
+// particle instead of a thread -- lanes test 32 consecutive candidates of a window at a time,
+// a ballot compacts the accepted ones into the list -- so a CTA's latency chain is a few
+// chunks per particle instead of one thread's ~270 candidates.  Same windows, same (row,
+// slot) order, same decisions: the list is identical to the thread-per-particle build's.
+template <bool SMALL>
 __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(NlistArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ BuildSmem S;
@@ -984,7 +990,77 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
     int kmax = 0;
     const int per = (m + a.parts - 1) / a.parts;
     const int q_end = min(m, (part + 1) * per);
-    for (int q = part * per + (int)threadIdx.x; q < q_end; q += kBuildThreads) {
+    if (SMALL) {
+        unsigned short* nbr16 = reinterpret_cast<unsigned short*>(a.nbr8);
+        for (int q = part * per + warp; q < q_end; q += kBuildThreads / 32) {   // warp-uniform
+            int ci = 0;
+            while (ci + 1 < ncell && S.cell_t0[ci + 1] <= q) ++ci;
+            const int lx = ci % T.tx, ly = (ci / T.tx) % T.ty, lz = ci / (T.tx * T.ty);
+            const int R0 = (lz + 1) * (T.ty + 2) + (ly + 1);
+            const int li = S.seg[R0][lx + 1] + (q - S.cell_t0[ci]);
+            const int t = t0 + q;
+            if (lane == 0) a.own_li[t] = li;
+            const float4 fi = sF[li];
+            const int cy = T.y0 + ly, cz = T.z0 + lz;
+            const float ylo = a.ylo_f[cy], yhi = a.ylo_f[cy + 1];
+            const float zlo = a.zlo_f[cz], zhi = a.zlo_f[cz + 1];
+            int k = 0;
+            for (int rz = 0; rz < 3; ++rz) {
+                const float ddz = rz == 0 ? fi.z - zlo : (rz == 2 ? zhi - fi.z : 0.f);
+                const float dz2 = fmaxf(ddz - slop, 0.f) * fmaxf(ddz - slop, 0.f);
+                for (int ry = 0; ry < 3; ++ry) {
+                    const float ddy = ry == 0 ? fi.y - ylo : (ry == 2 ? yhi - fi.y : 0.f);
+                    const float dyz2 = fmaf(fmaxf(ddy - slop, 0.f), fmaxf(ddy - slop, 0.f), dz2);
+                    if (dyz2 >= thr_hi) continue;
+                    const float xw = sqrtf(thr_hi - dyz2) + slop;
+                    const int R = (lz + rz) * (T.ty + 2) + (ly + ry);
+                    const float xl = fi.x - xw, xh = fi.x + xw;
+                    const int g0 = kSub * lx, g1 = kSub * (lx + 3);
+                    int gl = (int)floorf((xl - x0f) * inv_wsub) - 1;
+                    int gh = (int)floorf((xh - x0f) * inv_wsub) + 2;
+                    gl = min(max(gl, g0), g1);
+                    gh = min(max(gh, g0), g1);
+                    const int cl = min(gl / kSub, lx + 2), ch = min(gh / kSub, lx + 2);
+                    const int lo = S.sub[R][cl][gl - kSub * cl];
+                    const int hi = S.sub[R][ch][gh - kSub * ch];
+                    for (int base = lo; base < hi; base += 32) {   // 32 candidates per step
+                        const int jl = base + lane;
+                        bool take = false;
+                        if (jl < hi && jl != li) {   // R4 self exclusion
+                            const float4 fj = sF[jl];
+                            const float fx = fi.x - fj.x, fy = fi.y - fj.y, fz = fi.z - fj.z;
+                            const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
+                            if (r2f < thr_hi) {
+                                take = r2f < thr_lo;
+                                if (!take) {   // the canonical fp64 test in the band
+                                    const double4 xi = a.x[li + S.delta[R0]];
+                                    const double4 xj = a.x[jl + S.delta[R]];
+                                    take = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z) < a.rn2;
+                                }
+                            }
+                        }
+                        const unsigned mk = __ballot_sync(0xffffffffu, take);
+                        if (take) {
+                            const int pos = k + __popc(mk & ((1u << lane) - 1u));
+                            if (pos < K) nbr16[(((size_t)(pos >> 3) * stride + t) << 3) + (pos & 7)] = (unsigned short)jl;
+                        }
+                        k += __popc(mk);
+                    }
+                }
+            }
+            if ((k & 7) && k < K && lane < 8 - (k & 7)) {   // the last block: the tile's sentinel
+                const int pos = k + lane;
+                nbr16[(((size_t)(pos >> 3) * stride + t) << 3) + (pos & 7)] =
+                    (unsigned short)a.tr.off[tile * (kRowsMax + 1) + T.R];
+            }
+            if (lane == 0) {
+                a.ncount[t] = k;
+                kk += (unsigned long long)k;
+            }
+            kmax = max(kmax, k);
+        }
+    }
+    for (int q = part * per + (int)threadIdx.x; !SMALL && q < q_end; q += kBuildThreads) {
         int ci = 0;
         while (ci + 1 < ncell && S.cell_t0[ci + 1] <= q) ++ci;
         const int lx = ci % T.tx, ly = (ci / T.tx) % T.ty, lz = ci / (T.tx * T.ty);

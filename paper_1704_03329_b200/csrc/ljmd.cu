@@ -565,6 +565,14 @@ ljmd_status alloc_list(ljmd_ctx* c, int K) {
 // (+ the per-thread x-windows of the flattened candidate loop)
 inline size_t build_smem(const ljmd_ctx* c) { return 16 * (size_t)(c->stage_cap + 1) + 4 * (size_t)kBuildWinWords; }
 
+bool small_build_ok() {
+    static const bool ok = [] {
+        const char* e = getenv("LJMD_SMALL_BUILD");
+        return !(e && e[0] == '0');
+    }();
+    return ok;
+}
+
 ljmd_status launch_nlist(ljmd_ctx* c) {
     NlistArgs a;
     a.g = c->geo;
@@ -608,7 +616,10 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     a.stage_cap = c->stage_cap;
     a.parts = c->fparts;
     a.own_li = c->own_li;   // the force kernel's CTAs per tile (1 on large systems)
-    k_build_nlist<<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
+    if (c->fparts > 1 && small_build_ok())   // small systems: a warp per particle
+        k_build_nlist<true><<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
+    else
+        k_build_nlist<false><<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
     CKL();
     return LJMD_OK;
 }
@@ -711,7 +722,9 @@ cudaError_t force_attr() {
 }
 
 ljmd_status set_force_attrs(ljmd_ctx* c) {
-    cudaError_t e = cudaFuncSetAttribute(k_build_nlist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStageSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_build_nlist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStageSmem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_build_nlist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStageSmem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_list_rr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRrSmem);
     constexpr int KT = kKick | kThermo, DT = kKKD | kThermo;
