@@ -251,6 +251,25 @@ __global__ void k_scan_top(int* __restrict__ bsum, int nb, int* __restrict__ tot
     if (threadIdx.x == 0 && total_out) *total_out = carry;
 }
 
+// Small arrays (n <= kScanSingle): the whole exclusive scan and its total in one CTA -- one
+// launch instead of three (the per-rebuild scans of small systems are launch-latency-bound).
+constexpr int kScanSingle = 8192;
+__global__ void __launch_bounds__(1024) k_scan_single(const int* __restrict__ in, int n, int* __restrict__ out) {
+    __shared__ int sh[33];
+    const int per = (n + 1023) / 1024;
+    const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
+    int s = 0;
+    for (int i = b0; i < b1; ++i) s += in[i];
+    int tot;
+    int pre = block_excl_scan(s, sh, tot);
+    for (int i = b0; i < b1; ++i) {
+        const int v = in[i];
+        out[i] = pre;
+        pre += v;
+    }
+    if (threadIdx.x == 0) out[n] = tot;
+}
+
 // out[i] = exclusive prefix of in[0..i) (the total is written by k_scan_top)
 __global__ void k_scan_down(const int* __restrict__ in, int n, const int* __restrict__ bsum,
                             int* __restrict__ out, int /*unused*/) {

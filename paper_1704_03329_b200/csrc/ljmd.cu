@@ -324,6 +324,11 @@ inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 // exclusive scan of n ints: out[0..n) prefixes, out[n] = total
 ljmd_status scan(ljmd_ctx* c, const int* in, int n, int* out) {
+    if (n <= kScanSingle) {
+        k_scan_single<<<1, 1024, 0, c->stream>>>(in, n, out);
+        CKL();
+        return LJMD_OK;
+    }
     int nb = std::max(1, nblk(n, kScanTile));
     if (nb > c->scan_tmp_n) {
         TRY(dalloc(c, &c->scan_tmp, nb));
