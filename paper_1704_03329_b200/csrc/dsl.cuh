@@ -314,9 +314,21 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
              << " };\n";
     }
     if (pair) {
+        // the list in its 16-byte blocks of 8 indices (one load per block, the next block in
+        // flight while the current one is evaluated), as the engine's force kernel reads it
         s << "    const int ljmd_cnt = ljmd_p.ncount[ljmd_t];\n"
-             "    for (int ljmd_kk = 0; ljmd_kk < ljmd_cnt; ++ljmd_kk) {\n"
-             "      const int ljmd_l = ljmd_p.nbr[((long long)(ljmd_kk >> 3) * ljmd_p.n_pad + ljmd_t) * 8 + (ljmd_kk & 7)];\n"
+             "    const uint4* ljmd_nb = (const uint4*)ljmd_p.nbr + ljmd_t;\n"
+             "    const int ljmd_nblk = (ljmd_cnt + 7) >> 3;\n"
+             "    uint4 ljmd_cur = ljmd_nblk > 0 ? ljmd_nb[0] : make_uint4(0u, 0u, 0u, 0u);\n"
+             "    for (int ljmd_b = 0; ljmd_b < ljmd_nblk; ++ljmd_b) {\n"
+             "     const uint4 ljmd_nxt = ljmd_b + 1 < ljmd_nblk ? ljmd_nb[(long long)(ljmd_b + 1) * ljmd_p.n_pad]\n"
+             "                                                   : make_uint4(0u, 0u, 0u, 0u);\n"
+             "     const unsigned ljmd_w[4] = {ljmd_cur.x, ljmd_cur.y, ljmd_cur.z, ljmd_cur.w};\n"
+             "     ljmd_cur = ljmd_nxt;\n"
+             "     #pragma unroll\n"
+             "     for (int ljmd_e = 0; ljmd_e < 8; ++ljmd_e) {\n"
+             "      if (ljmd_b * 8 + ljmd_e >= ljmd_cnt) break;\n"
+             "      const int ljmd_l = (ljmd_e & 1) ? (int)(ljmd_w[ljmd_e >> 1] >> 16) : (int)(ljmd_w[ljmd_e >> 1] & 0xffffu);\n"
              "      const double* ljmd_xj = ljmd_sP + 3 * ljmd_l;\n"
              "      const double ljmd_dx = ljmd_xi[0] - ljmd_xj[0], ljmd_dy = ljmd_xi[1] - ljmd_xj[1];\n"
              "      const double ljmd_dz = ljmd_xi[2] - ljmd_xj[2];\n"
@@ -325,7 +337,7 @@ std::string generate(const DslLoop& L, const std::string& code, const std::strin
              "      if (!(ljmd_r2 < ljmd_p.cut2)) continue;\n"
              "      const int ljmd_tj = ljmd_sO[ljmd_l];\n"
              "      (void)ljmd_tj;\n"
-          << bind.str() << "      {\n" << code << "\n      }\n    }\n";
+          << bind.str() << "      {\n" << code << "\n      }\n     }\n    }\n";
     } else {
         s << "    {\n" << bind.str() << "      {\n" << code << "\n      }\n    }\n";
     }
