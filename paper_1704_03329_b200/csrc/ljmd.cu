@@ -570,12 +570,13 @@ ljmd_status alloc_list(ljmd_ctx* c, int K) {
 // (+ the per-thread x-windows of the flattened candidate loop)
 inline size_t build_smem(const ljmd_ctx* c) { return 16 * (size_t)(c->stage_cap + 1) + 4 * (size_t)kBuildWinWords; }
 
-bool small_build_ok() {
-    static const bool ok = [] {
+// LJMD_SMALL_BUILD: 0 never, 2 always (measurement), default on small systems
+int small_build_mode() {
+    static const int m = [] {
         const char* e = getenv("LJMD_SMALL_BUILD");
-        return !(e && e[0] == '0');
+        return e && *e ? atoi(e) : 1;
     }();
-    return ok;
+    return m;
 }
 
 ljmd_status launch_nlist(ljmd_ctx* c) {
@@ -621,7 +622,7 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     a.stage_cap = c->stage_cap;
     a.parts = c->fparts;
     a.own_li = c->own_li;   // the force kernel's CTAs per tile (1 on large systems)
-    if (c->fparts > 1 && small_build_ok())   // small systems: a warp per particle
+    if ((c->fparts > 1 && small_build_mode() == 1) || small_build_mode() == 2)   // small systems: a warp per particle
         k_build_nlist<true><<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
     else
         k_build_nlist<false><<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
