@@ -1,3 +1,4 @@
 OUT=gpurun_out
-timeout 600 python -m pytest tests/test_gpu_dsl.py tests/test_gpu_dsl_multirank.py -x -q > $OUT/gt47.log 2>&1; echo "rc=$?" >> $OUT/gt47.log
-python bench.py --steps 10 --no-cpu-baseline --no-validation --no-policy --no-boa --no-e2e > $OUT/b47.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $OUT/gt50.log 2>&1; echo "rc=$?" >> $OUT/gt50.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke50.log 2>&1
+timeout 1500 bash tools/bench_all.sh > $OUT/bench_all50.log 2>&1
