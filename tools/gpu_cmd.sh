@@ -1,4 +1,3 @@
 OUT=gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > $OUT/gt50.log 2>&1; echo "rc=$?" >> $OUT/gt50.log
-timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke50.log 2>&1
-timeout 1500 bash tools/bench_all.sh > $OUT/bench_all50.log 2>&1
+timeout 900 bash tools/klist.sh bl0 bl1 > $OUT/kl52.log 2>&1
+timeout 600 bash tools/ab.sh bl0 bl1 bl0 bl1 > $OUT/ab52.log 2>&1
