@@ -468,6 +468,24 @@ def main():
                       "note": "missed pair = r < rc at a step's positions but not in the list in use "
                               "(ljmd validate mode: fresh cell search minus in-range list entries)"}
 
+    # what the rebuild policy costs in energy conservation: 1000 NVE steps of the same workload
+    # with the continuous potential (V(rc) = 0, so that only a missed pair breaks conservation),
+    # relative drift of PE + KE under each policy (fresh contexts, not timed)
+    nve_drift = None
+    if not args.no_validation and world == 1 and not args.split_self and not args.newton3:
+        shift = (1.0 / li.RC) ** 6 - (1.0 / li.RC) ** 12
+        nve_drift = {"md_steps": 1000, "potential": "LJ shifted to V(rc) = 0", "energy_every": 10}
+        for name, chk in (("paper-fixed-20", 0), ("safe", 1)):
+            od = ljmd.default_options(device=local, stream=stream.cuda_stream, rebuild_check=chk,
+                                      energy_shift=shift)
+            with LJMD(pos, vel, box, rc=li.RC, dt=li.DT, options=od) as cd:
+                cd.step(1000)
+                pe_h, ke_h = cd.energy_history()
+                sd = cd.stats()
+            e_h = pe_h + ke_h
+            nve_drift[name] = {"rel_drift": float((e_h[-1] - e_h[0]) / abs(e_h[0])),
+                               "rebuilds": int(sd["n_rebuilds"]), "dangerous_builds": int(sd["dangerous_builds"])}
+
     # §8(f) NEXT-2 bond-order analysis on the same state (not part of the headline metric):
     # Q_6 with the first-shell cutoff 1.5 sigma, CUDA events around the call (kernel +
     # D2H of Q and |N(i)| + host scatter into caller order)
@@ -560,6 +578,7 @@ def main():
         "e2e": e2e,
         "other_rebuild_policy": policy,
         "validation": validation,
+        "nve_drift": nve_drift,
         "dangerous_builds": int(st1["dangerous_builds"] - st0["dangerous_builds"]),
         "rebuilds": int(st1["n_rebuilds"] - st0["n_rebuilds"]),
         "cpu_baseline": cpu,
