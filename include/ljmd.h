@@ -178,8 +178,17 @@ ljmd_status ljmd_wait_transfers(ljmd_ctx* c);
 /* Advance nsteps velocity-Verlet steps (Alg. alg:VelocityVerlet lines 5-9):
  * v += dt/(2m) F; r += dt v; [rebuild every Ns steps, after the drift, R8];
  * F <- sum over the list of Eq. eqn:LJforce (INC_ZERO, R5); v += dt/(2m) F.
- * PE and KE are sampled every energy_every steps.  On return x, v and F are
- * synchronised at the final step (velocities at full step). */
+ * PE and KE are sampled every energy_every steps.  After the call x, v and F are
+ * synchronised at the final step (velocities at full step).
+ * Asynchronous in graph mode under the fixed schedule (rebuild_check = 0): the call returns
+ * once its steps are queued on the stream, and the host reads its outcome (rebuild steps,
+ * energy samples, capacity aborts, error flags) when the NEXT ljmd_step call has been
+ * queued, or at the next call of any other function of this header that reads or changes
+ * the state -- so an error of one call (non-finite coordinates, coincident particles) is
+ * returned by the following call, and a call queued behind a capacity abort runs as no-ops
+ * and is re-run after the aborted one is resumed.  Work queued on the engine's stream after
+ * ljmd_step (events, copies) is ordered after the steps.  LJMD_DEFER=0 in the environment
+ * makes every call wait for its outcome (one host synchronisation per call). */
 ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps);
 
 /* Readback in the caller's order ([n][3] / [n]; with nranks > 1 only rows of

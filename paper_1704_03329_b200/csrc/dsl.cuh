@@ -471,7 +471,7 @@ ljmd_status dat_lookup(ljmd_ctx* c, int64_t h, DslDat** out) {
 }  // namespace
 
 extern "C" ljmd_status ljmd_dat_create(ljmd_ctx* c, int64_t ncomp, int64_t dtype, int64_t global, int64_t* handle) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!handle || ncomp < 1 || ncomp > (1 << 20) || dtype < 0 || dtype > 2)
         return set_err(c, LJMD_E_ARG, "ljmd_dat_create: ncomp >= 1 and dtype in {0 f64, 1 i32, 2 i64}");
     TRY(dsl_enable(c));
@@ -492,7 +492,7 @@ extern "C" ljmd_status ljmd_dat_create(ljmd_ctx* c, int64_t ncomp, int64_t dtype
 }
 
 extern "C" ljmd_status ljmd_dat_set(ljmd_ctx* c, int64_t h, const void* host) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     c->energy_current = false;   // engine velocities may change: no cached energies
     DslDat* d;
     TRY(dat_lookup(c, h, &d));
@@ -513,7 +513,7 @@ extern "C" ljmd_status ljmd_dat_set(ljmd_ctx* c, int64_t h, const void* host) {
 }
 
 extern "C" ljmd_status ljmd_dat_get(ljmd_ctx* c, int64_t h, void* host) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     DslDat* d;
     TRY(dat_lookup(c, h, &d));
     if (!host) return set_err(c, LJMD_E_ARG, "ljmd_dat_get: NULL");
@@ -544,7 +544,7 @@ extern "C" ljmd_status ljmd_dat_get(ljmd_ctx* c, int64_t h, void* host) {
 }
 
 extern "C" ljmd_status ljmd_dat_free(ljmd_ctx* c, int64_t h) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     DslDat* d;
     TRY(dat_lookup(c, h, &d));
     CK(cudaStreamSynchronize(c->stream));
@@ -558,7 +558,7 @@ extern "C" ljmd_status ljmd_loop_create(ljmd_ctx* c, int64_t kind, const char* n
                                         const char* constants, double shell_cutoff, int64_t nargs,
                                         const char* const* labels, const int64_t* handles, const int64_t* access,
                                         int64_t flags, int64_t* loop) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!loop || !name || !code || (nargs > 0 && (!labels || !handles || !access)) || nargs < 0 ||
         nargs > kDslMaxArgs || (kind != 0 && kind != 1))
         return set_err(c, LJMD_E_ARG, "ljmd_loop_create: bad arguments (kind 0/1, at most %d dats)", kDslMaxArgs);
@@ -719,7 +719,7 @@ ljmd_status dsl_halo(ljmd_ctx* c, DslLoop& L, size_t k, DslParams& p) {
 }  // namespace
 
 extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (loop < 0 || loop >= (int64_t)c->loops.size() || !c->loops[loop] || !c->loops[loop]->alive)
         return set_err(c, LJMD_E_ARG, "bad loop handle %lld", (long long)loop);
     DslLoop& L = *c->loops[loop];
@@ -826,7 +826,7 @@ extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
 }
 
 extern "C" ljmd_status ljmd_loop_source(ljmd_ctx* c, int64_t loop, char* out, int64_t cap, int64_t* len) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (loop < 0 || loop >= (int64_t)c->loops.size() || !c->loops[loop])
         return set_err(c, LJMD_E_ARG, "bad loop handle %lld", (long long)loop);
     const std::string& s = c->loops[loop]->source;
@@ -840,7 +840,7 @@ extern "C" ljmd_status ljmd_loop_source(ljmd_ctx* c, int64_t loop, char* out, in
 }
 
 extern "C" ljmd_status ljmd_loop_free(ljmd_ctx* c, int64_t loop) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (loop < 0 || loop >= (int64_t)c->loops.size() || !c->loops[loop])
         return set_err(c, LJMD_E_ARG, "bad loop handle %lld", (long long)loop);
     CK(cudaStreamSynchronize(c->stream));

@@ -107,6 +107,40 @@ __global__ void k_decide(DevCtl* ctl, DevFlags* fl, int ns, int check, int force
 
 __global__ void k_set_since(DevCtl* ctl, int since) { ctl->since = since; }
 
+// First node of a captured call: clears the per-call control -- unless an earlier call queued
+// on the stream aborted (deferred settlement): then the abort record stays and
+// every kernel of this call returns at once, so the host can resume the aborted call first.
+__global__ void k_call_begin(DevCtl* ctl) {
+    if (ctl->abort) return;
+    ctl->abort_step = 0;
+    ctl->nreb = 0;
+    ctl->nsamp = 0;
+    ctl->step = 0;
+}
+
+// Last node after a captured call: the call's control, flags, slot count, rebuild steps and
+// energy samples into mapped page-locked memory (one of two buffers, alternating per call),
+// so the host can read them after the NEXT call is queued.
+struct CallOut {
+    DevCtl ctl;
+    int slots;
+    int pad;
+    DevFlags fl;
+};
+
+__global__ void k_call_out(const DevCtl* __restrict__ ctl, const DevFlags* __restrict__ fl,
+                           const int* __restrict__ slots, const int* __restrict__ rstep,
+                           const double* __restrict__ hist, CallOut* out, int* out_rstep, double* out_hist) {
+    const DevCtl cc = *ctl;
+    if (threadIdx.x == 0) {
+        out->ctl = cc;
+        out->slots = *slots;
+        out->fl = *fl;
+    }
+    for (int i = threadIdx.x; i < cc.nreb; i += blockDim.x) out_rstep[i] = rstep[i];
+    for (int i = threadIdx.x; i < 2 * cc.nsamp; i += blockDim.x) out_hist[i] = hist[i];
+}
+
 // capacity checks inside a captured rebuild: stage 1 (before anything is permuted) the slot
 // count, stage 2 (after the tile tables) the staging size, stage 3 the list width
 __global__ void k_check_caps(DevCtl* ctl, const DevFlags* fl, const int* need_slots, int slot_cap, int stage_cap,
@@ -2079,7 +2113,8 @@ __global__ void k_kick_drift(int n_own, double4* __restrict__ x, const int* __re
                              const double* __restrict__ fx, const double* __restrict__ fy,
                              const double* __restrict__ fz, double h, double dt,
                              const double4* __restrict__ xbuild, DevFlags* fl, Images im, Geo g,
-                             double* __restrict__ xp, double4* __restrict__ xprev) {
+                             double* __restrict__ xp, double4* __restrict__ xprev, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured call behind an aborted one (k_call_begin)
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long bits = 0ull;
     if (t < n_own) {

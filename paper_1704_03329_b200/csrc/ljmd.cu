@@ -186,6 +186,24 @@ struct ljmd_ctx {
     int64_t graph_calls = 0, graph_aborts = 0;
     int64_t rebuild_kernels = 0;      // kernels of one captured rebuild (for the launch count)
     int64_t call_nsamp = 0;           // energy samples of the current ljmd_step call
+    // deferred settlement (graph mode, fixed rebuild schedule): ljmd_step returns once its
+    // graph is queued; the host reads the call's control (k_call_out, two alternating mapped
+    // buffers) after queueing the next call, or at the next API call
+    struct Pending {
+        bool on = false;
+        bool deferred = false;        // the host state was advanced at launch
+        int64_t step0 = 0, nsteps = 0, launches = 0;
+        int64_t sim_since = 0;        // fixed schedule: steps since the last rebuild at the end
+        int xc0 = 0, buf = 0;
+    };
+    Pending pend;
+    CallOut* h_out[2] = {nullptr, nullptr};     // mapped
+    int* h_orstep[2] = {nullptr, nullptr};      // mapped [out_cap]
+    double* h_ohist[2] = {nullptr, nullptr};    // mapped [2 out_cap]
+    int64_t out_cap = 0;
+    int out_next = 0;
+    cudaEvent_t ev_call[2] = {nullptr, nullptr};
+    int64_t deferred_calls = 0;
     int* h_slots = nullptr;        // pinned
     double* d_stage = nullptr;     // [3][own_cap] readback staging
     // overlapped host transfers (ljmd_stage_state / ljmd_get_positions_async)
@@ -1726,6 +1744,16 @@ ljmd_status readback(ljmd_ctx* c, const double* dsrc, int width, double* out) {
 // ====================================================================== C ABI
 extern "C" {
 
+// the last ljmd_step call's results on the host (deferred settlement); defined below
+ljmd_status settle(ljmd_ctx* c);
+
+// API entry that reads or changes the state: the context is usable and every queued
+// ljmd_step call has been settled (its errors surface here)
+static ljmd_status check_ready(ljmd_ctx* c) {
+    TRY(check_ctx(c));
+    return settle(c);
+}
+
 const char* ljmd_version(void) { return "ljmd 0.1 sm_100a"; }
 
 ljmd_status ljmd_default_options(ljmd_options* o) {
@@ -1937,7 +1965,7 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
 }
 
 ljmd_status ljmd_set_state(ljmd_ctx* c, const double* pos, const double* vel) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!pos && !vel) {
         if (c->stg_queued == 0) return set_err(c, LJMD_E_ARG, "ljmd_set_state(NULL, NULL): no staged state queued");
         const int b = (c->stg_next + 2 - c->stg_queued) & 1;   // oldest queued buffer
@@ -1986,7 +2014,7 @@ ljmd_status ljmd_stage_state(ljmd_ctx* c, const double* pos, const double* vel) 
 }
 
 ljmd_status ljmd_get_positions_async(ljmd_ctx* c, double* out) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!out) return LJMD_E_ARG;
     TRY(transfers_init(c));
     const int b = c->rb_next;
@@ -2021,11 +2049,11 @@ ljmd_status kick_drift(ljmd_ctx* c) {
     if (check)
         k_kick_drift<true><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
             c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h, c->dt,
-            c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
+            c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1], c->capturing ? c->d_ctl : nullptr);
     else
         k_kick_drift<false><<<nblk(c->n_own, 256), 256, 0, c->stream>>>(
             c->n_own, c->x[c->xc], c->own_slot, v, v + oc, v + 2 * oc, c->F, c->F + oc, c->F + 2 * oc, h, c->dt,
-            c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1]);
+            c->xbuild, c->d_fl, images(c), c->geo, c->xp[c->xc], c->x[c->xc ^ 1], c->capturing ? c->d_ctl : nullptr);
     CKL();
     return LJMD_OK;
 }
@@ -2124,7 +2152,9 @@ ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) 
     c->capturing = true;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     ljmd_status r = [&]() -> ljmd_status {
-        CK(cudaMemsetAsync(c->d_ctl, 0, offsetof(DevCtl, since), c->stream));   // since persists across calls
+        // the per-call control (since persists across calls; an earlier call's abort too)
+        k_call_begin<<<1, 1, 0, c->stream>>>(c->d_ctl);
+        CKL();
         TRY(kick_drift(c));
         int64_t sim_since = c->since;
         for (int64_t s = 1; s <= nsteps; ++s) {
@@ -2182,16 +2212,116 @@ ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) 
     return LJMD_OK;
 }
 
-ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps) {
+// Host side of a settled graph call p: rebuild bookkeeping, errors, energies; a capacity abort
+// resumes the call on the eager path.  next: a call queued after p (deferred), which ran as
+// no-ops if p aborted (k_call_begin) and is then re-run here.
+ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer);
+
+ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pending* next) {
+    const int64_t ee = c->opt.energy_every;
+    CK(cudaEventSynchronize(c->ev_call[p.buf]));
+    const CallOut o = *c->h_out[p.buf];
+    const DevCtl& ctl = o.ctl;
+    c->kernel_launches += p.launches + (int64_t)ctl.nreb * c->rebuild_kernels;
+    for (int k = 0; k < ctl.nreb; ++k) {
+        const int64_t st = p.step0 + c->h_orstep[p.buf][k];
+        if (c->last_build_step >= 0 && st > c->last_build_step)
+            c->interval_ema = 0.5 * c->interval_ema + 0.5 * (double)(st - c->last_build_step);
+        c->last_build_step = st;
+        note_rebuild(c, st);
+    }
+    if (o.fl.nonfinite_gid != INT_MAX)
+        return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d", o.fl.nonfinite_gid);
+    if (o.fl.overlap_pair != ~0ull)
+        return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)",
+                       (int)(o.fl.overlap_pair >> 32), (int)(o.fl.overlap_pair & 0xffffffffu));
+    if (ctl.nreb > 0) {
+        c->n_slots = o.slots;
+        c->max_staged = o.fl.max_staged;
+        c->n_gflat = o.fl.n_gflat;
+        c->max_nbr = o.fl.max_nbr;
+        c->total_nbr = o.fl.total_nbr;
+    }
+    if (!ctl.abort) {
+        c->h_hist.insert(c->h_hist.end(), c->h_ohist[p.buf], c->h_ohist[p.buf] + 2 * (size_t)ctl.nsamp);
+        if (!p.deferred) {   // else advanced at launch
+            c->steps_done = p.step0 + p.nsteps;
+            c->xc = p.xc0 ^ (int)((p.nsteps - 1) & 1);
+            c->since = c->opt.rebuild_check ? (int64_t)ctl.since : p.sim_since;
+            c->energy_current = ee > 0 && (c->steps_done % ee) == 0;
+        }
+        // the current energies: from this call unless a later one is queued
+        if (!(next && next->on) && ee > 0 && ((p.step0 + p.nsteps) % ee) == 0 && ctl.nsamp > 0) {
+            c->cur_pe = c->h_ohist[p.buf][2 * ctl.nsamp - 2];
+            c->cur_ke = c->h_ohist[p.buf][2 * ctl.nsamp - 1];
+        }
+        return LJMD_OK;
+    }
+    // a capacity ran short in the rebuild of step sa: steps 1 .. sa-1 are complete, step sa
+    // has drifted; resume there on the eager path (its rebuild regrows what is short)
+    ljmd_ctx::Pending skipped;
+    if (next && next->on) {
+        skipped = *next;
+        next->on = false;
+    }
+    // a skipped call may still be on the stream: let it drain before buffers (and the graphs
+    // holding their pointers) are regrown
+    CK(cudaStreamSynchronize(c->stream));
+    const int64_t sa = ctl.abort_step;
+    ++c->graph_aborts;
+    c->steps_done = p.step0 + sa;
+    c->since = 0;
+    c->xc = p.xc0 ^ (int)((sa - 1) & 1);
+    c->call_nsamp = ctl.nsamp;
+    CK(cudaMemsetAsync(c->d_ctl, 0, offsetof(DevCtl, since), c->stream));
+    TRY(rebuild(c, /*danger=*/false));   // the dangerous-build test of this rebuild already ran
+    TRY(step_eager(c, sa, p.nsteps, true));
+    TRY(pull_hist(c, c->call_nsamp));    // the graph's samples and the eager steps'
+    if (c->energy_current) {
+        c->cur_pe = c->h_hist[c->h_hist.size() - 2];
+        c->cur_ke = c->h_hist[c->h_hist.size() - 1];
+    }
+    if (skipped.on) TRY(step_call(c, skipped.nsteps, false));
+    return LJMD_OK;
+}
+
+ljmd_status settle(ljmd_ctx* c) {
+    if (!c->pend.on) return LJMD_OK;
+    const ljmd_ctx::Pending p = c->pend;
+    c->pend.on = false;
+    return settle_call(c, p, nullptr);
+}
+
+// mapped per-call output buffers for calls of up to n steps
+static ljmd_status ensure_out(ljmd_ctx* c, int64_t n) {
+    if (!c->ev_call[0]) {
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&c->ev_call[b], cudaEventDisableTiming));
+            CK(cudaHostAlloc(&c->h_out[b], sizeof(CallOut), cudaHostAllocMapped));
+        }
+    }
+    if (n <= c->out_cap) return LJMD_OK;
+    const int64_t cap = std::max<int64_t>(n, 64);
+    for (int b = 0; b < 2; ++b) {
+        if (c->h_orstep[b]) cudaFreeHost(c->h_orstep[b]);
+        if (c->h_ohist[b]) cudaFreeHost(c->h_ohist[b]);
+        c->h_orstep[b] = nullptr;
+        c->h_ohist[b] = nullptr;
+        CK(cudaHostAlloc(&c->h_orstep[b], sizeof(int) * (size_t)cap, cudaHostAllocMapped));
+        CK(cudaHostAlloc(&c->h_ohist[b], sizeof(double) * 2 * (size_t)(cap + 2), cudaHostAllocMapped));
+    }
+    c->out_cap = cap;
+    return LJMD_OK;
+}
+
+ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer) {
     const bool check = c->opt.rebuild_check != 0;
     const int64_t ee = c->opt.energy_every;
     if (c->rstep_cap < nsteps) {
         TRY(dalloc(c, &c->d_rstep, (size_t)nsteps));
-        if (c->h_rstep) cudaFreeHost(c->h_rstep);
-        c->h_rstep = nullptr;
-        CK(cudaHostAlloc(&c->h_rstep, sizeof(int) * (size_t)nsteps, cudaHostAllocMapped));
         c->rstep_cap = nsteps;
     }
+    TRY(ensure_out(c, nsteps));
     char key[160];
     snprintf(key, sizeof key, "n%lld x%d s%lld e%lld c%d r%d", (long long)nsteps, c->xc,
              check ? -1LL : (long long)c->since, ee > 0 ? (long long)(c->steps_done % ee) : 0LL, check ? 1 : 0,
@@ -2202,68 +2332,53 @@ ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps) {
         TRY(capture_call(c, nsteps, ge));
         it = c->graphs.emplace(key, ge).first;
     }
-    const int64_t step0 = c->steps_done;
-    const int xc0 = c->xc;
-    int64_t sim_since = c->since;   // fixed policy: the host-known schedule
-    for (int64_t s = 1; s <= nsteps; ++s)
-        if (++sim_since >= c->opt.rebuild_every) sim_since = 0;
+    ljmd_ctx::Pending p;
+    p.on = true;
+    p.step0 = c->steps_done;
+    p.nsteps = nsteps;
+    p.xc0 = c->xc;
+    p.launches = it->second.launches;
+    p.buf = c->out_next;
+    c->out_next ^= 1;
     if (check) {
         k_set_since<<<1, 1, 0, c->stream>>>(c->d_ctl, (int)c->since);
         CKL();
     }
     CK(cudaGraphLaunch(it->second.ex, c->stream));
     ++c->graph_calls;
-    TRY(to_host(c, c->h_ctl, c->d_ctl, sizeof(DevCtl)));
-    TRY(to_host(c, c->h_rstep, c->d_rstep, sizeof(int) * (size_t)nsteps));
-    TRY(to_host(c, c->h_slots, c->ebegin + c->n_ecell, sizeof(int)));
-    TRY(sync_flags(c));
-    const DevCtl ctl = *c->h_ctl;
-    c->kernel_launches += it->second.launches + (int64_t)ctl.nreb * c->rebuild_kernels;
-    for (int k = 0; k < ctl.nreb; ++k) {
-        const int64_t st = step0 + c->h_rstep[k];
-        if (c->last_build_step >= 0 && st > c->last_build_step)
-            c->interval_ema = 0.5 * c->interval_ema + 0.5 * (double)(st - c->last_build_step);
-        c->last_build_step = st;
-        note_rebuild(c, st);
-    }
-    c->call_nsamp = ctl.nsamp;
-    if (c->h_fl->nonfinite_gid != INT_MAX)
-        return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d", c->h_fl->nonfinite_gid);
-    if (c->h_fl->overlap_pair != ~0ull)
-        return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)",
-                       (int)(c->h_fl->overlap_pair >> 32), (int)(c->h_fl->overlap_pair & 0xffffffffu));
-    if (ctl.nreb > 0) {
-        c->n_slots = *c->h_slots;
-        c->max_staged = c->h_fl->max_staged;
-        c->n_gflat = c->h_fl->n_gflat;
-        c->max_nbr = c->h_fl->max_nbr;
-        c->total_nbr = c->h_fl->total_nbr;
-    }
-    if (!ctl.abort) {
-        c->steps_done = step0 + nsteps;
-        c->since = check ? ctl.since : sim_since;
-        c->xc = xc0 ^ (int)((nsteps - 1) & 1);
-        c->energy_current = ee > 0 && (c->steps_done % ee) == 0;
-        return LJMD_OK;
-    }
-    // a capacity ran short in the rebuild of step sa: steps 1 .. sa-1 are complete, step sa
-    // has drifted; resume there on the eager path (its rebuild regrows what is short)
-    const int64_t sa = ctl.abort_step;
-    ++c->graph_aborts;
-    c->steps_done = step0 + sa;
-    c->since = 0;
-    c->xc = xc0 ^ (int)((sa - 1) & 1);
-    CK(cudaMemsetAsync(c->d_ctl, 0, offsetof(DevCtl, since), c->stream));
-    TRY(rebuild(c, /*danger=*/false));   // the dangerous-build test of this rebuild already ran
-    return step_eager(c, sa, nsteps, true);
+    k_call_out<<<1, 256, 0, c->stream>>>(c->d_ctl, c->d_fl, c->ebegin + c->n_ecell, c->d_rstep, c->hist,
+                                         c->h_out[p.buf], c->h_orstep[p.buf], c->h_ohist[p.buf]);
+    CKL();
+    CK(cudaEventRecord(c->ev_call[p.buf], c->stream));
+    p.sim_since = c->since;
+    for (int64_t s = 1; s <= nsteps; ++s)
+        if (++p.sim_since >= c->opt.rebuild_every) p.sim_since = 0;
+    if (!defer) return settle_call(c, p, nullptr);   // one host wait per call
+    // the fixed schedule is host-known: advance the state now, settle the previous call
+    p.deferred = true;
+    const ljmd_ctx::Pending prev = c->pend;
+    c->pend = p;
+    c->steps_done = p.step0 + nsteps;
+    c->since = p.sim_since;
+    c->xc = p.xc0 ^ (int)((nsteps - 1) & 1);
+    c->energy_current = ee > 0 && (c->steps_done % ee) == 0;
+    ++c->deferred_calls;
+    if (prev.on) TRY(settle_call(c, prev, &c->pend));
+    return LJMD_OK;
 }
 
-ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
-    TRY(check_ctx(c));
-    if (nsteps < 0) return set_err(c, LJMD_E_ARG, "ljmd_step: nsteps < 0");
-    if (nsteps == 0) return LJMD_OK;
+// One ljmd_step call.  defer: graph mode under the fixed schedule returns once the call is
+// queued (LJMD_DEFER=0 turns that off).
+ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer) {
     const int64_t ee = c->opt.energy_every;
-    TRY(ensure_hist(c, nsteps / std::max<int64_t>(ee, 1) + 2));
+    const int64_t need_hist = nsteps / std::max<int64_t>(ee, 1) + 2;
+    const bool graph = graph_ok(c);
+    defer = defer && graph && c->opt.rebuild_check == 0;
+    // buffers a queued call uses are regrown only after it has been settled
+    if (c->pend.on && (!defer || need_hist > c->hist_cap || nsteps > c->rstep_cap || nsteps > c->out_cap))
+        TRY(settle(c));
+    TRY(settle_init(c));
+    TRY(ensure_hist(c, need_hist));
     c->call_nsamp = 0;
     const int64_t first_launch = c->force_launches;
     const int64_t step0 = c->steps_done;
@@ -2277,13 +2392,9 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
         CK(cudaMemsetAsync(c->vhist, 0, sizeof(int) * 2 * (size_t)nsteps, c->stream));
     }
     decide_list_order(c);
-    if (graph_ok(c)) {
-        TRY(step_graph(c, nsteps));
-    } else {
-        TRY(kick_drift(c));
-        TRY(step_eager(c, 1, nsteps, false));
-    }
-    TRY(settle_init(c));
+    if (graph) return step_graph(c, nsteps, defer);   // settled there unless deferred
+    TRY(kick_drift(c));
+    TRY(step_eager(c, 1, nsteps, false));
     TRY(pull_hist(c, c->call_nsamp));
     if (c->energy_current) {
         c->cur_pe = c->h_hist[c->h_hist.size() - 2];
@@ -2307,8 +2418,15 @@ ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
     return LJMD_OK;
 }
 
-ljmd_status ljmd_get_forces(ljmd_ctx* c, double* out) {
+ljmd_status ljmd_step(ljmd_ctx* c, int64_t nsteps) {
     TRY(check_ctx(c));
+    if (nsteps < 0) return set_err(c, LJMD_E_ARG, "ljmd_step: nsteps < 0");
+    if (nsteps == 0) return LJMD_OK;
+    return step_call(c, nsteps, getenv_int("LJMD_DEFER", 1) != 0);
+}
+
+ljmd_status ljmd_get_forces(ljmd_ctx* c, double* out) {
+    TRY(check_ready(c));
     if (!out) return LJMD_E_ARG;
     const size_t oc = c->own_cap;
     k_gather_soa<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->F, c->F + oc, c->F + 2 * oc, c->d_stage);
@@ -2317,7 +2435,7 @@ ljmd_status ljmd_get_forces(ljmd_ctx* c, double* out) {
 }
 
 ljmd_status ljmd_get_velocities(ljmd_ctx* c, double* out) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!out) return LJMD_E_ARG;
     const size_t oc = c->own_cap;
     const double* v = c->v[c->oc_cur];
@@ -2327,7 +2445,7 @@ ljmd_status ljmd_get_velocities(ljmd_ctx* c, double* out) {
 }
 
 ljmd_status ljmd_get_positions(ljmd_ctx* c, double* out, int64_t wrapped) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!out) return LJMD_E_ARG;
     k_gather_pos<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->x[c->xc], c->own_slot, c->d_stage);
     CKL();
@@ -2352,14 +2470,14 @@ ljmd_status ljmd_get_positions(ljmd_ctx* c, double* out, int64_t wrapped) {
 }
 
 ljmd_status ljmd_get_particle_energy(ljmd_ctx* c, double* out) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!out) return LJMD_E_ARG;
     TRY(energy_now(c));
     return readback(c, c->e, 1, out);
 }
 
 ljmd_status ljmd_get_energy(ljmd_ctx* c, double* pe, double* ke) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     TRY(energy_now(c));
     if (pe) *pe = c->cur_pe;
     if (ke) *ke = c->cur_ke;
@@ -2375,7 +2493,7 @@ extern "C" int ljmd_debug_phases(unsigned long long* out, int n) {
 #endif
 
 ljmd_status ljmd_get_energy_history(ljmd_ctx* c, double* pe, double* ke, int64_t cap, int64_t* count) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     TRY(settle_init(c));
     int64_t avail = (int64_t)c->h_hist.size() / 2;
     if (count) *count = avail;
@@ -2387,7 +2505,7 @@ ljmd_status ljmd_get_energy_history(ljmd_ctx* c, double* pe, double* ke, int64_t
 }
 
 ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, int64_t cap) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!offsets) return LJMD_E_ARG;
     const int n = c->n_own;
     std::vector<int> cnt(n), g(n);
@@ -2421,7 +2539,7 @@ ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, in
 }
 
 ljmd_status ljmd_get_rebuild_steps(ljmd_ctx* c, int64_t* out, int64_t cap, int64_t* count) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     int64_t n = (int64_t)c->rebuild_steps.size();
     if (count) *count = n;
     for (int64_t i = 0; out && i < std::min(n, cap); ++i) out[i] = c->rebuild_steps[(size_t)i];
@@ -2429,7 +2547,7 @@ ljmd_status ljmd_get_rebuild_steps(ljmd_ctx* c, int64_t* out, int64_t cap, int64
 }
 
 ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!s) return LJMD_E_ARG;
     std::memset(s, 0, sizeof *s);
     s->steps_done = c->steps_done;
@@ -2464,7 +2582,7 @@ ljmd_status ljmd_get_stats(ljmd_ctx* c, ljmd_stats* s) {
 }
 
 ljmd_status ljmd_get_validation(ljmd_ctx* c, int64_t* out, int64_t cap, int64_t* count) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!c->opt.validate) return set_err(c, LJMD_E_ARG, "ljmd_get_validation: validation mode is off");
     const int64_t nv = (int64_t)c->h_val.size() / 3;
     if (count) *count = nv;
@@ -2511,6 +2629,12 @@ void ljmd_destroy(ljmd_ctx* c) {
     drop_graphs(c);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     if (c->h_rstep) cudaFreeHost(c->h_rstep);
+    for (int b = 0; b < 2; ++b) {
+        if (c->h_out[b]) cudaFreeHost(c->h_out[b]);
+        if (c->h_orstep[b]) cudaFreeHost(c->h_orstep[b]);
+        if (c->h_ohist[b]) cudaFreeHost(c->h_ohist[b]);
+        if (c->ev_call[b]) cudaEventDestroy(c->ev_call[b]);
+    }
     for (void* p : {(void*)c->d_ctl, (void*)c->d_rstep, (void*)c->halo_flag})
         if (p) cudaFree(p);
     for (cudaStream_t st : c->cap_stream)
@@ -2553,7 +2677,7 @@ void boa_launch(ljmd_ctx* c, const BoaArgs& a, size_t smem) {
 }
 
 extern "C" ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q, int64_t* nnb) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!Q || ell < 0 || ell > kBoaMaxL || !(rcut > 0.0))
         return set_err(c, LJMD_E_ARG, "ljmd_boa: need 0 <= ell <= %d and rcut > 0", kBoaMaxL);
     if (rcut > c->rc)
@@ -2607,7 +2731,7 @@ extern "C" ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q
 
 
 extern "C" ljmd_status ljmd_set_thermostat(ljmd_ctx* c, double nu, double temperature, uint64_t seed) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!(nu >= 0.0) || !(temperature >= 0.0) || !(nu * c->dt <= 1.0))
         return set_err(c, LJMD_E_ARG, "ljmd_set_thermostat: need nu >= 0, T >= 0 and nu*dt <= 1 (nu*dt = %g)",
                        nu * c->dt);
@@ -2618,14 +2742,14 @@ extern "C" ljmd_status ljmd_set_thermostat(ljmd_ctx* c, double nu, double temper
 }
 
 extern "C" ljmd_status ljmd_set_profile(ljmd_ctx* c, int64_t profile) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (profile != 0 && profile != 1) return set_err(c, LJMD_E_ARG, "ljmd_set_profile: profile must be 0 or 1");
     c->opt.profile = profile;
     return LJMD_OK;
 }
 
 extern "C" ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t* trip, int64_t* nnb) {
-    TRY(check_ctx(c));
+    TRY(check_ready(c));
     if (!cls || !(rcut > 0.0)) return set_err(c, LJMD_E_ARG, "ljmd_cna: cls and rcut > 0 required");
     if (rcut > c->rc)
         return set_err(c, LJMD_E_ARG, "ljmd_cna: rcut %g exceeds the force cutoff rc = %g (list validity)", rcut,

@@ -77,3 +77,46 @@ def test_graph_parity_with_oracle(eng, orc):
     r = orc.run(pos, vel, box, 40)
     np.testing.assert_allclose(pe, r.pe, rtol=1e-8)
     np.testing.assert_allclose(ke, r.ke, rtol=1e-8)
+
+
+def test_deferred_settlement_equals_synchronous(eng, monkeypatch):
+    """Graph calls under the fixed schedule return once queued; the host settles a call after
+    queueing the next one (or at the next getter).  Against LJMD_DEFER=0 (one host wait per
+    call) and the eager path: the same trajectory, energies and rebuild steps bit for bit,
+    with getters interleaved between the calls."""
+    pos, vel, box = state()
+    calls = [20, 20, 20, 3, 17, 20, 40, 1]
+
+    def run_mixed(**kw):
+        hist = []
+        with eng.LJMD(pos, vel, box, **kw) as ctx:
+            for k, n in enumerate(calls):
+                ctx.step(n)
+                if k % 3 == 2:
+                    hist.append(ctx.energy())
+                    hist.append(ctx.stats()["steps_done"])
+            out = dict(x=ctx.positions(), v=ctx.velocities(), F=ctx.forces(), e=ctx.energy_history(),
+                       reb=ctx.rebuild_steps(), st=ctx.stats())
+        return out, hist
+
+    monkeypatch.setenv("LJMD_DEFER", "0")
+    s, hs = run_mixed(graphs=1)
+    e, he = run_mixed(graphs=0)
+    monkeypatch.setenv("LJMD_DEFER", "1")
+    d, hd = run_mixed(graphs=1)
+    same(d, s)
+    same(d, e)
+    assert hd == hs == he
+    assert d["st"]["steps_done"] == sum(calls) and d["st"]["graph_calls"] == len(calls)
+
+
+def test_deferred_abort_with_queued_calls(eng):
+    """A capacity abort in a call that already has the next one queued behind it: the queued
+    call runs as no-ops on the device (k_call_begin keeps the abort record), the host resumes
+    the aborted call eagerly and re-runs the queued one -- the eager trajectory bit for bit."""
+    pos, vel, box = state(sigma_d=0.0, t0=2.0)
+    calls = [20, 20, 20, 20]
+    g = run(eng, pos, vel, box, calls, graphs=1, tight_caps=1)
+    e = run(eng, pos, vel, box, calls, graphs=0)
+    same(g, e)
+    assert g["st"]["graph_aborts"] >= 1 and g["st"]["steps_done"] == sum(calls)
