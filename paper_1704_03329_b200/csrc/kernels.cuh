@@ -87,10 +87,12 @@ struct DevCtl {
 // delta^2), the last from the previous step's epilogue (non-negative doubles compare as
 // their bit patterns); the maximum is cleared for this step's epilogue.
 // step_now: the step of the call (1-based) this decision belongs to
+// has_cond = 0 (a forced rebuild of the fixed schedule, captured without a conditional node:
+// its kernels check the abort flag themselves): the decision is only recorded
 __global__ void k_decide(DevCtl* ctl, DevFlags* fl, int ns, int check, int forced, double delta2, int* rstep,
-                         int step_now, cudaGraphConditionalHandle h) {
+                         int step_now, cudaGraphConditionalHandle h, int has_cond) {
     if (ctl->abort) {
-        cudaGraphSetConditional(h, 0u);
+        if (has_cond) cudaGraphSetConditional(h, 0u);
         return;
     }
     ctl->step = step_now;
@@ -102,7 +104,7 @@ __global__ void k_decide(DevCtl* ctl, DevFlags* fl, int ns, int check, int force
         ctl->since = 0;
         rstep[ctl->nreb++] = ctl->step;
     }
-    cudaGraphSetConditional(h, due ? 1u : 0u);
+    if (has_cond) cudaGraphSetConditional(h, due ? 1u : 0u);
 }
 
 __global__ void k_set_since(DevCtl* ctl, int since) { ctl->since = since; }
@@ -143,14 +145,14 @@ __global__ void k_call_out(const DevCtl* __restrict__ ctl, const DevFlags* __res
 
 // capacity checks inside a captured rebuild: stage 1 (before anything is permuted) the slot
 // count, stage 2 (after the tile tables) the staging size, stage 3 the list width
+// (the kernels after a failed check return at entry: cctl() in the launches)
 __global__ void k_check_caps(DevCtl* ctl, const DevFlags* fl, const int* need_slots, int slot_cap, int stage_cap,
-                             int K, int stage, cudaGraphConditionalHandle h) {
+                             int K, int stage) {
     bool ok = !ctl->abort;
     if (ok && stage == 1 && *need_slots > slot_cap) { ctl->abort = 1; ok = false; }
     if (ok && stage == 2 && fl->max_staged > stage_cap) { ctl->abort = 2; ok = false; }
     if (ok && stage == 3 && fl->max_nbr > K) { ctl->abort = 2; ok = false; }
     if (!ok && ctl->abort_step == 0) ctl->abort_step = ctl->step;
-    if (stage < 3) cudaGraphSetConditional(h, ok ? 1u : 0u);
 }
 
 __device__ __forceinline__ double4 ld256(const double4* p) {
@@ -288,6 +290,38 @@ __global__ void k_scan_top(int* __restrict__ bsum, int nb, int* __restrict__ tot
 // Small arrays (n <= kScanSingle): the whole exclusive scan and its total in one CTA -- one
 // launch instead of three (the per-rebuild scans of small systems are launch-latency-bound).
 constexpr int kScanSingle = 8192;
+__device__ __forceinline__ void scan_single_block(const int* __restrict__ in, int n, int* __restrict__ out, int* sh) {
+    const int per = (n + 1023) / 1024;
+    const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
+    int s = 0;
+    for (int i = b0; i < b1; ++i) s += in[i];
+    int tot;
+    int pre = block_excl_scan(s, sh, tot);
+    for (int i = b0; i < b1; ++i) {
+        const int v = in[i];
+        out[i] = pre;
+        pre += v;
+    }
+    if (threadIdx.x == 0) out[n] = tot;
+}
+
+// Small systems (both cell counts <= kScanSingle): the owned-cell offsets, the extended-cell
+// counts (as k_ext_counts) and their offsets in one CTA -- one launch instead of three.
+__global__ void __launch_bounds__(1024) k_bin_offsets_single(const int* __restrict__ ocount, int n_ocell,
+                                                            int* __restrict__ obegin, int n_ecell,
+                                                            const int* __restrict__ ecell_src,
+                                                            const int* __restrict__ recv_cnt,
+                                                            int* __restrict__ ecount, int* __restrict__ ebegin) {
+    __shared__ int sh[33];
+    scan_single_block(ocount, n_ocell, obegin, sh);
+    for (int ec = threadIdx.x; ec < n_ecell; ec += blockDim.x) {
+        const int src = ecell_src[ec];
+        ecount[ec] = src >= 0 ? ocount[src] : recv_cnt[-src - 1];
+    }
+    __syncthreads();   // the block's ecount writes are visible to the whole block
+    scan_single_block(ecount, n_ecell, ebegin, sh);
+}
+
 __global__ void __launch_bounds__(1024) k_scan_single(const int* __restrict__ in, int n, int* __restrict__ out) {
     __shared__ int sh[33];
     const int per = (n + 1023) / 1024;
@@ -406,7 +440,8 @@ __global__ void k_wrap_bin(int n_own, const double4* __restrict__ x, const int* 
                            Geo g, double4* __restrict__ xw, int* __restrict__ ocount,
                            int* __restrict__ cell_of, int* __restrict__ rank_in,
                            const int* __restrict__ gid, DevFlags* fl, const double* __restrict__ v,
-                           double* __restrict__ vcopy, int* __restrict__ gcopy, int cap) {
+                           double* __restrict__ vcopy, int* __restrict__ gcopy, int cap, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_own) return;
     if (vcopy) {
@@ -455,7 +490,8 @@ __global__ void k_ext_counts(int n_ecell, const int* __restrict__ ocount, Geo g,
 }
 
 __global__ void k_scatter(int n_own, const int* __restrict__ cell_of, const int* __restrict__ rank_in,
-                          const int* __restrict__ obegin, int* __restrict__ perm) {
+                          const int* __restrict__ obegin, int* __restrict__ perm, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_own) return;
     perm[obegin[cell_of[t]] + rank_in[t]] = t;
@@ -475,7 +511,8 @@ __global__ void k_cell_sort(int n_ocell, Geo g, const int* __restrict__ obegin,
                             double* __restrict__ vz_n, int* __restrict__ gid_new,
                             int* __restrict__ own_slot, int* __restrict__ ocell_of,
                             int* __restrict__ slot_gid, double4* __restrict__ xbuild,
-                            double* __restrict__ xp_new, DevFlags* fl) {
+                            double* __restrict__ xp_new, DevFlags* fl, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= n_ocell) return;
@@ -558,7 +595,9 @@ __global__ void k_ghost_refresh(GhostCells gc, const int* __restrict__ ebegin,
                                 const int* __restrict__ ecount, Geo g, double4* __restrict__ x,
                                 float4* __restrict__ xf, int* __restrict__ slot_gid,
                                 const int* __restrict__ recv_cnt, const int* __restrict__ recv_off,
-                                int n_slots, int4* __restrict__ gflat, double* __restrict__ xp, DevFlags* fl) {
+                                int n_slots, int4* __restrict__ gflat, double* __restrict__ xp, DevFlags* fl,
+                                const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int lane = threadIdx.x & 31;
     if (warp >= gc.n) return;
@@ -649,7 +688,8 @@ __global__ void k_xp_from_x(int b0, int n0, int b1, int n1, const double4* __res
     st_packed(xp, sl, ld256(x + sl));
 }
 
-__global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __restrict__ slot2t) {
+__global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __restrict__ slot2t, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < n_own) slot2t[own_slot[t]] = t;
 }
@@ -660,7 +700,8 @@ __global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __res
 template <bool FILL>
 __global__ void k_img_build(int n, const int4* __restrict__ gflat, int n_slots, const int* __restrict__ slot2t,
                             int* __restrict__ cnt, const int* __restrict__ off, int2* __restrict__ img,
-                            int4* __restrict__ grecv, DevFlags* fl, const int* n_dev) {
+                            int4* __restrict__ grecv, DevFlags* fl, const int* n_dev, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (n_dev) n = *n_dev;
     if (i >= n) return;
@@ -855,7 +896,8 @@ struct TileRows {
 };
 
 __global__ void k_tile_rows(int n_tiles, Geo g, const int* __restrict__ ebegin,
-                            const int* __restrict__ ecount, TileRows tr, DevFlags* fl) {
+                            const int* __restrict__ ecount, TileRows tr, DevFlags* fl, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     const int tile = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (tile >= n_tiles) return;
@@ -928,6 +970,7 @@ struct NlistArgs {
     int stage_cap;       // staged records per tile the dynamic shared memory is sized for
     int parts;           // CTAs per tile (small systems)
     int* own_li;         // out: each owned particle's index in its tile's staged halo
+    const DevCtl* ctl;   // captured rebuild: skip after a failed capacity check
 };
 
 // One CTA per force tile (the same halo rows and local numbering as k_force).
@@ -981,6 +1024,7 @@ template <bool SMALL>
 __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(NlistArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ BuildSmem S;
+    if (a.ctl && a.ctl->abort) return;
     // a.parts CTAs per tile on small systems (each stages the whole halo, takes a share of
     // the particles): enough CTAs for the chip where tiles are few
     const int tile = blockIdx.x / a.parts, part = blockIdx.x % a.parts;
@@ -1309,7 +1353,8 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
                                                        const int* __restrict__ ocell_of,
                                                        const int* __restrict__ obegin,
                                                        const int* __restrict__ tile_oc0,
-                                                       uint4* __restrict__ out) {
+                                                       uint4* __restrict__ out, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     extern __shared__ unsigned rr_smem[];
     const int tid = threadIdx.x;
     const int t = blockIdx.x * kRrThreads + tid;
@@ -1411,7 +1456,8 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
                                                        const int* __restrict__ ocell_of,
                                                        const int* __restrict__ obegin,
                                                        const int* __restrict__ tile_oc0,
-                                                       uint4* __restrict__ out) {
+                                                       uint4* __restrict__ out, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     extern __shared__ unsigned rr_smem[];
     const int tid = threadIdx.x;
     const int t = blockIdx.x * kRrThreads + tid;
@@ -2166,11 +2212,44 @@ struct DevStats {                  // persistent device counters (not reset by k
     double max_disp2;              // largest such value seen since init / set_state
 };
 
+// captured rebuilds: k_maxdisp also clears the owned-cell counts for the binning (one
+// memset node fewer)
+__global__ void k_maxdisp_z(int n_own, const double4* __restrict__ xprev, const int* __restrict__ own_slot,
+                            const double4* __restrict__ xbuild, unsigned long long* __restrict__ out,
+                            int* __restrict__ ocount, int n_ocell, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int i = t; i < n_ocell; i += gridDim.x * blockDim.x) ocount[i] = 0;
+    unsigned long long bits = 0ull;
+    if (t < n_own) {
+        const double4 p = xprev[own_slot[t]];
+        const double4 q = xbuild[t];
+        bits = __double_as_longlong(r2_canon(p.x - q.x, p.y - q.y, p.z - q.z));
+    }
+    block_atomic_max(bits, out);
+}
+
 __global__ void k_dangerous(DevStats* st, double delta2) {
     const double m2 = __longlong_as_double((long long)st->disp_bits);
     if (4.0 * m2 > delta2) st->dangerous += 1ull;
     if (m2 > st->max_disp2) st->max_disp2 = m2;
     st->disp_bits = 0ull;
+}
+
+// captured rebuilds: k_dangerous and k_reset_flags(keep_errors = 1) in one launch
+__global__ void k_dangerous_reset(DevStats* st, double delta2, DevFlags* fl, const DevCtl* ctl) {
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
+    const double m2 = __longlong_as_double((long long)st->disp_bits);
+    if (4.0 * m2 > delta2) st->dangerous += 1ull;
+    if (m2 > st->max_disp2) st->max_disp2 = m2;
+    st->disp_bits = 0ull;
+    DevFlags f;
+    memset(&f, 0, sizeof f);
+    f.migrate_gid = fl->migrate_gid;
+    f.nonfinite_gid = fl->nonfinite_gid;
+    f.overlap_pair = fl->overlap_pair;
+    f.val_error = fl->val_error;
+    *fl = f;
 }
 
 // Validation mode (ljmd_options.validate; single rank): for every step, the number of

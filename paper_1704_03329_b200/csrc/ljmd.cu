@@ -340,6 +340,9 @@ ljmd_status dalloc(ljmd_ctx* c, T** p, size_t n) {
 
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
+// the control a captured rebuild's kernels check (skip after a failed capacity check)
+inline const DevCtl* cctl(const ljmd_ctx* c) { return c->capturing ? c->d_ctl : nullptr; }
+
 // exclusive scan of n ints: out[0..n) prefixes, out[n] = total
 ljmd_status scan(ljmd_ctx* c, const int* in, int n, int* out) {
     if (n <= kScanSingle) {
@@ -358,6 +361,21 @@ ljmd_status scan(ljmd_ctx* c, const int* in, int n, int* out) {
     c->kernel_launches += 2;
     CKL();
     return LJMD_OK;
+}
+
+// the binning's cell offsets: owned-cell begin (scan of ocount), extended-cell counts and begin
+ljmd_status bin_offsets(ljmd_ctx* c) {
+    if (c->n_ocell <= kScanSingle && c->n_ecell <= kScanSingle) {   // small systems: one launch
+        k_bin_offsets_single<<<1, 1024, 0, c->stream>>>(c->ocount, c->n_ocell, c->obegin, c->n_ecell, c->ecell_src,
+                                                       c->recv_cnt, c->ecount, c->ebegin);
+        CKL();
+        return LJMD_OK;
+    }
+    TRY(scan(c, c->ocount, c->n_ocell, c->obegin));
+    k_ext_counts<<<nblk(c->n_ecell, 256), 256, 0, c->stream>>>(c->n_ecell, c->ocount, c->geo, c->ecell_src,
+                                                              c->recv_cnt, c->ecount);
+    CKL();
+    return scan(c, c->ecount, c->n_ecell, c->ebegin);
 }
 
 // device -> mapped host memory by a kernel (no copy engine); complete after a stream sync
@@ -599,6 +617,7 @@ int small_build_mode() {
 
 ljmd_status launch_nlist(ljmd_ctx* c) {
     NlistArgs a;
+    a.ctl = cctl(c);
     a.g = c->geo;
     a.x = c->x[c->xc];
     a.xf = c->xf;
@@ -1078,7 +1097,7 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
     if (at_build)
         k_ghost_refresh<true><<<blocks, 256, 0, c->stream>>>(gc, c->ebegin, c->ecount, c->geo, c->x[c->xc],
                                                              c->xf, c->slot_gid, c->recv_cnt, c->recv_off,
-                                                             c->n_slots, c->gflat, c->xp[c->xc], c->d_fl);
+                                                             c->n_slots, c->gflat, c->xp[c->xc], c->d_fl, cctl(c));
     else if (c->n_gflat > 0)
         k_ghost_flat<<<nblk(c->n_gflat, 256), 256, 0, c->stream>>>(c->n_gflat, c->gflat, c->geo, c->x[c->xc],
                                                                     c->xp[c->xc]);
@@ -1093,7 +1112,7 @@ ljmd_status build_images(ljmd_ctx* c) {
         CK(cudaMemsetAsync(c->img_off, 0, sizeof(int) * ((size_t)c->n_own + 1), c->stream));
         return LJMD_OK;
     }
-    k_slot2t<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->own_slot, c->slot2t);
+    k_slot2t<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->own_slot, c->slot2t, cctl(c));
     CKL();
     CK(cudaMemsetAsync(c->img_cnt, 0, sizeof(int) * (size_t)c->n_own, c->stream));
     // captured: the ghost count is only known on the device (grid over the slot capacity)
@@ -1101,11 +1120,11 @@ ljmd_status build_images(ljmd_ctx* c) {
     const int* ndev = c->capturing ? &c->d_fl->n_gflat : nullptr;
     const int nsl = c->capturing ? INT_MAX : c->n_slots;   // single rank: every source is local
     k_img_build<false><<<nblk(ng, 256), 256, 0, c->stream>>>(ng, c->gflat, nsl, c->slot2t, c->img_cnt, c->img_off,
-                                                             c->img, c->grecv, c->d_fl, ndev);
+                                                             c->img, c->grecv, c->d_fl, ndev, cctl(c));
     CKL();
     TRY(scan(c, c->img_cnt, c->n_own, c->img_off));
     k_img_build<true><<<nblk(ng, 256), 256, 0, c->stream>>>(ng, c->gflat, nsl, c->slot2t, c->img_cnt, c->img_off,
-                                                            c->img, c->grecv, c->d_fl, ndev);
+                                                            c->img, c->grecv, c->d_fl, ndev, cctl(c));
     CKL();
     return LJMD_OK;
 }
@@ -1205,7 +1224,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     double* vcopy = c->split ? nullptr : c->v[1];
     int* gcopy = c->split ? nullptr : c->gid[1];
     k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, xin, slot_in, c->geo, c->xw, c->ocount, c->cell_of,
-                                                    c->rank_in, gid_old, c->d_fl, vo, vcopy, gcopy, (int)oc);
+                                                    c->rank_in, gid_old, c->d_fl, vo, vcopy, gcopy, (int)oc, nullptr);
     CKL();
     if (!c->split) {
         vo = c->v[1];
@@ -1224,11 +1243,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
         CK(cudaMemcpyAsync(c->h_tot + 2, c->recv_off + npc, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(c->h_tot + 3, c->recv_off + 2 * npc, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     }
-    TRY(scan(c, c->ocount, c->n_ocell, c->obegin));
-    k_ext_counts<<<nblk(c->n_ecell, 256), 256, 0, c->stream>>>(c->n_ecell, c->ocount, c->geo, c->ecell_src,
-                                                              c->recv_cnt, c->ecount);
-    CKL();
-    TRY(scan(c, c->ecount, c->n_ecell, c->ebegin));
+    TRY(bin_offsets(c));
     TRY(to_host(c, c->h_slots, c->ebegin + c->n_ecell, sizeof(int)));
     TRY(sync_flags(c));
     if (c->h_fl->nonfinite_gid != INT_MAX)
@@ -1254,7 +1269,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
         ++c->regrows;
     }
     c->n_slots = need;
-    k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm);
+    k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm, cctl(c));
     CKL();
     // in place: the new layout goes into the current buffers (positions from xw, velocities
     // and gids from the copies), so no buffer pointer changes at a rebuild
@@ -1264,7 +1279,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
         c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, gid_old, c->xw, vo, vo + oc, vo + 2 * oc,
         xn, c->xf, vn, vn + oc, vn + 2 * oc, c->gid[0], c->own_slot, c->ocell_of, c->slot_gid,
-        c->xbuild, c->xp[c->xc], c->d_fl);
+        c->xbuild, c->xp[c->xc], c->d_fl, cctl(c));
     CKL();
     TRY(dsl_after_sort(c));
     if (c->split) {   // ghost planes: positions + gids of the neighbours' boundary planes
@@ -1282,7 +1297,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     TRY(refresh_ghosts(c, true));
     if (c->split) TRY(send_map(c));
     k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
-        c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl);
+        c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl, cctl(c));
     CKL();
     TRY(sync_flags(c));
     c->max_staged = c->h_fl->max_staged;
@@ -1341,7 +1356,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
         CKL();
     } else if (c->use_rr) {
         k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
-            c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b);
+            c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b, cctl(c));
         CKL();
     }
 
@@ -1462,67 +1477,53 @@ ljmd_status cond_if(ljmd_ctx* c, cudaStream_t body, Setter setter, Body fn) {
 // The rebuild of one step inside a captured sequence (single rank): the eager rebuild's
 // kernels without its host synchronisations, capacities checked on the device in three
 // stages (slots before anything is permuted; staging after the tile tables; list width
-// after the build), each gating the rest through a nested conditional node.
+// after the build); a failed check makes the rest return at entry.
 ljmd_status rebuild_captured(ljmd_ctx* c) {
     const int n = c->n_own;
     const size_t oc = c->own_cap;
-    k_maxdisp<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc ^ 1], c->own_slot, c->xbuild, &c->d_st->disp_bits);
+    k_maxdisp_z<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc ^ 1], c->own_slot, c->xbuild,
+                                                     &c->d_st->disp_bits, c->ocount, c->n_ocell, c->d_ctl);
     CKL();
-    k_dangerous<<<1, 1, 0, c->stream>>>(c->d_st, c->opt.delta * c->opt.delta);
+    k_dangerous_reset<<<1, 1, 0, c->stream>>>(c->d_st, c->opt.delta * c->opt.delta, c->d_fl, c->d_ctl);
     CKL();
-    TRY(reset_flags(c));
-    CK(cudaMemsetAsync(c->ocount, 0, sizeof(int) * c->n_ocell, c->stream));
     k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, c->geo, c->xw, c->ocount, c->cell_of,
                                                     c->rank_in, c->gid[0], c->d_fl, c->v[0], c->v[1], c->gid[1],
-                                                    (int)oc);
+                                                    (int)oc, c->d_ctl);
     CKL();
-    TRY(scan(c, c->ocount, c->n_ocell, c->obegin));
-    k_ext_counts<<<nblk(c->n_ecell, 256), 256, 0, c->stream>>>(c->n_ecell, c->ocount, c->geo, c->ecell_src,
-                                                              c->recv_cnt, c->ecount);
-    CKL();
-    TRY(scan(c, c->ecount, c->n_ecell, c->ebegin));
+    TRY(bin_offsets(c));
     DevCtl* ctl = c->d_ctl;
     DevFlags* fl = c->d_fl;
     const int* need = c->ebegin + c->n_ecell;
     const int slot_cap = c->slot_cap, stage_cap = c->stage_cap, K = c->K;
-    return cond_if(
-        c, c->cap_stream[1],
-        [&](cudaGraphConditionalHandle h) {
-            k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 1, h);
-        },
-        [&]() -> ljmd_status {
-            k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm);
-            CKL();
-            double* vo = c->v[1];
-            k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
-                c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, c->gid[1], c->xw, vo, vo + oc,
-                vo + 2 * oc, c->x[c->xc], c->xf, c->v[0], c->v[0] + oc, c->v[0] + 2 * oc, c->gid[0], c->own_slot,
-                c->ocell_of, c->slot_gid, c->xbuild, c->xp[c->xc], c->d_fl);
-            CKL();
-            TRY(refresh_ghosts(c, true));
-            k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
-                c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl);
-            CKL();
-            return cond_if(
-                c, c->cap_stream[2],
-                [&](cudaGraphConditionalHandle h) {
-                    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 2, h);
-                },
-                [&]() -> ljmd_status {
-                    TRY(build_images(c));
-                    TRY(launch_nlist(c));
-                    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 3,
-                                                         cudaGraphConditionalHandle{});
-                    CKL();
-                    if (c->use_rr) {
-                        k_list_rr<<<nblk(n, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
-                            n, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0,
-                            c->nbr8b);
-                        CKL();
-                    }
-                    return LJMD_OK;
-                });
-        });
+    // stage 1 before anything is permuted; a failed check makes every later kernel of the
+    // sequence return at entry (round 2: in-kernel checks instead of two nested conditional
+    // nodes, whose body launches cost ~4 us each on the device timeline)
+    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 1);
+    CKL();
+    k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm, cctl(c));
+    CKL();
+    double* vo = c->v[1];
+    k_cell_sort<<<nblk((int64_t)c->n_ocell * 32, 256), 256, 0, c->stream>>>(
+        c->n_ocell, c->geo, c->obegin, c->ocount, c->ebegin, c->perm, c->gid[1], c->xw, vo, vo + oc,
+        vo + 2 * oc, c->x[c->xc], c->xf, c->v[0], c->v[0] + oc, c->v[0] + 2 * oc, c->gid[0], c->own_slot,
+        c->ocell_of, c->slot_gid, c->xbuild, c->xp[c->xc], c->d_fl, cctl(c));
+    CKL();
+    TRY(refresh_ghosts(c, true));
+    k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
+        c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl, cctl(c));
+    CKL();
+    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 2);
+    CKL();
+    TRY(build_images(c));
+    TRY(launch_nlist(c));
+    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 3);
+    CKL();
+    if (c->use_rr) {
+        k_list_rr<<<nblk(n, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
+            n, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b, cctl(c));
+        CKL();
+    }
+    return LJMD_OK;
 }
 
 // The list order of the rebuilds of one ljmd_step call (eager and graph paths alike): the
@@ -2167,13 +2168,21 @@ ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) 
                     cond = forced = true;
                 }
             }
-            if (cond) {
+            if (forced) {
+                // the fixed schedule's rebuild: no conditional node (its kernels skip themselves
+                // after an abort), only the decision record; counted in the graph's launches
+                k_decide<<<1, 1, 0, c->stream>>>(c->d_ctl, c->d_fl, ns, 0, 1, delta2, c->d_rstep, (int)s,
+                                                cudaGraphConditionalHandle{}, 0);
+                CKL();
+                TRY(rebuild_captured(c));
+                c->pdl_ok = false;   // the force after the rebuild reads the new list
+            } else if (cond) {
                 const int64_t kb = c->kernel_launches;
                 TRY(cond_if(
                     c, c->cap_stream[0],
                     [&](cudaGraphConditionalHandle h) {
-                        k_decide<<<1, 1, 0, c->stream>>>(c->d_ctl, c->d_fl, ns, check ? 1 : 0, forced ? 1 : 0, delta2,
-                                                        c->d_rstep, (int)s, h);
+                        k_decide<<<1, 1, 0, c->stream>>>(c->d_ctl, c->d_fl, ns, check ? 1 : 0, 0, delta2,
+                                                        c->d_rstep, (int)s, h, 1);
                     },
                     [&]() { return rebuild_captured(c); }));
                 body_k = c->kernel_launches - kb - 1;
