@@ -1004,7 +1004,10 @@ constexpr int kBuildThreads = LJMD_BUILD_THREADS;
 constexpr int kBuildWinWords = LJMD_BUILD_FLAT ? 9 * LJMD_BUILD_THREADS : 0;   // per-thread windows
 constexpr int kTileCells = kTX * kTY * kTZ;
 constexpr int kSegW = kTX + 3;            // cell boundaries per halo row (ext x = 0 .. tx + 2)
-constexpr int kSub = 16;                  // x sub-bins per cell for the window lookup
+#ifndef LJMD_KSUB
+#define LJMD_KSUB 16
+#endif
+constexpr int kSub = LJMD_KSUB;           // x sub-bins per cell for the window lookup
 
 struct BuildSmem {
     int cell_t0[kTileCells + 1];          // first particle (tile-relative) of each owned cell
@@ -1722,6 +1725,12 @@ __device__ __forceinline__ FPart fpart_load(const ForceArgs& a, int t) {
 // register prefetch of one block ahead left the loop head waiting on the list load (the top
 // long_scoreboard stall of the kernel).  Slot d of thread q: ring + (d * kForceThreads + q)
 // * 16, so a warp's 32 slots are one contiguous 512-byte run (conflict-free LDS.128).
+#ifndef LJMD_PF_L2
+#define LJMD_PF_L2 0       // > 0: also an L2 prefetch this many blocks ahead
+#endif
+#ifndef LJMD_PF_DIST
+#define LJMD_PF_DIST 2     // list block prefetched into L1 this many blocks ahead
+#endif
 #ifndef LJMD_RING
 #define LJMD_RING 0        // 0: register prefetch of one block + L1 prefetch of the next (default)
 #endif
@@ -1791,7 +1800,11 @@ __device__ __forceinline__ void force_particle(const ForceArgs& a, const FPart& 
         // a short block is padded with the sentinel, so every entry is evaluated unpredicated
         uint4 nxt = make_uint4(0u, 0u, 0u, 0u);
         if (kRing == 0) {   // block b+2 into L1 now, block b+1 into registers
-            if (b + 2 < nblk) prefetch_l1(nb + (size_t)(b + 2) * stride);
+            if (b + LJMD_PF_DIST < nblk) prefetch_l1(nb + (size_t)(b + LJMD_PF_DIST) * stride);
+#if LJMD_PF_L2
+            if (b + LJMD_PF_L2 < nblk)
+                asm volatile("prefetch.global.L2 [%0];" :: "l"(nb + (size_t)(b + LJMD_PF_L2) * stride));
+#endif
             if (b + 1 < nblk) nxt = nb[(size_t)(b + 1) * stride];
 #if LJMD_LOADFENCE
             __syncwarp(__activemask());   // keeps ptxas from sinking the load to the loop end
