@@ -729,7 +729,6 @@ extern "C" ljmd_status ljmd_loop_execute(ljmd_ctx* c, int64_t loop) {
     std::memset(&p, 0, sizeof p);
     p.x = reinterpret_cast<const double*>(c->x[c->xc]);
     p.own_slot = c->own_slot;
-    TRY(ensure_build_list(c));
     p.nbr = reinterpret_cast<const unsigned short*>(c->nbr8);
     p.ncount = c->ncount;
     p.obegin = c->obegin;

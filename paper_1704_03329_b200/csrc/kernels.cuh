@@ -34,7 +34,7 @@ struct DevFlags {
     int val_error;               // validation: a listed in-range pair the fresh search missed
     int rr_ovf;                  // list build: a bank-aware overflow run exceeded kRrRun
     int halo_timeout;            // a boundary force tile waited too long for the halo
-    int max_rec;                 // most window records of one particle at the last build (masks)
+    int pad2;
     int max_staged;              // largest tile staging count at the last build
     int migrate_gid;             // a particle that moved further than one cell plane (INT_MAX: none)
     int overflow;     // analysis capacity exceeded (ljmd_cna)
@@ -147,11 +147,11 @@ __global__ void k_call_out(const DevCtl* __restrict__ ctl, const DevFlags* __res
 // count, stage 2 (after the tile tables) the staging size, stage 3 the list width
 // (the kernels after a failed check return at entry: cctl() in the launches)
 __global__ void k_check_caps(DevCtl* ctl, const DevFlags* fl, const int* need_slots, int slot_cap, int stage_cap,
-                             int K, int rmax, int stage) {
+                             int K, int stage) {
     bool ok = !ctl->abort;
     if (ok && stage == 1 && *need_slots > slot_cap) { ctl->abort = 1; ok = false; }
     if (ok && stage == 2 && fl->max_staged > stage_cap) { ctl->abort = 2; ok = false; }
-    if (ok && stage == 3 && (fl->max_nbr > K || fl->max_rec > rmax)) { ctl->abort = 2; ok = false; }
+    if (ok && stage == 3 && fl->max_nbr > K) { ctl->abort = 2; ok = false; }
     if (!ok && ctl->abort_step == 0) ctl->abort_step = ctl->step;
 }
 
@@ -971,13 +971,6 @@ struct NlistArgs {
     int parts;           // CTAs per tile (small systems)
     int* own_li;         // out: each owned particle's index in its tile's staged halo
     const DevCtl* ctl;   // captured rebuild: skip after a failed capacity check
-    // LJMD_BUILD_MASK: per particle up to rmax window records (first local index, 64-bit
-    // acceptance mask), [r * n_pad + t]; the u16 list is written from them by k_list_rr_m
-    // (bank-aware order) or k_decode_masks (build order)
-    unsigned short* rec_lo;
-    unsigned long long* rec_m;
-    int* nrec;
-    int rmax;
 };
 
 // One CTA per force tile (the same halo rows and local numbering as k_force).
@@ -1004,11 +997,6 @@ constexpr int kBuildThreads = LJMD_BUILD_THREADS;
 // one iteration ahead.  Same candidates, same order, same decisions: the list is unchanged.
 #ifndef LJMD_BUILD_FLAT
 #define LJMD_BUILD_FLAT 0
-#endif
-// Acceptance-mask build (large systems): records of (first index, 64-bit mask) per window
-// chunk instead of the u16 list; the list itself is written by the pass after the build
-#ifndef LJMD_BUILD_MASK
-#define LJMD_BUILD_MASK 0
 #endif
 #ifndef LJMD_BUILD_MINB
 #define LJMD_BUILD_MINB (LJMD_BUILD_FLAT ? 3 : 4)
@@ -1099,7 +1087,7 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
     const float thr_lo = a.thr_lo, thr_hi = a.thr_hi, slop = a.slop_f;
     const int K = a.K;
     unsigned long long kk = 0ull;
-    int kmax = 0, rmx = 0;
+    int kmax = 0;
     const int per = (m + a.parts - 1) / a.parts;
     const int q_end = min(m, (part + 1) * per);
     if (SMALL) {
@@ -1184,65 +1172,6 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
         const float ylo = a.ylo_f[cy], yhi = a.ylo_f[cy + 1];
         const float zlo = a.zlo_f[cz], zhi = a.zlo_f[cz + 1];
         const int t = t0 + q;
-#if LJMD_BUILD_MASK
-        {
-            // acceptance masks: a candidate costs its test and two predicated 64-bit ORs/shifts
-            // (no divergent accept path); the entries leave as (first index, mask) records per
-            // window chunk of <= 64 candidates, in stencil-row order -- the build order
-            int nrec = 0, k = 0;
-            for (int rz = 0; rz < 3; ++rz) {
-                const float ddz = rz == 0 ? fi.z - zlo : (rz == 2 ? zhi - fi.z : 0.f);
-                const float dz2 = fmaxf(ddz - slop, 0.f) * fmaxf(ddz - slop, 0.f);
-                for (int ry = 0; ry < 3; ++ry) {
-                    const float ddy = ry == 0 ? fi.y - ylo : (ry == 2 ? yhi - fi.y : 0.f);
-                    const float dyz2 = fmaf(fmaxf(ddy - slop, 0.f), fmaxf(ddy - slop, 0.f), dz2);
-                    if (dyz2 >= thr_hi) continue;
-                    const float xw = sqrtf(thr_hi - dyz2) + slop;
-                    const int R = (lz + rz) * (T.ty + 2) + (ly + ry);
-                    const float xl = fi.x - xw, xh = fi.x + xw;
-                    const int g0 = kSub * lx, g1 = kSub * (lx + 3);
-                    int gl = (int)floorf((xl - x0f) * inv_wsub) - 1;
-                    int gh = (int)floorf((xh - x0f) * inv_wsub) + 2;
-                    gl = min(max(gl, g0), g1);
-                    gh = min(max(gh, g0), g1);
-                    const int cl = min(gl / kSub, lx + 2), ch = min(gh / kSub, lx + 2);
-                    const int lo = S.sub[R][cl][gl - kSub * cl];
-                    const int hi = S.sub[R][ch][gh - kSub * ch];
-                    for (int c0 = lo; c0 < hi; c0 += 64) {
-                        const int c1 = min(hi, c0 + 64);
-                        unsigned long long m = 0ull, bit = 1ull;
-                        for (int jl = c0; jl < c1; ++jl, bit <<= 1) {
-                            const float4 fj = sF[jl];
-                            const float fx = fi.x - fj.x, fy = fi.y - fj.y, fz = fi.z - fj.z;
-                            const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-                            bool take = r2f < thr_lo;
-                            if (!take && r2f < thr_hi) {   // rare: the canonical fp64 test (the oracle's)
-                                const double4 xi = a.x[li + S.delta[R0]];
-                                const double4 xj = a.x[jl + S.delta[R]];
-                                take = r2_canon(xi.x - xj.x, xi.y - xj.y, xi.z - xj.z) < a.rn2;
-                            }
-                            m |= take ? bit : 0ull;
-                        }
-                        if (li >= c0 && li < c1) m &= ~(1ull << (li - c0));   // R4 self exclusion
-                        if (m) {
-                            if (nrec < a.rmax) {
-                                a.rec_m[(size_t)nrec * a.n_pad + t] = m;
-                                a.rec_lo[(size_t)nrec * a.n_pad + t] = (unsigned short)c0;
-                            }
-                            ++nrec;
-                            k += __popcll(m);
-                        }
-                    }
-                }
-            }
-            a.nrec[t] = nrec;
-            a.ncount[t] = k;
-            kmax = max(kmax, k);
-            kk += (unsigned long long)k;
-            rmx = max(rmx, nrec);
-            continue;
-        }
-#endif
         uint4* outb = a.nbr8 + t;
         unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
         int k = 0;
@@ -1384,12 +1313,10 @@ __global__ void __launch_bounds__(kBuildThreads, LJMD_BUILD_MINB) k_build_nlist(
     for (int o = 16; o > 0; o >>= 1) {
         kk += __shfl_down_sync(0xffffffffu, kk, o);
         kmax = max(kmax, __shfl_down_sync(0xffffffffu, kmax, o));
-        rmx = max(rmx, __shfl_down_sync(0xffffffffu, rmx, o));
     }
     if (lane == 0 && kk) {
         atomicAdd(&a.fl->total_nbr, kk);
         atomicMax(&a.fl->max_nbr, kmax);
-        if (rmx) atomicMax(&a.fl->max_rec, rmx);
     }
 }
 
@@ -1613,181 +1540,6 @@ __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, in
 }
 
 #endif
-
-#if LJMD_BUILD_MASK && !LJMD_RR_LEAN
-#error "LJMD_BUILD_MASK needs the LJMD_RR_LEAN record layout"
-#endif
-// ------------------------------------------------------------ lists from the build's masks
-// (LJMD_BUILD_MASK) the u16 list from the (first index, 64-bit mask) window records, in the
-// build order: records in stencil-row order, set bits ascending -- the entries the
-// register-shift build wrote, in the same order.
-
-// Walks a particle's records entry by entry (one loop over the entries, not one per record:
-// the lanes of a warp hold different bit counts per record), the next record in flight
-struct RecWalk {
-    const unsigned short* __restrict__ lo_p;
-    const unsigned long long* __restrict__ m_p;
-    size_t stride;
-    int t, nr, r;
-    unsigned long long m, mn;
-    unsigned lo, lon;
-    __device__ __forceinline__ RecWalk(const unsigned short* lp, const unsigned long long* mp, size_t st, int t_,
-                                       int nr_)
-        : lo_p(lp), m_p(mp), stride(st), t(t_), nr(nr_), r(2) {
-        m = nr > 0 ? m_p[t] : 0ull;
-        lo = nr > 0 ? lo_p[t] : 0u;
-        mn = nr > 1 ? m_p[stride + t] : 0ull;
-        lon = nr > 1 ? lo_p[stride + t] : 0u;
-    }
-    __device__ __forceinline__ unsigned next() {   // stored records are non-empty
-        if (m == 0ull) {
-            m = mn;
-            lo = lon;
-            mn = r < nr ? m_p[(size_t)r * stride + t] : 0ull;
-            lon = r < nr ? lo_p[(size_t)r * stride + t] : 0u;
-            ++r;
-        }
-        const unsigned lw = (unsigned)m, hw = (unsigned)(m >> 32);
-        const unsigned b = lw ? (unsigned)(__ffs((int)lw) - 1) : 32u + (unsigned)(__ffs((int)hw) - 1);
-        m &= m - 1ull;
-        return lo + b;
-    }
-};
-
-// the tile's sentinel local index (list padding: a far-away staged record)
-__device__ __forceinline__ unsigned tile_sentinel(const Geo& g, const int* __restrict__ ocell_of,
-                                                  const int* __restrict__ tr_off, int t, int* tile_out) {
-    int cx, cy, cz;
-    lex_xyz(g, g.lex_of_oc[ocell_of[t]], cx, cy, cz);
-    const int tile = tile_of_cell(g, cx, cy, cz);
-    if (tile_out) *tile_out = tile;
-    return (unsigned)tr_off[tile * (kRowsMax + 1) + tile_geo(g, tile).R];
-}
-
-// build order (lists not re-sequenced: the displacement-checked policy's short-lived lists,
-// the Newton-3 half list's input)
-__global__ void __launch_bounds__(256) k_decode_masks(int n_own, int n_pad, int K, Geo g,
-                                                      const unsigned short* __restrict__ rec_lo,
-                                                      const unsigned long long* __restrict__ rec_m,
-                                                      const int* __restrict__ nrec, const int* __restrict__ ncount,
-                                                      const int* __restrict__ ocell_of,
-                                                      const int* __restrict__ tr_off, uint4* __restrict__ out,
-                                                      const DevCtl* ctl) {
-    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_own) return;
-    const size_t stride = (size_t)n_pad;
-    const int n = min(ncount[t], K);
-    unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
-    uint4* o = out + t;
-    int k = 0;
-    auto emit = [&](unsigned l) {
-        w0 = __funnelshift_r(w0, w1, 16);
-        w1 = __funnelshift_r(w1, w2, 16);
-        w2 = __funnelshift_r(w2, w3, 16);
-        w3 = __funnelshift_r(w3, l, 16);
-        if ((k & 7) == 7) {
-            *o = make_uint4(w0, w1, w2, w3);
-            o += stride;
-        }
-        ++k;
-    };
-    RecWalk w(rec_lo, rec_m, stride, t, nrec[t]);
-    while (k < n) emit(w.next());
-    if (k & 7) {
-        const unsigned sen = tile_sentinel(g, ocell_of, tr_off, t, nullptr);
-        while (k & 7) emit(sen);
-    }
-}
-
-// bank-aware order (k_list_rr's greedy walk) straight from the records: the filing pass
-// decodes the masks instead of reading the u16 list; the same output as k_list_rr on the
-// register-shift build's list
-__global__ void __launch_bounds__(kRrThreads) k_list_rr_m(int n_own, int n_pad, int K, Geo g,
-                                                         const unsigned short* __restrict__ rec_lo,
-                                                         const unsigned long long* __restrict__ rec_m,
-                                                         const int* __restrict__ nrec,
-                                                         const int* __restrict__ ncount,
-                                                         const int* __restrict__ ocell_of,
-                                                         const int* __restrict__ obegin,
-                                                         const int* __restrict__ tile_oc0,
-                                                         const int* __restrict__ tr_off,
-                                                         uint4* __restrict__ out, const DevCtl* ctl) {
-    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
-    extern __shared__ unsigned rr_smem[];
-    const int tid = threadIdx.x;
-    const int t = blockIdx.x * kRrThreads + tid;
-    unsigned* rec = rr_smem + (size_t)tid * kRrStrideW;
-    unsigned short* bkt = reinterpret_cast<unsigned short*>(rec);
-    unsigned short* ovf = bkt + 16 * kRrCap;
-    constexpr int kCw = (16 * kRrCap + kRrOvf) / 2;   // first counter word
-    unsigned char* C = reinterpret_cast<unsigned char*>(rec + kCw);
-    unsigned char* U = C + 16;
-    if (t >= n_own) return;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) rec[kCw + w] = 0u;
-    const int n = min(ncount[t], K);
-    const int nb = (n + 7) >> 3;
-    const size_t stride = (size_t)n_pad;
-    int tile;
-    const unsigned pad = tile_sentinel(g, ocell_of, tr_off, t, &tile);
-    const int off = (t - obegin[tile_oc0[tile]]) & 15;
-    int novf = 0;
-    bool overflow = false;
-    auto file = [&](unsigned short l) {
-        const int r = l & 15;
-        const int c = C[r];
-        const bool ok = c < kRrCap;
-        unsigned short* dst = ok ? bkt + r * kRrCap + c : ovf + min(novf, kRrOvf - 1);
-        *dst = l;
-        C[r] = (unsigned char)(c + (ok ? 1 : 0));
-        overflow |= !ok && novf >= kRrOvf;
-        novf += ok ? 0 : 1;
-    };
-    const int nr = nrec[t];
-    {
-        RecWalk w(rec_lo, rec_m, stride, t, nr);
-        for (int q = 0; q < n; ++q) file((unsigned short)w.next());
-    }
-    unsigned w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;   // 8 pending entries, shifted in from the top
-    uint4* o = out + t;
-    int k = 0;
-    auto emit = [&](unsigned l) {
-        w0 = __funnelshift_r(w0, w1, 16);
-        w1 = __funnelshift_r(w1, w2, 16);
-        w2 = __funnelshift_r(w2, w3, 16);
-        w3 = __funnelshift_r(w3, l, 16);
-        if ((k & 7) == 7) {
-            *o = make_uint4(w0, w1, w2, w3);
-            o += stride;
-        }
-        ++k;
-    };
-    if (overflow) {   // a residue beyond bucket + overflow room: this particle keeps build order
-        RecWalk w(rec_lo, rec_m, stride, t, nr);
-        while (k < n) emit(w.next());
-        while (k < nb * 8) emit(pad);
-        return;
-    }
-    unsigned avail = 0u;
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-        if (C[r]) avail |= 1u << r;
-    const int nin = n - novf;
-    unsigned av2 = avail | (avail << 16);   // bit r and r + 16: a rotation is one shift
-    int tgt = off;                          // (off + k) mod 16
-    for (int q = 0; q < nin; ++q) {         // the greedy walk over the residues
-        const int rr = (tgt + __ffs(av2 >> tgt) - 1) & 15;
-        tgt = (tgt + 1) & 15;
-        const int u = U[rr];
-        const unsigned l = bkt[rr * kRrCap + u];
-        U[rr] = (unsigned char)(u + 1);
-        av2 &= u + 1 == (int)C[rr] ? ~(0x10001u << rr) : 0xffffffffu;
-        emit(l);
-    }
-    for (int q = 0; q < novf; ++q) emit(ovf[q]);   // overflow entries, build order
-    while (k < nb * 8) emit(pad);                  // the last block's sentinel padding
-}
 
 // --------------------------------------------------------------------------- force
 // LJ force over the full (both-orders) list, written only to i: no atomics.

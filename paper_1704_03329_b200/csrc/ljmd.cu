@@ -119,13 +119,7 @@ struct ljmd_ctx {
     double interval_ema = 0.0;        // steps a list has served, running estimate
     int64_t last_build_step = -1;     // steps_done at the last rebuild (-1: none yet)
     bool newton3 = false;             // half list + reaction reductions (NEXT-1)
-    uint4* nbr8h = nullptr;
-    // acceptance-mask build (LJMD_BUILD_MASK, large systems): window records [rmax][n_pad]
-    unsigned short* rec_lo = nullptr;
-    unsigned long long* rec_m = nullptr;
-    int* nrec = nullptr;
-    int rmax = 0;
-    int64_t list_gen = 0, blist_gen = -1;   // list builds so far; the build whose records nbr8 holds           // half list (newton3), blocked like nbr8
+    uint4* nbr8h = nullptr;           // half list (newton3), blocked like nbr8
     int* ncount_h = nullptr;
     int* slot_t = nullptr;            // slot -> owned index (newton3)
     int* tmap = nullptr;              // gid -> owned index (newton3, DSL)
@@ -599,14 +593,6 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
     return LJMD_OK;
 }
 
-ljmd_status alloc_recs(ljmd_ctx* c, int R) {
-    c->rmax = R;
-    TRY(dalloc(c, &c->rec_lo, (size_t)R * c->n_pad));
-    TRY(dalloc(c, &c->rec_m, (size_t)R * c->n_pad));
-    if (!c->nrec) TRY(dalloc(c, &c->nrec, (size_t)c->n_pad));
-    return LJMD_OK;
-}
-
 ljmd_status alloc_list(ljmd_ctx* c, int K) {
     c->K = K;
     TRY(dalloc(c, &c->nbr8, (size_t)(K / 8) * c->n_pad));
@@ -629,15 +615,7 @@ int small_build_mode() {
     return m;
 }
 
-bool small_build(const ljmd_ctx* c) {
-    return (c->fparts > 1 && small_build_mode() == 1) || small_build_mode() == 2;   // a warp per particle
-}
-
-// the build writes window records, the list comes from k_list_rr_m / k_decode_masks
-bool mask_build(const ljmd_ctx* c) { return LJMD_BUILD_MASK && !small_build(c); }
-
 ljmd_status launch_nlist(ljmd_ctx* c) {
-    if (mask_build(c) && c->rmax == 0) TRY(alloc_recs(c, 16));   // ~9 windows of <= 64 candidates
     NlistArgs a;
     a.ctl = cctl(c);
     a.g = c->geo;
@@ -681,11 +659,7 @@ ljmd_status launch_nlist(ljmd_ctx* c) {
     a.stage_cap = c->stage_cap;
     a.parts = c->fparts;
     a.own_li = c->own_li;   // the force kernel's CTAs per tile (1 on large systems)
-    a.rec_lo = c->rec_lo;
-    a.rec_m = c->rec_m;
-    a.nrec = c->nrec;
-    a.rmax = c->rmax;
-    if (small_build(c))   // small systems: a warp per particle
+    if ((c->fparts > 1 && small_build_mode() == 1) || small_build_mode() == 2)   // small systems: a warp per particle
         k_build_nlist<true><<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
     else
         k_build_nlist<false><<<c->n_tiles * c->fparts, kBuildThreads, build_smem(c), c->stream>>>(a);
@@ -1202,44 +1176,6 @@ ljmd_status migrate(ljmd_ctx* c) {
 
 // Cell binning (counting sort + gid order), ghost images and the Verlet list
 // (Sec. 3.4; IntegratorRange rebuild).
-// The u16 list(s) of a finished build: the bank-aware order into nbr8b (use_rr), else the
-// build order into nbr8 (register-shift builds wrote nbr8 themselves)
-ljmd_status write_lists(ljmd_ctx* c) {
-    const bool rr = c->use_rr && !c->newton3;
-    if (!mask_build(c)) {
-        if (rr) {
-            k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
-                c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b,
-                cctl(c));
-            CKL();
-        }
-        return LJMD_OK;
-    }
-    if (rr) {
-        k_list_rr_m<<<nblk(c->n_own, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
-            c->n_own, c->n_pad, c->K, c->geo, c->rec_lo, c->rec_m, c->nrec, c->ncount, c->ocell_of, c->obegin,
-            c->tile_oc0, c->tr_off, c->nbr8b, cctl(c));
-    } else {
-        k_decode_masks<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->n_pad, c->K, c->geo, c->rec_lo,
-                                                                    c->rec_m, c->nrec, c->ncount, c->ocell_of,
-                                                                    c->tr_off, c->nbr8, cctl(c));
-    }
-    CKL();
-    return LJMD_OK;
-}
-
-// nbr8 in build order for the on-demand readers (neighbour readback, BOA, CNA, DSL loops) when
-// the last build's list went only into nbr8b (bank-aware order, mask build)
-ljmd_status ensure_build_list(ljmd_ctx* c) {
-    if (!mask_build(c) || c->blist_gen == c->list_gen) return LJMD_OK;
-    k_decode_masks<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->n_pad, c->K, c->geo, c->rec_lo, c->rec_m,
-                                                                c->nrec, c->ncount, c->ocell_of, c->tr_off, c->nbr8,
-                                                                nullptr);
-    CKL();
-    c->blist_gen = c->list_gen;
-    return LJMD_OK;
-}
-
 ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     // Bank-aware re-ordering costs about 1.4 force launches and saves about 13 % of each
     // launch it serves (C2: 225 us against 21 us per step), so it pays for lists that serve
@@ -1398,9 +1334,9 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     if (c->h_fl->overlap_pair != ~0ull)
         return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)",
                        (int)(c->h_fl->overlap_pair >> 32), (int)(c->h_fl->overlap_pair & 0xffffffffu));
-    if (c->h_fl->max_nbr > c->K || (mask_build(c) && c->h_fl->max_rec > c->rmax)) {
-        if (c->h_fl->max_nbr > c->K) TRY(alloc_list(c, (c->h_fl->max_nbr * 5 / 4 + 8) / 8 * 8));
-        if (mask_build(c) && c->h_fl->max_rec > c->rmax) TRY(alloc_recs(c, c->h_fl->max_rec + 4));
+    if (c->h_fl->max_nbr > c->K) {
+        int K = (c->h_fl->max_nbr * 5 / 4 + 8) / 8 * 8;
+        TRY(alloc_list(c, K));
         ++c->regrows;
         TRY(reset_flags(c));
         TRY(launch_nlist(c));
@@ -1408,8 +1344,6 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     }
     c->max_nbr = c->h_fl->max_nbr;
     c->total_nbr = c->h_fl->total_nbr;
-    ++c->list_gen;
-    TRY(write_lists(c));
     if (c->newton3) {
         const int* g = c->gid[c->oc_cur];
         k_cna_tmap<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, g, c->tmap);
@@ -1420,7 +1354,12 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
                                                                  c->ocell_of, TileRows{c->tr_begin, c->tr_off, c->tr_len},
                                                                  c->slot_gid, g, c->nbr8h, c->ncount_h);
         CKL();
+    } else if (c->use_rr) {
+        k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
+            c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b, cctl(c));
+        CKL();
     }
+
     return LJMD_OK;
 }
 
@@ -1559,7 +1498,7 @@ ljmd_status rebuild_captured(ljmd_ctx* c) {
     // stage 1 before anything is permuted; a failed check makes every later kernel of the
     // sequence return at entry (round 2: in-kernel checks instead of two nested conditional
     // nodes, whose body launches cost ~4 us each on the device timeline)
-    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, INT_MAX, 1);
+    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 1);
     CKL();
     k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm, cctl(c));
     CKL();
@@ -1573,13 +1512,18 @@ ljmd_status rebuild_captured(ljmd_ctx* c) {
     k_tile_rows<<<nblk((int64_t)c->n_tiles * 32, 256), 256, 0, c->stream>>>(
         c->n_tiles, c->geo, c->ebegin, c->ecount, TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->d_fl, cctl(c));
     CKL();
-    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, INT_MAX, 2);
+    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 2);
     CKL();
     TRY(build_images(c));
     TRY(launch_nlist(c));
-    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, mask_build(c) ? c->rmax : INT_MAX, 3);
+    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 3);
     CKL();
-    return write_lists(c);
+    if (c->use_rr) {
+        k_list_rr<<<nblk(n, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
+            n, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b, cctl(c));
+        CKL();
+    }
+    return LJMD_OK;
 }
 
 // The list order of the rebuilds of one ljmd_step call (eager and graph paths alike): the
@@ -2013,7 +1957,6 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         // testing: every capacity exactly what this state needs, so that a later rebuild inside
         // a captured step sequence runs short and takes the abort / eager-resume path
         c->stage_cap = c->max_staged;
-        if (mask_build(c) && c->h_fl->max_rec > 0 && (s = alloc_recs(c, c->h_fl->max_rec)) != LJMD_OK) return fail(s);
         if ((s = alloc_list(c, std::max(8, (c->max_nbr + 7) / 8 * 8))) != LJMD_OK ||
             (s = alloc_slots(c, c->n_slots, false)) != LJMD_OK || (s = load_state(c, pos, vel)) != LJMD_OK)
             return fail(s);
@@ -2289,7 +2232,6 @@ ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pendi
     const CallOut o = *c->h_out[p.buf];
     const DevCtl& ctl = o.ctl;
     c->kernel_launches += p.launches + (int64_t)ctl.nreb * c->rebuild_kernels;
-    c->list_gen += ctl.nreb;
     for (int k = 0; k < ctl.nreb; ++k) {
         const int64_t st = p.step0 + c->h_orstep[p.buf][k];
         if (c->last_build_step >= 0 && st > c->last_build_step)
@@ -2591,7 +2533,6 @@ ljmd_status ljmd_get_neighbours(ljmd_ctx* c, int64_t* offsets, int64_t* gids, in
     TRY(dalloc(c, &d_off, n + 1));
     TRY(dalloc(c, &d_out, (size_t)std::max<long long>(toff[n], 1)));
     CK(cudaMemcpyAsync(d_off, toff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, c->stream));
-    TRY(ensure_build_list(c));
     k_list_gids<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->n_pad, c->geo, (const unsigned short*)c->nbr8,
                                                      c->ncount, c->ocell_of,
                                                      TileRows{c->tr_begin, c->tr_off, c->tr_len}, c->slot_gid, d_off, d_out);
@@ -2675,7 +2616,7 @@ void ljmd_destroy(ljmd_ctx* c) {
     void* ptrs[] = {c->x[0], c->x[1], c->xf, c->slot_gid, c->v[0], c->v[1], c->gid[0], c->gid[1],
                     c->own_slot, c->own_li, c->ocell_of, c->F, c->e, c->xbuild, c->xw, c->cell_of, c->rank_in, c->perm,
                     c->ocount, c->obegin, c->ecount, c->ebegin, c->ecell_src, c->gc_dst, c->gc_src, c->gc_shift,
-                    c->scan_tmp, c->nbr8, c->nbr8b, c->rec_lo, c->rec_m, c->nrec, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin, c->ylo_f, c->zlo_f,
+                    c->scan_tmp, c->nbr8, c->nbr8b, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin, c->ylo_f, c->zlo_f,
                     c->tr_off, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -2751,7 +2692,6 @@ extern "C" ljmd_status ljmd_boa(ljmd_ctx* c, int64_t ell, double rcut, double* Q
     if (rcut > c->rc)
         return set_err(c, LJMD_E_ARG, "ljmd_boa: rcut %g exceeds the force cutoff rc = %g (list validity)", rcut,
                        c->rc);
-    TRY(ensure_build_list(c));
     BoaArgs a;
     a.g = c->geo;
     a.x = c->x[c->xc];
@@ -2832,7 +2772,6 @@ extern "C" ljmd_status ljmd_cna(ljmd_ctx* c, double rcut, int32_t* cls, int32_t*
     TRY(dalloc(c, &dtrip, (size_t)n * kCnaMax));
     TRY(dalloc(c, &dcls, n));
     TRY(reset_flags(c));
-    TRY(ensure_build_list(c));
     CnaArgs a;
     a.g = c->geo;
     a.x = c->x[c->xc];
