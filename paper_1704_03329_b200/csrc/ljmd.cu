@@ -2229,6 +2229,10 @@ ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer);
 ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pending* next) {
     const int64_t ee = c->opt.energy_every;
     CK(cudaEventSynchronize(c->ev_call[p.buf]));
+    if (c->init_pending) {   // the init sequence ran before this call: its energies are in place
+        c->h_hist.insert(c->h_hist.begin(), c->h_init, c->h_init + 2);
+        c->init_pending = false;
+    }
     const CallOut o = *c->h_out[p.buf];
     const DevCtl& ctl = o.ctl;
     c->kernel_launches += p.launches + (int64_t)ctl.nreb * c->rebuild_kernels;
@@ -2386,7 +2390,7 @@ ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer) {
     // buffers a queued call uses are regrown only after it has been settled
     if (c->pend.on && (!defer || need_hist > c->hist_cap || nsteps > c->rstep_cap || nsteps > c->out_cap))
         TRY(settle(c));
-    TRY(settle_init(c));
+    if (!defer) TRY(settle_init(c));   // deferred: the init energies are read when this call settles
     TRY(ensure_hist(c, need_hist));
     c->call_nsamp = 0;
     const int64_t first_launch = c->force_launches;
