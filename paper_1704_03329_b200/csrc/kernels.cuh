@@ -50,6 +50,13 @@ struct DevFlags {
 // Small device->host results (flags, counts, energies) are written by a kernel into mapped
 // page-locked memory instead of a copy-engine transfer, so they never queue behind a bulk
 // host transfer of the copy stream (ljmd_get_positions_async / ljmd_stage_state).
+// device memory cleared by a kernel, not cudaMemsetAsync: a memset can queue behind bulk host
+// transfers on the copy engine (measured: tens of microseconds of compute-stream idle while
+// ljmd_stage_state / ljmd_get_positions_async copies run)
+__global__ void k_zero_words(unsigned* __restrict__ p, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = 0u;
+}
+
 __global__ void k_copy_words(const unsigned* __restrict__ src, unsigned* dst, int n) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }

@@ -378,6 +378,15 @@ ljmd_status bin_offsets(ljmd_ctx* c) {
     return scan(c, c->ecount, c->n_ecell, c->ebegin);
 }
 
+// zero `bytes` (a multiple of 4) of device memory on the engine's stream (k_zero_words)
+ljmd_status zero_async(ljmd_ctx* c, void* p, size_t bytes) {
+    const size_t n = bytes / 4;
+    const int blocks = (int)std::min<size_t>((n + 255) / 256, 1184);
+    k_zero_words<<<std::max(blocks, 1), 256, 0, c->stream>>>(static_cast<unsigned*>(p), n);
+    CKL();
+    return LJMD_OK;
+}
+
 // device -> mapped host memory by a kernel (no copy engine); complete after a stream sync
 ljmd_status to_host(ljmd_ctx* c, void* hmapped, const void* dsrc, size_t bytes) {
     k_copy_words<<<1, 256, 0, c->stream>>>(static_cast<const unsigned*>(dsrc), static_cast<unsigned*>(hmapped),
@@ -798,8 +807,8 @@ void vv_launch(ljmd_ctx* c, const VvArgs& v) {
 ljmd_status launch_half(ljmd_ctx* c, bool energy, int mode, bool check, cudaEvent_t e0, cudaEvent_t e1) {
     const size_t oc = c->own_cap;
     if (e0) CK(cudaEventRecord(e0, c->stream));
-    CK(cudaMemsetAsync(c->F, 0, sizeof(double) * 3 * oc, c->stream));
-    if (energy) CK(cudaMemsetAsync(c->e, 0, sizeof(double) * oc, c->stream));
+    TRY(zero_async(c, c->F, sizeof(double) * 3 * oc));
+    if (energy) TRY(zero_async(c, c->e, sizeof(double) * oc));
     const double s2 = c->sigma * c->sigma, s6 = s2 * s2 * s2, s12 = s6 * s6;
     HalfArgs h;
     h.g = c->geo;
@@ -1109,12 +1118,12 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
 // the list of received-plane images; from the build-time ghost list
 ljmd_status build_images(ljmd_ctx* c) {
     if (c->newton3 || (!c->capturing && c->n_gflat == 0)) {
-        CK(cudaMemsetAsync(c->img_off, 0, sizeof(int) * ((size_t)c->n_own + 1), c->stream));
+        TRY(zero_async(c, c->img_off, sizeof(int) * ((size_t)c->n_own + 1)));
         return LJMD_OK;
     }
     k_slot2t<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->own_slot, c->slot2t, cctl(c));
     CKL();
-    CK(cudaMemsetAsync(c->img_cnt, 0, sizeof(int) * (size_t)c->n_own, c->stream));
+    TRY(zero_async(c, c->img_cnt, sizeof(int) * (size_t)c->n_own));
     // captured: the ghost count is only known on the device (grid over the slot capacity)
     const int ng = c->capturing ? c->slot_cap : c->n_gflat;
     const int* ndev = c->capturing ? &c->d_fl->n_gflat : nullptr;
@@ -1203,7 +1212,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     c->last_build_step = c->steps_done;
     (void)kRrMinSteps;   // the list order is chosen per ljmd_step call (decide_list_order)
     TRY(reset_flags(c));
-    CK(cudaMemsetAsync(c->ocount, 0, sizeof(int) * c->n_ocell, c->stream));
+    TRY(zero_async(c, c->ocount, sizeof(int) * c->n_ocell));
     // input of the binning: the current owned particles, or the post-migration compaction
     const double4* xin = c->x[c->xc];
     const int* slot_in = c->own_slot;
@@ -1658,7 +1667,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const 
     c->h_hist.clear();
     c->h_val.clear();
     c->last_build_step = -1;
-    CK(cudaMemsetAsync(c->d_st, 0, sizeof(DevStats), c->stream));
+    TRY(zero_async(c, c->d_st, sizeof(DevStats)));
     decide_list_order(c);
     TRY(rebuild(c));
     TRY(ensure_hist(c, 1));
@@ -2043,7 +2052,7 @@ ljmd_status ljmd_wait_transfers(ljmd_ctx* c) {
 ljmd_status kick_drift(ljmd_ctx* c) {
     // Alg. alg:VelocityVerlet line 6 of the first step of a call (uses the stored F)
     const bool check = c->opt.rebuild_check != 0;
-    if (check) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
+    if (check) TRY(zero_async(c, &c->d_fl->maxdisp2, sizeof(unsigned long long)));
     double* v = c->v[c->oc_cur];
     const size_t oc = c->own_cap;
     const double h = 0.5 * c->dt / c->opt.mass;
@@ -2113,7 +2122,7 @@ ljmd_status step_eager(ljmd_ctx* c, int64_t s_first, int64_t nsteps, bool rebuil
         }
         const bool sample = ee > 0 && (c->steps_done % ee) == 0;
         const bool last = s == nsteps;
-        if (check && !last) CK(cudaMemsetAsync(&c->d_fl->maxdisp2, 0, sizeof(unsigned long long), c->stream));
+        if (check && !last) TRY(zero_async(c, &c->d_fl->maxdisp2, sizeof(unsigned long long)));
         if (c->opt.validate) TRY(validate_step(c, (int)(s - 1)));
         TRY(launch_force(c, sample, last ? kKick : kKKD, check && !last, halo_pending));
         if (last) c->energy_current = sample && ee > 0;
@@ -2286,7 +2295,7 @@ ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pendi
     c->since = 0;
     c->xc = p.xc0 ^ (int)((sa - 1) & 1);
     c->call_nsamp = ctl.nsamp;
-    CK(cudaMemsetAsync(c->d_ctl, 0, offsetof(DevCtl, since), c->stream));
+    TRY(zero_async(c, c->d_ctl, offsetof(DevCtl, since)));
     TRY(rebuild(c, /*danger=*/false));   // the dangerous-build test of this rebuild already ran
     TRY(step_eager(c, sa, p.nsteps, true));
     TRY(pull_hist(c, c->call_nsamp));    // the graph's samples and the eager steps'
