@@ -170,9 +170,7 @@ struct ljmd_ctx {
     // ---- graph mode (single rank): ljmd_step captured into CUDA graphs, rebuild decided and
     // capacity-checked on the device
     DevCtl* d_ctl = nullptr;
-    DevCtl* h_ctl = nullptr;          // mapped readback
     int* d_rstep = nullptr;           // rebuild steps of the current call (1-based within it)
-    int* h_rstep = nullptr;           // mapped readback
     int64_t rstep_cap = 0;
     int stage_cap = 0;                // staged particles per tile the force/build launches are sized for
     struct GraphEntry {
@@ -203,7 +201,6 @@ struct ljmd_ctx {
     int64_t out_cap = 0;
     int out_next = 0;
     cudaEvent_t ev_call[2] = {nullptr, nullptr};
-    int64_t deferred_calls = 0;
     int* h_slots = nullptr;        // pinned
     double* d_stage = nullptr;     // [3][own_cap] readback staging
     // overlapped host transfers (ljmd_stage_state / ljmd_get_positions_async)
@@ -1913,7 +1910,6 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
     if ((s = set_force_attrs(c)) != LJMD_OK) return fail(s);
     if (cudaMalloc(&c->d_fl, sizeof(DevFlags)) != cudaSuccess ||
         cudaMalloc(&c->d_ctl, sizeof(DevCtl)) != cudaSuccess ||
-        cudaHostAlloc(&c->h_ctl, sizeof(DevCtl), cudaHostAllocMapped) != cudaSuccess ||
         cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess ||
         cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostAlloc(&c->h_fl, sizeof(DevFlags), cudaHostAllocMapped) != cudaSuccess ||
@@ -2384,7 +2380,6 @@ ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer) {
     c->since = p.sim_since;
     c->xc = p.xc0 ^ (int)((nsteps - 1) & 1);
     c->energy_current = ee > 0 && (c->steps_done % ee) == 0;
-    ++c->deferred_calls;
     if (prev.on) TRY(settle_call(c, prev, &c->pend));
     return LJMD_OK;
 }
@@ -2649,8 +2644,6 @@ void ljmd_destroy(ljmd_ctx* c) {
     if (c->h_fl) cudaFreeHost(c->h_fl);
     if (c->h_st) cudaFreeHost(c->h_st);
     drop_graphs(c);
-    if (c->h_ctl) cudaFreeHost(c->h_ctl);
-    if (c->h_rstep) cudaFreeHost(c->h_rstep);
     for (int b = 0; b < 2; ++b) {
         if (c->h_out[b]) cudaFreeHost(c->h_out[b]);
         if (c->h_orstep[b]) cudaFreeHost(c->h_orstep[b]);
