@@ -117,6 +117,9 @@ struct ljmd_ctx {
     int bank_order = 1;               // 0: the force kernel walks the build order
     bool use_rr = false;              // the current list is in the bank-aware order
     double interval_ema = 0.0;        // steps a list has served, running estimate
+    int64_t ncalls = 0;               // ljmd_step calls so far
+    double ema_after[4] = {0, 0, 0, 0};   // interval_ema after call k (k mod 4): list order lags 2 calls
+    bool dev_since_ok = false;        // the device's step control holds the current since (graph calls)
     int64_t last_build_step = -1;     // steps_done at the last rebuild (-1: none yet)
     bool newton3 = false;             // half list + reaction reductions (NEXT-1)
     uint4* nbr8h = nullptr;           // half list (newton3), blocked like nbr8
@@ -190,7 +193,7 @@ struct ljmd_ctx {
     struct Pending {
         bool on = false;
         bool deferred = false;        // the host state was advanced at launch
-        int64_t step0 = 0, nsteps = 0, launches = 0;
+        int64_t step0 = 0, nsteps = 0, launches = 0, call = 0;
         int64_t sim_since = 0;        // fixed schedule: steps since the last rebuild at the end
         int xc0 = 0, buf = 0;
     };
@@ -1542,7 +1545,11 @@ ljmd_status rebuild_captured(ljmd_ctx* c) {
 // instructions (C1: 17.2 -> 16.7 us per MD step without it).
 void decide_list_order(ljmd_ctx* c) {
     if (c->interval_ema == 0.0) c->interval_ema = (double)c->opt.rebuild_every;
-    c->use_rr = c->bank_order && c->interval_ema >= 10.0 && c->fparts == 1;
+    // the estimate as of the end of call ncalls - 2: known before call ncalls is queued also
+    // while the call before it is unsettled (deferred settlement), so the eager, synchronous
+    // graph and deferred paths take the same decision
+    const double e = c->ncalls >= 2 ? c->ema_after[(c->ncalls - 2) & 3] : (double)c->opt.rebuild_every;
+    c->use_rr = c->bank_order && e >= 10.0 && c->fparts == 1;
 }
 
 // bookkeeping of one rebuild at MD step `step` (eager and graph paths)
@@ -1658,6 +1665,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const 
     c->init_pending = false;
     c->n_own = (int)n;
     c->since = 0;
+    c->dev_since_ok = false;
     c->steps_done = 0;
     c->n_rebuilds = 0;
     c->rebuild_steps.clear();
@@ -2067,6 +2075,7 @@ ljmd_status kick_drift(ljmd_ctx* c) {
 // Steps s_first .. n of a call on the eager path (host decides each rebuild).  rebuilt_first:
 // step s_first's drift and rebuild are already done (resumption after a graph abort).
 ljmd_status step_eager(ljmd_ctx* c, int64_t s_first, int64_t nsteps, bool rebuilt_first) {
+    c->dev_since_ok = false;   // the host decides these steps
     const bool check = c->opt.rebuild_check != 0;
     const int64_t ee = c->opt.energy_every;
     const double delta2 = c->opt.delta * c->opt.delta;
@@ -2229,7 +2238,7 @@ ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) 
 // Host side of a settled graph call p: rebuild bookkeeping, errors, energies; a capacity abort
 // resumes the call on the eager path.  next: a call queued after p (deferred), which ran as
 // no-ops if p aborted (k_call_begin) and is then re-run here.
-ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer);
+ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer, int64_t call = -1);
 
 ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pending* next) {
     const int64_t ee = c->opt.energy_every;
@@ -2265,9 +2274,11 @@ ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pendi
         if (!p.deferred) {   // else advanced at launch
             c->steps_done = p.step0 + p.nsteps;
             c->xc = p.xc0 ^ (int)((p.nsteps - 1) & 1);
-            c->since = c->opt.rebuild_check ? (int64_t)ctl.since : p.sim_since;
+            c->since = p.sim_since;
             c->energy_current = ee > 0 && (c->steps_done % ee) == 0;
         }
+        if (c->opt.rebuild_check) c->since = ctl.since;   // decided on the device
+        c->ema_after[p.call & 3] = c->interval_ema;
         // the current energies: from this call unless a later one is queued
         if (!(next && next->on) && ee > 0 && ((p.step0 + p.nsteps) % ee) == 0 && ctl.nsamp > 0) {
             c->cur_pe = c->h_ohist[p.buf][2 * ctl.nsamp - 2];
@@ -2299,7 +2310,8 @@ ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pendi
         c->cur_pe = c->h_hist[c->h_hist.size() - 2];
         c->cur_ke = c->h_hist[c->h_hist.size() - 1];
     }
-    if (skipped.on) TRY(step_call(c, skipped.nsteps, false));
+    c->ema_after[p.call & 3] = c->interval_ema;
+    if (skipped.on) TRY(step_call(c, skipped.nsteps, false, skipped.call));
     return LJMD_OK;
 }
 
@@ -2332,7 +2344,7 @@ static ljmd_status ensure_out(ljmd_ctx* c, int64_t n) {
     return LJMD_OK;
 }
 
-ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer) {
+ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer, int64_t call) {
     const bool check = c->opt.rebuild_check != 0;
     const int64_t ee = c->opt.energy_every;
     if (c->rstep_cap < nsteps) {
@@ -2357,11 +2369,13 @@ ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer) {
     p.xc0 = c->xc;
     p.launches = it->second.launches;
     p.buf = c->out_next;
+    p.call = call;
     c->out_next ^= 1;
-    if (check) {
+    if (check && !c->dev_since_ok) {   // after eager steps or a new state: the host's count
         k_set_since<<<1, 1, 0, c->stream>>>(c->d_ctl, (int)c->since);
         CKL();
     }
+    c->dev_since_ok = true;
     CK(cudaGraphLaunch(it->second.ex, c->stream));
     ++c->graph_calls;
     k_call_out<<<1, 256, 0, c->stream>>>(c->d_ctl, c->d_fl, c->ebegin + c->n_ecell, c->d_rstep, c->hist,
@@ -2372,25 +2386,28 @@ ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer) {
     for (int64_t s = 1; s <= nsteps; ++s)
         if (++p.sim_since >= c->opt.rebuild_every) p.sim_since = 0;
     if (!defer) return settle_call(c, p, nullptr);   // one host wait per call
-    // the fixed schedule is host-known: advance the state now, settle the previous call
+    // the step count, buffer parity and sample phase after the call are known in advance (the
+    // displacement-checked schedule's since is read at settlement): advance now, settle the
+    // previous call
     p.deferred = true;
     const ljmd_ctx::Pending prev = c->pend;
     c->pend = p;
     c->steps_done = p.step0 + nsteps;
-    c->since = p.sim_since;
+    if (!check) c->since = p.sim_since;
     c->xc = p.xc0 ^ (int)((nsteps - 1) & 1);
     c->energy_current = ee > 0 && (c->steps_done % ee) == 0;
     if (prev.on) TRY(settle_call(c, prev, &c->pend));
     return LJMD_OK;
 }
 
-// One ljmd_step call.  defer: graph mode under the fixed schedule returns once the call is
-// queued (LJMD_DEFER=0 turns that off).
-ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer) {
+// One ljmd_step call.  defer: graph mode returns once the call is queued (LJMD_DEFER=0 turns
+// that off).  call: the call's index (a call re-run after an abort keeps its own)
+ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer, int64_t call) {
+    if (call < 0) call = c->ncalls++;
     const int64_t ee = c->opt.energy_every;
     const int64_t need_hist = nsteps / std::max<int64_t>(ee, 1) + 2;
     const bool graph = graph_ok(c);
-    defer = defer && graph && c->opt.rebuild_check == 0;
+    defer = defer && graph;
     // buffers a queued call uses are regrown only after it has been settled
     if (c->pend.on && (!defer || need_hist > c->hist_cap || nsteps > c->rstep_cap || nsteps > c->out_cap))
         TRY(settle(c));
@@ -2409,7 +2426,7 @@ ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer) {
         CK(cudaMemsetAsync(c->vhist, 0, sizeof(int) * 2 * (size_t)nsteps, c->stream));
     }
     decide_list_order(c);
-    if (graph) return step_graph(c, nsteps, defer);   // settled there unless deferred
+    if (graph) return step_graph(c, nsteps, defer, call);   // settled there unless deferred
     TRY(kick_drift(c));
     TRY(step_eager(c, 1, nsteps, false));
     TRY(pull_hist(c, c->call_nsamp));
@@ -2417,6 +2434,7 @@ ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer) {
         c->cur_pe = c->h_hist[c->h_hist.size() - 2];
         c->cur_ke = c->h_hist[c->h_hist.size() - 1];
     }
+    c->ema_after[call & 3] = c->interval_ema;
     TRY(collect_profile(c, first_launch));
     TRY(sync_flags(c));
     if (c->h_fl->halo_timeout) return set_err(c, LJMD_E_NCCL, "a boundary force tile timed out waiting for the halo");

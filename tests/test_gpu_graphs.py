@@ -79,15 +79,19 @@ def test_graph_parity_with_oracle(eng, orc):
     np.testing.assert_allclose(ke, r.ke, rtol=1e-8)
 
 
-def test_deferred_settlement_equals_synchronous(eng, monkeypatch):
-    """Graph calls under the fixed schedule return once queued; the host settles a call after
-    queueing the next one (or at the next getter).  Against LJMD_DEFER=0 (one host wait per
-    call) and the eager path: the same trajectory, energies and rebuild steps bit for bit,
-    with getters interleaved between the calls."""
-    pos, vel, box = state()
-    calls = [20, 20, 20, 3, 17, 20, 40, 1]
+@pytest.mark.parametrize("check,cells", [(0, 8), (1, 8), (1, 32)])
+def test_deferred_settlement_equals_synchronous(eng, monkeypatch, check, cells):
+    """Graph calls return once queued; the host settles a call after queueing the next one
+    (or at the next getter).  Against LJMD_DEFER=0 (one host wait per call) and the eager
+    path: the same trajectory, energies and rebuild steps bit for bit, with getters
+    interleaved between the calls -- under both rebuild policies; 32^3 cells is large enough
+    for one force CTA per tile, where the displacement-checked policy's list order (bank-aware
+    or build order, from the rebuild intervals two calls back) changes between calls."""
+    pos, vel, box = state(cells=cells)
+    calls = [20, 20, 20, 3, 17, 20, 40, 1] if cells == 8 else [20, 20, 20, 7, 13, 20]
 
     def run_mixed(**kw):
+        kw["rebuild_check"] = check
         hist = []
         with eng.LJMD(pos, vel, box, **kw) as ctx:
             for k, n in enumerate(calls):
