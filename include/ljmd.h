@@ -180,7 +180,7 @@ ljmd_status ljmd_wait_transfers(ljmd_ctx* c);
  * F <- sum over the list of Eq. eqn:LJforce (INC_ZERO, R5); v += dt/(2m) F.
  * PE and KE are sampled every energy_every steps.  After the call x, v and F are
  * synchronised at the final step (velocities at full step).
- * Asynchronous in graph mode under the fixed schedule (rebuild_check = 0): the call returns
+ * Asynchronous in graph mode (either rebuild policy): the call returns
  * once its steps are queued on the stream, and the host reads its outcome (rebuild steps,
  * energy samples, capacity aborts, error flags) when the NEXT ljmd_step call has been
  * queued, or at the next call of any other function of this header that reads or changes
