@@ -1358,12 +1358,12 @@ constexpr int kRrStrideW = (16 * kRrCap + kRrOvf) / 2 + 8 + 1;
 constexpr size_t kRrSmem = sizeof(unsigned) * (size_t)kRrThreads * kRrStrideW;
 
 __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, int K, Geo g,
-                                                       const uint4* __restrict__ in,
+                                                       const uint4* in,
                                                        const int* __restrict__ ncount,
                                                        const int* __restrict__ ocell_of,
                                                        const int* __restrict__ obegin,
                                                        const int* __restrict__ tile_oc0,
-                                                       uint4* __restrict__ out, const DevCtl* ctl) {
+                                                       uint4* out, const DevCtl* ctl) {
     if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     extern __shared__ unsigned rr_smem[];
     const int tid = threadIdx.x;
@@ -1461,12 +1461,12 @@ constexpr size_t kRrSmem = sizeof(unsigned) * (size_t)kRrThreads * kRrStrideW;
 __device__ __forceinline__ unsigned nib(unsigned long long w, int r) { return (unsigned)(w >> (4 * r)) & 15u; }
 
 __global__ void __launch_bounds__(kRrThreads) k_list_rr(int n_own, int n_pad, int K, Geo g,
-                                                       const uint4* __restrict__ in,
+                                                       const uint4* in,
                                                        const int* __restrict__ ncount,
                                                        const int* __restrict__ ocell_of,
                                                        const int* __restrict__ obegin,
                                                        const int* __restrict__ tile_oc0,
-                                                       uint4* __restrict__ out, const DevCtl* ctl) {
+                                                       uint4* out, const DevCtl* ctl) {
     if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     extern __shared__ unsigned rr_smem[];
     const int tid = threadIdx.x;

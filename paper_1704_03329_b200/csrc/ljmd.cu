@@ -113,7 +113,6 @@ struct ljmd_ctx {
     int scan_tmp_n = 0;
     // ---- list
     uint4* nbr8 = nullptr;            // 16-bit tile-local indices in blocks of 8: [K/8][n_pad]
-    uint4* nbr8b = nullptr;           // the same, bank-aware order (what k_force reads)
     int bank_order = 1;               // 0: the force kernel walks the build order
     bool use_rr = false;              // the current list is in the bank-aware order
     double interval_ema = 0.0;        // steps a list has served, running estimate
@@ -605,7 +604,6 @@ ljmd_status alloc_slots(ljmd_ctx* c, int cap, bool keep_current) {
 ljmd_status alloc_list(ljmd_ctx* c, int K) {
     c->K = K;
     TRY(dalloc(c, &c->nbr8, (size_t)(K / 8) * c->n_pad));
-    TRY(dalloc(c, &c->nbr8b, (size_t)(K / 8) * c->n_pad));
     if (c->newton3) TRY(dalloc(c, &c->nbr8h, (size_t)(K / 8) * c->n_pad));
     return LJMD_OK;
 }
@@ -694,7 +692,7 @@ ForceArgs force_args(ljmd_ctx* c) {
     a.xp_next = c->xp[c->xc ^ 1];
     a.own_slot = c->own_slot;
     a.own_li = c->own_li;
-    a.nbr = c->use_rr ? c->nbr8b : c->nbr8;
+    a.nbr = c->nbr8;   // the last build's list, re-sequenced in place when use_rr
     a.ncount = c->ncount;
     a.fx = c->F;
     a.fy = c->F + c->own_cap;
@@ -1365,7 +1363,7 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
         CKL();
     } else if (c->use_rr) {
         k_list_rr<<<nblk(c->n_own, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
-            c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b, cctl(c));
+            c->n_own, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8, cctl(c));   // in place
         CKL();
     }
 
@@ -1399,7 +1397,7 @@ ljmd_status validate_step(ljmd_ctx* c, int vslot) {
     a.vcell = c->vcell;
     a.vbegin = c->vbegin;
     a.vpos = c->vpos;
-    a.nbr = reinterpret_cast<const unsigned short*>(c->use_rr ? c->nbr8b : c->nbr8);
+    a.nbr = reinterpret_cast<const unsigned short*>(c->nbr8);
     a.ncount = c->ncount;
     a.ocell_of = c->ocell_of;
     a.tr = TileRows{c->tr_begin, c->tr_off, c->tr_len};
@@ -1529,7 +1527,7 @@ ljmd_status rebuild_captured(ljmd_ctx* c) {
     CKL();
     if (c->use_rr) {
         k_list_rr<<<nblk(n, kRrThreads), kRrThreads, kRrSmem, c->stream>>>(
-            n, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8b, cctl(c));
+            n, c->n_pad, c->K, c->geo, c->nbr8, c->ncount, c->ocell_of, c->obegin, c->tile_oc0, c->nbr8, cctl(c));   // in place
         CKL();
     }
     return LJMD_OK;
@@ -1543,12 +1541,12 @@ ljmd_status rebuild_captured(ljmd_ctx* c) {
 // Small systems (several force CTAs per tile) keep the build order: their pair loops are
 // latency-bound, not shared-memory-bound, and the pass is a per-thread chain of ~5000
 // instructions (C1: 17.2 -> 16.7 us per MD step without it).
-void decide_list_order(ljmd_ctx* c) {
+void decide_list_order(ljmd_ctx* c, int64_t call) {
     if (c->interval_ema == 0.0) c->interval_ema = (double)c->opt.rebuild_every;
-    // the estimate as of the end of call ncalls - 2: known before call ncalls is queued also
-    // while the call before it is unsettled (deferred settlement), so the eager, synchronous
-    // graph and deferred paths take the same decision
-    const double e = c->ncalls >= 2 ? c->ema_after[(c->ncalls - 2) & 3] : (double)c->opt.rebuild_every;
+    // call k (or a new state before call k): the estimate as of the end of call k - 2, known
+    // before call k is queued also while call k - 1 is unsettled (deferred settlement), so the
+    // eager, synchronous-graph and deferred paths take the same decision
+    const double e = call >= 2 ? c->ema_after[(call - 2) & 3] : (double)c->opt.rebuild_every;
     c->use_rr = c->bank_order && e >= 10.0 && c->fparts == 1;
 }
 
@@ -1673,7 +1671,7 @@ ljmd_status load_state(ljmd_ctx* c, const double* pos, const double* vel, const 
     c->h_val.clear();
     c->last_build_step = -1;
     TRY(zero_async(c, c->d_st, sizeof(DevStats)));
-    decide_list_order(c);
+    decide_list_order(c, c->ncalls);
     TRY(rebuild(c));
     TRY(ensure_hist(c, 1));
     TRY(launch_force(c, true, kStore, false));
@@ -2425,7 +2423,7 @@ ljmd_status step_call(ljmd_ctx* c, int64_t nsteps, bool defer, int64_t call) {
         }
         CK(cudaMemsetAsync(c->vhist, 0, sizeof(int) * 2 * (size_t)nsteps, c->stream));
     }
-    decide_list_order(c);
+    decide_list_order(c, call);
     if (graph) return step_graph(c, nsteps, defer, call);   // settled there unless deferred
     TRY(kick_drift(c));
     TRY(step_eager(c, 1, nsteps, false));
@@ -2642,7 +2640,7 @@ void ljmd_destroy(ljmd_ctx* c) {
     void* ptrs[] = {c->x[0], c->x[1], c->xf, c->slot_gid, c->v[0], c->v[1], c->gid[0], c->gid[1],
                     c->own_slot, c->own_li, c->ocell_of, c->F, c->e, c->xbuild, c->xw, c->cell_of, c->rank_in, c->perm,
                     c->ocount, c->obegin, c->ecount, c->ebegin, c->ecell_src, c->gc_dst, c->gc_src, c->gc_shift,
-                    c->scan_tmp, c->nbr8, c->nbr8b, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin, c->ylo_f, c->zlo_f,
+                    c->scan_tmp, c->nbr8, c->ncount, c->oc_of_lex, c->lex_of_oc, c->tile_oc0, c->tr_begin, c->ylo_f, c->zlo_f,
                     c->tr_off, c->pe_part, c->ke_part, c->hist, c->d_fl, c->d_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
