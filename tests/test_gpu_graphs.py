@@ -124,3 +124,30 @@ def test_deferred_abort_with_queued_calls(eng):
     e = run(eng, pos, vel, box, calls, graphs=0)
     same(g, e)
     assert g["st"]["graph_aborts"] >= 1 and g["st"]["steps_done"] == sum(calls)
+
+
+def test_list_order_change_between_calls(eng):
+    """Under the displacement check the bank-aware list order is chosen per call from the
+    rebuild intervals (two calls back): a hot melt (rebuilds every few steps: build order)
+    followed by a cold state of the same particles (long intervals: bank-aware order) changes
+    the choice between calls without a rebuild in between.  Every force launch must read the
+    last build's list (the pass re-sequences it in place): graph (deferred) and eager runs agree
+    bit for bit and the energies stay finite."""
+    pos, vel, box = state(cells=32, sigma_d=0.05, t0=1.44)
+    cold = li.velocities(len(pos), 0.05)
+
+    def run(**kw):
+        with eng.LJMD(pos, vel, box, rebuild_check=1, **kw) as ctx:
+            for _ in range(3):
+                ctx.step(20)
+            ctx.set_state(ctx.positions(), cold)
+            for _ in range(6):
+                ctx.step(20)
+            return dict(x=ctx.positions(), v=ctx.velocities(), F=ctx.forces(), e=ctx.energy_history(),
+                        reb=ctx.rebuild_steps(), st=ctx.stats())
+
+    g = run(graphs=1)
+    e = run(graphs=0)
+    same(g, e)
+    assert np.isfinite(g["e"][0]).all() and np.isfinite(g["e"][1]).all()
+    assert np.isfinite(g["F"]).all()
