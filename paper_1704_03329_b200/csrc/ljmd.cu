@@ -182,6 +182,9 @@ struct ljmd_ctx {
     };
     std::map<std::string, GraphEntry> graphs;
     bool capturing = false;           // launches go into a graph being captured
+    bool spec = false;                // eager rebuild with device-side capacity checks (one host wait)
+    DevCtl* h_sctl = nullptr;         // mapped: its control
+    int64_t spec_aborts = 0;
     cudaStream_t cap_stream[3] = {nullptr, nullptr, nullptr};   // capture of nested rebuild bodies
     int64_t graph_calls = 0, graph_aborts = 0;
     int64_t rebuild_kernels = 0;      // kernels of one captured rebuild (for the launch count)
@@ -340,7 +343,9 @@ ljmd_status dalloc(ljmd_ctx* c, T** p, size_t n) {
 inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 // the control a captured rebuild's kernels check (skip after a failed capacity check)
-inline const DevCtl* cctl(const ljmd_ctx* c) { return c->capturing ? c->d_ctl : nullptr; }
+inline const DevCtl* cctl(const ljmd_ctx* c) { return (c->capturing || c->spec) ? c->d_ctl : nullptr; }
+// the rebuild's capacities are checked on the device (captured, or speculative eager)
+inline bool dev_caps(const ljmd_ctx* c) { return c->capturing || c->spec; }
 
 // exclusive scan of n ints: out[0..n) prefixes, out[n] = total
 ljmd_status scan(ljmd_ctx* c, const int* in, int n, int* out) {
@@ -1115,7 +1120,7 @@ ljmd_status refresh_ghosts(ljmd_ctx* c, bool at_build) {
 // CSR of the ghost images of every owned particle (written by the kernels that move it) and
 // the list of received-plane images; from the build-time ghost list
 ljmd_status build_images(ljmd_ctx* c) {
-    if (c->newton3 || (!c->capturing && c->n_gflat == 0)) {
+    if (c->newton3 || (!dev_caps(c) && c->n_gflat == 0)) {
         TRY(zero_async(c, c->img_off, sizeof(int) * ((size_t)c->n_own + 1)));
         return LJMD_OK;
     }
@@ -1123,9 +1128,9 @@ ljmd_status build_images(ljmd_ctx* c) {
     CKL();
     TRY(zero_async(c, c->img_cnt, sizeof(int) * (size_t)c->n_own));
     // captured: the ghost count is only known on the device (grid over the slot capacity)
-    const int ng = c->capturing ? c->slot_cap : c->n_gflat;
-    const int* ndev = c->capturing ? &c->d_fl->n_gflat : nullptr;
-    const int nsl = c->capturing ? INT_MAX : c->n_slots;   // single rank: every source is local
+    const int ng = dev_caps(c) ? c->slot_cap : c->n_gflat;
+    const int* ndev = dev_caps(c) ? &c->d_fl->n_gflat : nullptr;
+    const int nsl = dev_caps(c) ? INT_MAX : c->n_slots;   // single rank: every source is local
     k_img_build<false><<<nblk(ng, 256), 256, 0, c->stream>>>(ng, c->gflat, nsl, c->slot2t, c->img_cnt, c->img_off,
                                                              c->img, c->grecv, c->d_fl, ndev, cctl(c));
     CKL();
@@ -1183,6 +1188,14 @@ ljmd_status migrate(ljmd_ctx* c) {
 
 // Cell binning (counting sort + gid order), ghost images and the Verlet list
 // (Sec. 3.4; IntegratorRange rebuild).
+ljmd_status rebuild_dev_body(ljmd_ctx* c);
+
+// the eager rebuild may run speculatively (one rank, no Newton-3 half list / DSL data hooks)
+bool spec_ok(const ljmd_ctx* c) {
+    return !c->split && !c->newton3 && !c->dsl_on && c->stage_cap > 0 && !c->capturing &&
+           getenv_int("LJMD_SPEC_REBUILD", 1) != 0;
+}
+
 ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     // Bank-aware re-ordering costs about 1.4 force launches and saves about 13 % of each
     // launch it serves (C2: 225 us against 21 us per step), so it pays for lists that serve
@@ -1211,6 +1224,38 @@ ljmd_status rebuild(ljmd_ctx* c, bool danger = true) {
     (void)kRrMinSteps;   // the list order is chosen per ljmd_step call (decide_list_order)
     TRY(reset_flags(c));
     TRY(zero_async(c, c->ocount, sizeof(int) * c->n_ocell));
+    if (spec_ok(c)) {
+        // speculative: the captured rebuild's kernels (capacities checked on the device), one
+        // host wait at the end instead of three; a shortfall falls through to the sequence
+        // below, which regrows it (abort 1: nothing permuted; 2: the new layout is in place)
+        TRY(zero_async(c, c->d_ctl, offsetof(DevCtl, since)));
+        c->spec = true;
+        const ljmd_status r = rebuild_dev_body(c);
+        c->spec = false;
+        TRY(r);
+        TRY(to_host(c, c->h_slots, c->ebegin + c->n_ecell, sizeof(int)));
+        TRY(to_host(c, c->h_sctl, c->d_ctl, sizeof(DevCtl)));
+        TRY(sync_flags(c));
+        if (c->h_fl->nonfinite_gid != INT_MAX)
+            return set_err(c, LJMD_E_NONFINITE, "non-finite position or velocity at particle %d",
+                           c->h_fl->nonfinite_gid);
+        if (!c->h_sctl->abort) {
+            if (c->h_fl->overlap_pair != ~0ull)
+                return set_err(c, LJMD_E_OVERLAP, "particles %d and %d coincide (r^2 == 0)",
+                               (int)(c->h_fl->overlap_pair >> 32), (int)(c->h_fl->overlap_pair & 0xffffffffu));
+            c->n_slots = *c->h_slots;
+            c->max_staged = c->h_fl->max_staged;
+            c->n_gflat = c->h_fl->n_gflat;
+            c->n_grecv = c->h_fl->n_grecv;
+            c->max_nbr = c->h_fl->max_nbr;
+            c->total_nbr = c->h_fl->total_nbr;
+            return LJMD_OK;
+        }
+        ++c->spec_aborts;
+        TRY(zero_async(c, c->d_ctl, offsetof(DevCtl, since)));
+        TRY(reset_flags(c));
+        TRY(zero_async(c, c->ocount, sizeof(int) * c->n_ocell));
+    }
     // input of the binning: the current owned particles, or the post-migration compaction
     const double4* xin = c->x[c->xc];
     const int* slot_in = c->own_slot;
@@ -1487,12 +1532,19 @@ ljmd_status cond_if(ljmd_ctx* c, cudaStream_t body, Setter setter, Body fn) {
 // after the build); a failed check makes the rest return at entry.
 ljmd_status rebuild_captured(ljmd_ctx* c) {
     const int n = c->n_own;
-    const size_t oc = c->own_cap;
     k_maxdisp_z<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc ^ 1], c->own_slot, c->xbuild,
                                                      &c->d_st->disp_bits, c->ocount, c->n_ocell, c->d_ctl);
     CKL();
     k_dangerous_reset<<<1, 1, 0, c->stream>>>(c->d_st, c->opt.delta * c->opt.delta, c->d_fl, c->d_ctl);
     CKL();
+    return rebuild_dev_body(c);
+}
+
+// The rebuild from the binning on, capacities checked on the device (a failed check makes the
+// rest return at entry): the body of a captured rebuild and of the speculative eager one.
+ljmd_status rebuild_dev_body(ljmd_ctx* c) {
+    const int n = c->n_own;
+    const size_t oc = c->own_cap;
     k_wrap_bin<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc], c->own_slot, c->geo, c->xw, c->ocount, c->cell_of,
                                                     c->rank_in, c->gid[0], c->d_fl, c->v[0], c->v[1], c->gid[1],
                                                     (int)oc, c->d_ctl);
@@ -1919,7 +1971,8 @@ ljmd_status ljmd_init(ljmd_ctx** out, int64_t n, const double* pos, const double
         cudaMalloc(&c->d_st, sizeof(DevStats)) != cudaSuccess ||
         cudaHostAlloc(&c->h_st, sizeof(DevStats), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostAlloc(&c->h_fl, sizeof(DevFlags), cudaHostAllocMapped) != cudaSuccess ||
-        cudaHostAlloc(&c->h_slots, sizeof(int), cudaHostAllocMapped) != cudaSuccess) {
+        cudaHostAlloc(&c->h_slots, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostAlloc(&c->h_sctl, sizeof(DevCtl), cudaHostAllocMapped) != cudaSuccess) {
         set_err(c, LJMD_E_CUDA, "flag allocation failed");
         return fail(LJMD_E_CUDA);
     }
@@ -2676,6 +2729,7 @@ void ljmd_destroy(ljmd_ctx* c) {
     if (c->h_histm) cudaFreeHost(c->h_histm);
     if (c->h_init) cudaFreeHost(c->h_init);
     if (c->h_slots) cudaFreeHost(c->h_slots);
+    if (c->h_sctl) cudaFreeHost(c->h_sctl);
     for (auto e : c->ev) cudaEventDestroy(e);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);

@@ -151,3 +151,16 @@ def test_list_order_change_between_calls(eng):
     same(g, e)
     assert np.isfinite(g["e"][0]).all() and np.isfinite(g["e"][1]).all()
     assert np.isfinite(g["F"]).all()
+
+
+def test_speculative_eager_rebuild(eng, monkeypatch):
+    """The eager rebuild runs the captured rebuild's kernels with device-side capacity checks
+    and one host wait; a shortfall (tight_caps) falls back to the host-checked sequence, which
+    regrows it.  Bitwise the host-checked rebuild's trajectory (LJMD_SPEC_REBUILD=0)."""
+    pos, vel, box = state(sigma_d=0.0, t0=2.0)   # perfect FCC melting: the layout grows
+    calls = [20, 20, 20]
+    s = run(eng, pos, vel, box, calls, graphs=0, tight_caps=1)
+    monkeypatch.setenv("LJMD_SPEC_REBUILD", "0")
+    h = run(eng, pos, vel, box, calls, graphs=0, tight_caps=1)
+    same(s, h)
+    assert s["st"]["regrows"] >= 1
