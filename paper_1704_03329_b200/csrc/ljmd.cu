@@ -179,6 +179,7 @@ struct ljmd_ctx {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ex = nullptr;
         int64_t launches = 0;         // kernels outside the conditional rebuild bodies
+        int64_t body_k = 0;           // kernels of one conditional rebuild body
     };
     std::map<std::string, GraphEntry> graphs;
     bool capturing = false;           // launches go into a graph being captured
@@ -187,7 +188,6 @@ struct ljmd_ctx {
     int64_t spec_aborts = 0;
     cudaStream_t cap_stream[3] = {nullptr, nullptr, nullptr};   // capture of nested rebuild bodies
     int64_t graph_calls = 0, graph_aborts = 0;
-    int64_t rebuild_kernels = 0;      // kernels of one captured rebuild (for the launch count)
     int64_t call_nsamp = 0;           // energy samples of the current ljmd_step call
     // deferred settlement (graph mode, fixed rebuild schedule): ljmd_step returns once its
     // graph is queued; the host reads the call's control (k_call_out, two alternating mapped
@@ -195,7 +195,7 @@ struct ljmd_ctx {
     struct Pending {
         bool on = false;
         bool deferred = false;        // the host state was advanced at launch
-        int64_t step0 = 0, nsteps = 0, launches = 0, call = 0;
+        int64_t step0 = 0, nsteps = 0, launches = 0, body_k = 0, call = 0;
         int64_t sim_since = 0;        // fixed schedule: steps since the last rebuild at the end
         int xc0 = 0, buf = 0;
     };
@@ -2281,7 +2281,7 @@ ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) 
     ge.g = g;
     ge.ex = ex;
     ge.launches = (c->kernel_launches - k0) - nconds * body_k;   // without the conditional bodies
-    c->rebuild_kernels = body_k;
+    ge.body_k = body_k;
     c->kernel_launches = k0;   // counted per replay below
     return LJMD_OK;
 }
@@ -2300,7 +2300,7 @@ ljmd_status settle_call(ljmd_ctx* c, const ljmd_ctx::Pending& p, ljmd_ctx::Pendi
     }
     const CallOut o = *c->h_out[p.buf];
     const DevCtl& ctl = o.ctl;
-    c->kernel_launches += p.launches + (int64_t)ctl.nreb * c->rebuild_kernels;
+    c->kernel_launches += p.launches + (int64_t)ctl.nreb * p.body_k;
     for (int k = 0; k < ctl.nreb; ++k) {
         const int64_t st = p.step0 + c->h_orstep[p.buf][k];
         if (c->last_build_step >= 0 && st > c->last_build_step)
@@ -2403,15 +2403,30 @@ ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer, int64_t call) {
         c->rstep_cap = nsteps;
     }
     TRY(ensure_out(c, nsteps));
-    char key[160];
-    snprintf(key, sizeof key, "n%lld x%d s%lld e%lld c%d r%d", (long long)nsteps, c->xc,
-             check ? -1LL : (long long)c->since, ee > 0 ? (long long)(c->steps_done % ee) : 0LL, check ? 1 : 0,
-             c->use_rr ? 1 : 0);
+    auto key_of = [&](bool rr) {
+        char key[160];
+        snprintf(key, sizeof key, "n%lld x%d s%lld e%lld c%d r%d", (long long)nsteps, c->xc,
+                 check ? -1LL : (long long)c->since, ee > 0 ? (long long)(c->steps_done % ee) : 0LL, check ? 1 : 0,
+                 rr ? 1 : 0);
+        return std::string(key);
+    };
+    const std::string key = key_of(c->use_rr);
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
         ljmd_ctx::GraphEntry ge;
         TRY(capture_call(c, nsteps, ge));
         it = c->graphs.emplace(key, ge).first;
+        // the displacement check's list order can change from call to call (decide_list_order):
+        // the other variant is captured now as well, so a later change costs no capture
+        if (check && c->bank_order && c->fparts == 1 && !c->graphs.count(key_of(!c->use_rr))) {
+            c->use_rr = !c->use_rr;
+            ljmd_ctx::GraphEntry g2;
+            const ljmd_status r = capture_call(c, nsteps, g2);
+            c->use_rr = !c->use_rr;
+            TRY(r);
+            c->graphs.emplace(key_of(!c->use_rr), g2);
+            it = c->graphs.find(key);
+        }
     }
     ljmd_ctx::Pending p;
     p.on = true;
@@ -2419,6 +2434,7 @@ ljmd_status step_graph(ljmd_ctx* c, int64_t nsteps, bool defer, int64_t call) {
     p.nsteps = nsteps;
     p.xc0 = c->xc;
     p.launches = it->second.launches;
+    p.body_k = it->second.body_k;
     p.buf = c->out_next;
     p.call = call;
     c->out_next ^= 1;
