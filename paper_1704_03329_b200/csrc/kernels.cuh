@@ -318,8 +318,10 @@ __global__ void __launch_bounds__(1024) k_bin_offsets_single(const int* __restri
                                                             int* __restrict__ obegin, int n_ecell,
                                                             const int* __restrict__ ecell_src,
                                                             const int* __restrict__ recv_cnt,
-                                                            int* __restrict__ ecount, int* __restrict__ ebegin) {
+                                                            int* __restrict__ ecount, int* __restrict__ ebegin,
+                                                            DevCtl* ctl, int slot_cap) {
     __shared__ int sh[33];
+    if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     scan_single_block(ocount, n_ocell, obegin, sh);
     for (int ec = threadIdx.x; ec < n_ecell; ec += blockDim.x) {
         const int src = ecell_src[ec];
@@ -327,6 +329,11 @@ __global__ void __launch_bounds__(1024) k_bin_offsets_single(const int* __restri
     }
     __syncthreads();   // the block's ecount writes are visible to the whole block
     scan_single_block(ecount, n_ecell, ebegin, sh);
+    // device-checked rebuilds: k_check_caps' stage 1 (the slot count) folded in
+    if (ctl && threadIdx.x == 0 && ebegin[n_ecell] > slot_cap) {
+        ctl->abort = 1;
+        if (ctl->abort_step == 0) ctl->abort_step = ctl->step;
+    }
 }
 
 __global__ void __launch_bounds__(1024) k_scan_single(const int* __restrict__ in, int n, int* __restrict__ out) {
@@ -695,10 +702,15 @@ __global__ void k_xp_from_x(int b0, int n0, int b1, int n1, const double4* __res
     st_packed(xp, sl, ld256(x + sl));
 }
 
-__global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __restrict__ slot2t, const DevCtl* ctl) {
+// also clears the image counts of k_img_build (one memset node fewer)
+__global__ void k_slot2t(int n_own, const int* __restrict__ own_slot, int* __restrict__ slot2t, int* __restrict__ img_cnt,
+                         const DevCtl* ctl) {
     if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < n_own) slot2t[own_slot[t]] = t;
+    if (t < n_own) {
+        slot2t[own_slot[t]] = t;
+        img_cnt[t] = 0;
+    }
 }
 
 // FILL = false: count the images of each owned source (and move received-plane images to
@@ -2234,11 +2246,20 @@ struct DevStats {                  // persistent device counters (not reset by k
 
 // captured rebuilds: k_maxdisp also clears the owned-cell counts for the binning (one
 // memset node fewer)
+// record_step > 0 (the fixed schedule's captured rebuild): also k_decide's record of the
+// rebuild step (one node fewer)
 __global__ void k_maxdisp_z(int n_own, const double4* __restrict__ xprev, const int* __restrict__ own_slot,
                             const double4* __restrict__ xbuild, unsigned long long* __restrict__ out,
-                            int* __restrict__ ocount, int n_ocell, const DevCtl* ctl) {
+                            int* __restrict__ ocount, int n_ocell, DevCtl* ctl, DevFlags* fl, int* rstep,
+                            int record_step) {
     if (ctl && ctl->abort) return;   // captured rebuild after a failed capacity check
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (record_step > 0 && t == 0) {
+        ctl->step = record_step;
+        ctl->since = 0;
+        fl->maxdisp2 = 0ull;
+        rstep[ctl->nreb++] = record_step;
+    }
     for (int i = t; i < n_ocell; i += gridDim.x * blockDim.x) ocount[i] = 0;
     unsigned long long bits = 0ull;
     if (t < n_own) {

@@ -371,7 +371,8 @@ ljmd_status scan(ljmd_ctx* c, const int* in, int n, int* out) {
 ljmd_status bin_offsets(ljmd_ctx* c) {
     if (c->n_ocell <= kScanSingle && c->n_ecell <= kScanSingle) {   // small systems: one launch
         k_bin_offsets_single<<<1, 1024, 0, c->stream>>>(c->ocount, c->n_ocell, c->obegin, c->n_ecell, c->ecell_src,
-                                                       c->recv_cnt, c->ecount, c->ebegin);
+                                                       c->recv_cnt, c->ecount, c->ebegin,
+                                                       const_cast<DevCtl*>(cctl(c)), c->slot_cap);
         CKL();
         return LJMD_OK;
     }
@@ -1124,9 +1125,8 @@ ljmd_status build_images(ljmd_ctx* c) {
         TRY(zero_async(c, c->img_off, sizeof(int) * ((size_t)c->n_own + 1)));
         return LJMD_OK;
     }
-    k_slot2t<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->own_slot, c->slot2t, cctl(c));
+    k_slot2t<<<nblk(c->n_own, 256), 256, 0, c->stream>>>(c->n_own, c->own_slot, c->slot2t, c->img_cnt, cctl(c));
     CKL();
-    TRY(zero_async(c, c->img_cnt, sizeof(int) * (size_t)c->n_own));
     // captured: the ghost count is only known on the device (grid over the slot capacity)
     const int ng = dev_caps(c) ? c->slot_cap : c->n_gflat;
     const int* ndev = dev_caps(c) ? &c->d_fl->n_gflat : nullptr;
@@ -1530,10 +1530,12 @@ ljmd_status cond_if(ljmd_ctx* c, cudaStream_t body, Setter setter, Body fn) {
 // kernels without its host synchronisations, capacities checked on the device in three
 // stages (slots before anything is permuted; staging after the tile tables; list width
 // after the build); a failed check makes the rest return at entry.
-ljmd_status rebuild_captured(ljmd_ctx* c) {
+// record_step > 0: the fixed schedule's rebuild of that step (the decision record folded in)
+ljmd_status rebuild_captured(ljmd_ctx* c, int record_step) {
     const int n = c->n_own;
     k_maxdisp_z<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->x[c->xc ^ 1], c->own_slot, c->xbuild,
-                                                     &c->d_st->disp_bits, c->ocount, c->n_ocell, c->d_ctl);
+                                                     &c->d_st->disp_bits, c->ocount, c->n_ocell, c->d_ctl, c->d_fl,
+                                                     c->d_rstep, record_step);
     CKL();
     k_dangerous_reset<<<1, 1, 0, c->stream>>>(c->d_st, c->opt.delta * c->opt.delta, c->d_fl, c->d_ctl);
     CKL();
@@ -1557,8 +1559,10 @@ ljmd_status rebuild_dev_body(ljmd_ctx* c) {
     // stage 1 before anything is permuted; a failed check makes every later kernel of the
     // sequence return at entry (round 2: in-kernel checks instead of two nested conditional
     // nodes, whose body launches cost ~4 us each on the device timeline)
-    k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 1);
-    CKL();
+    if (!(c->n_ocell <= kScanSingle && c->n_ecell <= kScanSingle)) {   // else folded into the offsets
+        k_check_caps<<<1, 1, 0, c->stream>>>(ctl, fl, need, slot_cap, stage_cap, K, 1);
+        CKL();
+    }
     k_scatter<<<nblk(n, 256), 256, 0, c->stream>>>(n, c->cell_of, c->rank_in, c->obegin, c->perm, cctl(c));
     CKL();
     double* vo = c->v[1];
@@ -2235,11 +2239,9 @@ ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) 
             }
             if (forced) {
                 // the fixed schedule's rebuild: no conditional node (its kernels skip themselves
-                // after an abort), only the decision record; counted in the graph's launches
-                k_decide<<<1, 1, 0, c->stream>>>(c->d_ctl, c->d_fl, ns, 0, 1, delta2, c->d_rstep, (int)s,
-                                                cudaGraphConditionalHandle{}, 0);
-                CKL();
-                TRY(rebuild_captured(c));
+                // after an abort), the decision record in its first kernel; counted in the
+                // graph's launches
+                TRY(rebuild_captured(c, (int)s));
                 c->pdl_ok = false;   // the force after the rebuild reads the new list
             } else if (cond) {
                 const int64_t kb = c->kernel_launches;
@@ -2249,7 +2251,7 @@ ljmd_status capture_call(ljmd_ctx* c, int64_t nsteps, ljmd_ctx::GraphEntry& ge) 
                         k_decide<<<1, 1, 0, c->stream>>>(c->d_ctl, c->d_fl, ns, check ? 1 : 0, 0, delta2,
                                                         c->d_rstep, (int)s, h, 1);
                     },
-                    [&]() { return rebuild_captured(c); }));
+                    [&]() { return rebuild_captured(c, 0); }));
                 body_k = c->kernel_launches - kb - 1;
                 ++nconds;
                 c->pdl_ok = false;   // the force after the rebuild node reads the new list
